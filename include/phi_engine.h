@@ -1,0 +1,169 @@
+/*
+ * phi_engine.h -- C ABI of the B200 engine for the time-stepping operator Phi
+ * of MGRIT + p-multigrid (arXiv 2107.05337 reference code `miga`,
+ * /root/reference/proj/include/miga).
+ *
+ * Plain C: opaque handles, int32 indices, fp64 values, no torch types.  Every
+ * entry point cites the reference interface it replaces.  All compute runs on
+ * the GPU (sm_100a); there is no CPU fallback -- a missing device returns
+ * PHI_ERR_CUDA.
+ *
+ * Status codes: 0 ok, 1 invalid argument (std::invalid_argument in the
+ * reference), 2 non-convergence (std::runtime_error "spatial solve did not
+ * converge ..."), 3 CUDA failure, 4 other runtime error (zero pivot, singular
+ * coarse matrix ...).  phi_last_error() returns the thread-local message,
+ * worded as the reference's exception text.
+ */
+#ifndef PHI_ENGINE_H
+#define PHI_ENGINE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHI_OK 0
+#define PHI_ERR_INVALID 1
+#define PHI_ERR_NOT_CONVERGED 2
+#define PHI_ERR_CUDA 3
+#define PHI_ERR_RUNTIME 4
+
+/* source / initial-condition kinds (the reference takes std::function values,
+ * theta.hpp:17-48; the engine evaluates these named kinds on device) */
+#define PHI_SOURCE_CONSTANT 0  /* SourceTerm::constant(param); 0 -> zero source */
+#define PHI_SOURCE_SIN_EXP 1   /* transient param * exp(-t) * sin(pi x) sin(pi y) */
+#define PHI_SOURCE_SIN 2       /* steady    param * sin(pi x) sin(pi y)           */
+#define PHI_INIT_ZERO 0        /* ProblemSpec::initial empty                       */
+#define PHI_INIT_SIN 1         /* sin(pi x) sin(pi y), L2-projected                */
+#define PHI_INIT_COEFFS 2      /* spline sum_i c_i phi_i (free dofs), L2-projected */
+
+typedef struct phi_disc phi_disc;
+typedef struct phi_hier phi_hier;
+typedef struct phi_stepper phi_stepper;
+typedef struct phi_mgrit phi_mgrit;
+
+/* PMultigridOptions, pmultigrid.hpp:161-168 */
+typedef struct {
+    double ilut_tau; /* 1e-13 */
+    int ilut_fill;   /* 0 = average row fill */
+    int nu_pre, nu_post, gs_pre, gs_post;
+} phi_pmg_options;
+
+/* SpatialSolverConfig, theta.hpp:66-75 (p-multigrid kind) */
+typedef struct {
+    double rel_tol; /* 1e-12 */
+    int max_iter;   /* 400 */
+    int fixed_cycles;
+    phi_pmg_options pmg;
+} phi_solver_config;
+
+/* MgritConfig, mgrit.hpp:17-31 (workers replaced by the device batch) */
+typedef struct {
+    int cycle; /* 0 V, 1 F, 2 two-level */
+    int relax; /* 0 F, 1 FCF */
+    int m;
+    double halt_tol;
+    int max_iter;
+    int coarse_floor;
+} phi_mgrit_config;
+
+/* ProblemSpec, theta.hpp:42-62 (unit square; degree / mesh come from the disc) */
+typedef struct {
+    double kappa, t_final, theta;
+    int n_time_steps;
+    int source_kind;
+    double source_param;
+    int init_kind;
+    const double* init_coeffs; /* n_free, PHI_INIT_COEFFS only */
+    const double* load_terms;  /* optional caller load schedule: steps x n_free, or n_free if steady */
+    int load_terms_steady;
+} phi_problem;
+
+/* MgritResult, mgrit.hpp:33-42 (trajectory via phi_mgrit_trajectory) */
+typedef struct {
+    int iterations;
+    int converged;
+    double g_norm;
+    double final_relative_residual;
+    long long total_spatial_solves;
+    double mean_spatial_iterations;
+} phi_mgrit_result;
+
+const char* phi_last_error(void);
+void phi_default_solver_config(phi_solver_config* cfg);
+void phi_default_mgrit_config(phi_mgrit_config* cfg);
+void phi_default_problem(phi_problem* ps);
+int phi_device_count(void);
+int phi_set_device(int device);
+int phi_synchronize(void);
+
+/* ---- SpatialDiscretization::build (pmultigrid.hpp:94-158), unit square ---- */
+int phi_disc_build(int degree, int mesh_exponent, phi_disc** out);
+void phi_disc_free(phi_disc* d);
+/* info: [n_free_p, n_free_1, n_h_levels, n_elements, degree] */
+int phi_disc_info(const phi_disc* d, int* info);
+/* selectors as the reference fields: 0 mass_p, 1 stiff_p, 2 transfer_p1,
+ * 100+l h_chain[l].mass, 200+l h_chain[l].stiff, 300+l h_chain[l].embed.
+ * Two-pass: call with null arrays for the sizes. */
+int phi_disc_export(const phi_disc* d, int which, int* n_rows, int* n_cols, int* nnz, int* row_offsets,
+                    int* col_indices, double* values);
+/* 0 inv_lumped_p, 1 inv_lumped_1 */
+int phi_disc_vector(const phi_disc* d, int which, double* out);
+
+/* ---- PMultigridHierarchy(disc, c, opt) (pmultigrid.hpp:217-224) ---------- */
+int phi_hier_create(const phi_disc* d, double c, const phi_pmg_options* opt, phi_hier** out);
+void phi_hier_free(phi_hier* h);
+/* 0 op() = A_p, 1 smoother().lower, 2 smoother().upper, 100+l a_h[l] */
+int phi_hier_export(const phi_hier* h, int which, int* n_rows, int* n_cols, int* nnz, int* row_offsets,
+                    int* col_indices, double* values);
+/* vcycle(b, x) (pmultigrid.hpp:256) on nrhs vectors with stride ld.
+ * device_ptrs = 0: host arrays (copied in/out); 1: device arrays. */
+int phi_hier_vcycle(phi_hier* h, const double* b, double* x, int nrhs, long long ld, int device_ptrs);
+/* solve(b, x0, rel_tol, max_iter, fixed_cycles) (pmultigrid.hpp:271-307) per rhs;
+ * x holds x0 on entry (ignored if x0_empty) and the solution on exit.
+ * iters / converged / final_rel: nrhs entries each (host, nullable). */
+int phi_hier_solve(phi_hier* h, const double* b, double* x, int nrhs, long long ld, double rel_tol,
+                   int max_iter, int fixed_cycles, int x0_empty, int* iters, int* converged,
+                   double* final_rel, int device_ptrs);
+/* Building blocks for parity tests (single vector, host arrays):
+ * op 0 y = A_p x; 1 z = ilut_apply(r); 2 r1 = restrict_to_linear(r);
+ * 3 x += prolong_from_linear(e1) (x in/out); 4 x1 = hmg_wcycle(b1, x1);
+ * 5 x = gauss_seidel_sweep(a_h[arg], b, x, arg2 ? backward : forward) */
+int phi_hier_unit(phi_hier* h, int op, int arg, int arg2, const double* in, int n_in, double* out,
+                  int n_out);
+
+/* ---- ThetaStepper (theta.hpp:92-146) ----------------------------------- */
+int phi_stepper_create(const phi_disc* d, double kappa, double dt, double theta,
+                       const phi_solver_config* cfg, phi_stepper** out);
+void phi_stepper_free(phi_stepper* s);
+/* step(u_prev, load, guess) for nrhs states (theta.hpp:132-137): x holds the
+ * guess on entry (ignored if guess_empty) and Phi(u_prev) + ... on exit;
+ * load may be null. Non-convergence of any rhs returns PHI_ERR_NOT_CONVERGED. */
+int phi_stepper_step(phi_stepper* s, const double* u_prev, const double* load, double* x, int nrhs,
+                     long long ld, int guess_empty, int* iters, int device_ptrs);
+/* sequential_integrate (theta.hpp:216-237) with a given projected u0 and an
+ * optional load schedule (steps x n, or n if steady). traj: (nt+1) x n host. */
+int phi_sequential_integrate(phi_stepper* s, int nt, const double* u0, const double* loads, int load_steady,
+                             double* traj, long long* solves, long long* iterations);
+
+/* ---- MgritSolver (mgrit.hpp:50-331) ------------------------------------ */
+int phi_mgrit_create(const phi_disc* d, const phi_problem* ps, const phi_mgrit_config* cfg,
+                     const phi_solver_config* scfg, phi_mgrit** out);
+void phi_mgrit_free(phi_mgrit* g);
+int phi_mgrit_levels(const phi_mgrit* g, int* steps, double* dts);
+/* solve() (mgrit.hpp:93-118); history: residual_history (nullable, cap entries) */
+int phi_mgrit_solve(phi_mgrit* g, phi_mgrit_result* res, double* history, int history_cap);
+/* level-0 free-dof trajectory after solve(): (steps+1) x n_free, host */
+int phi_mgrit_trajectory(const phi_mgrit* g, double* out);
+/* projected initial condition of the last initialize() (n_free) */
+int phi_mgrit_initial(const phi_mgrit* g, double* out);
+/* Phase-level entry points (for the time-sharded multi-GPU driver and tests) */
+int phi_mgrit_initialize(phi_mgrit* g, double* g_norm);
+int phi_mgrit_cycle(phi_mgrit* g, int level);
+int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out);
+/* kernel launches issued by the last solve() (bench evidence) */
+long long phi_mgrit_launches(const phi_mgrit* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,79 @@
+"""Build the engine shared library in-tree (nvcc / g++, no JIT cache).
+
+    python -m paper_2107_05337_b200.build
+
+Produces ``paper_2107_05337_b200/_lib/libphi_engine.so`` for sm_100a.  CUDA
+sources are compiled with ``-fmad=false`` and host sources with
+``-ffp-contract=off``: the engine reproduces the reference's (non-fused)
+floating-point evaluation order, which is what makes its results
+bit-identical to the CPU reference on identical inputs.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT_DIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(OUT_DIR, "libphi_engine.so")
+ROOT = os.path.dirname(HERE)
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_INC = "/usr/local/cuda/include"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
+                     "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-unused-function",
+             f"-I{CUDA_INC}"]
+
+CU = ["phi_kernels.cu", "assembly.cu"]
+CPP = ["setup_host.cpp", "engine.cpp", "capi.cpp"]
+HEADERS = ["common.hpp", "device_types.cuh", "phi_kernels.cuh", "setup_host.hpp", "engine.hpp"]
+
+
+def _newer(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str], log: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    log.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(cmd[:3])} ...")
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "phi_engine.h")]
+    objs, log, changed = [], [], False
+    for src in CU:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OUT_DIR, "obj", src + ".o")
+        if _newer(o, [s] + hdrs):
+            _run([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], log)
+            changed = True
+        objs.append(o)
+    for src in CPP:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OUT_DIR, "obj", src + ".o")
+        if _newer(o, [s] + hdrs):
+            _run(["g++"] + CXX_FLAGS + ["-c", s, "-o", o], log)
+            changed = True
+        objs.append(o)
+    if changed or _newer(LIB, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"], log)
+    with open(os.path.join(OUT_DIR, "build.log"), "w") as f:
+        f.write("\n".join(log))
+    if verbose:
+        print("\n".join(log))
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

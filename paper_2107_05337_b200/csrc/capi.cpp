@@ -1,0 +1,550 @@
+// extern "C" boundary of the engine (include/phi_engine.h).  Maps the
+// reference's exception types onto status codes and keeps the message
+// thread-local, worded as the reference's exception text.
+#include <climits>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/phi_engine.h"
+#include "engine.hpp"
+
+using namespace phi;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PHI_OK;
+    } catch (const InvalidArgument& e) {
+        g_err = e.what();
+        return PHI_ERR_INVALID;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return PHI_ERR_INVALID;
+    } catch (const NotConverged& e) {
+        g_err = e.what();
+        return PHI_ERR_NOT_CONVERGED;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return PHI_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PHI_ERR_RUNTIME;
+    }
+}
+
+int export_csr(const HostCsr& a, int* n_rows, int* n_cols, int* nnz, int* ro, int* ci, double* v) {
+    if (n_rows) *n_rows = a.n_rows;
+    if (n_cols) *n_cols = a.n_cols;
+    if (nnz) *nnz = a.nnz();
+    if (ro) std::memcpy(ro, a.row_offsets.data(), sizeof(int) * (a.n_rows + 1));
+    if (ci) std::memcpy(ci, a.col_indices.data(), sizeof(int) * a.nnz());
+    if (v) std::memcpy(v, a.values.data(), sizeof(double) * a.nnz());
+    return PHI_OK;
+}
+
+HierOptions to_opts(const phi_pmg_options* o) {
+    HierOptions h;
+    if (o) {
+        h.ilut_tau = o->ilut_tau;
+        h.ilut_fill = o->ilut_fill;
+        h.nu_pre = o->nu_pre;
+        h.nu_post = o->nu_post;
+        h.gs_pre = o->gs_pre;
+        h.gs_post = o->gs_post;
+    }
+    return h;
+}
+
+SolverConfig to_cfg(const phi_solver_config* c) {
+    SolverConfig s;
+    if (c) {
+        s.rel_tol = c->rel_tol;
+        s.max_iter = c->max_iter;
+        s.fixed_cycles = c->fixed_cycles;
+        s.pmg = to_opts(&c->pmg);
+    }
+    return s;
+}
+
+void require_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw CudaError(std::string("no CUDA device available (the engine has no CPU path): ") +
+                        cudaGetErrorString(e));
+}
+
+/// Staging of host or device batch arrays (nrhs vectors, stride ld).
+struct Batch {
+    DevBuf<double> buf;
+    double* ptr = nullptr;
+    long long ld = 0;
+    void in(const double* src, int nrhs, long long ld_, int n, int device_ptrs, cudaStream_t s) {
+        if (!src) {
+            ptr = nullptr;
+            return;
+        }
+        if (device_ptrs) {
+            ptr = const_cast<double*>(src);
+            ld = ld_;
+            return;
+        }
+        buf.alloc((size_t)nrhs * n);
+        for (int r = 0; r < nrhs; ++r)
+            PHI_CUDA(cudaMemcpyAsync(buf.get() + (size_t)r * n, src + (size_t)r * ld_, sizeof(double) * n,
+                                     cudaMemcpyHostToDevice, s));
+        ptr = buf.get();
+        ld = n;
+    }
+    void out(double* dst, int nrhs, long long ld_, int n, int device_ptrs, cudaStream_t s) {
+        if (device_ptrs) return;
+        for (int r = 0; r < nrhs; ++r)
+            PHI_CUDA(cudaMemcpyAsync(dst + (size_t)r * ld_, buf.get() + (size_t)r * n, sizeof(double) * n,
+                                     cudaMemcpyDeviceToHost, s));
+    }
+};
+
+}  // namespace
+
+struct phi_disc {
+    std::shared_ptr<Disc> d;
+    HostCsr csr_cache(int which) const {
+        if (which == 0) return d->to_csr(d->M);
+        if (which == 1) return d->to_csr(d->K);
+        if (which == 2) return d->to_csr(d->T);
+        if (which >= 100 && which < 200) return d->to_csr(d->h.at(which - 100).M);
+        if (which >= 200 && which < 300) return d->to_csr(d->h.at(which - 200).K);
+        if (which >= 300 && which < 400) {
+            const auto& hl = d->h.at(which - 300);
+            if (which - 300 + 1 >= (int)d->h.size()) throw InvalidArgument("embed: coarsest level has none");
+            return hl.E;
+        }
+        throw InvalidArgument("phi_disc_export: bad selector");
+    }
+};
+
+struct phi_hier {
+    std::unique_ptr<Hier> h;
+    Workspace ws;
+    cudaStream_t s = nullptr;
+};
+
+struct phi_stepper {
+    std::unique_ptr<Stepper> st;
+    Workspace ws;
+    DevBuf<int> iters, conv;
+    DevBuf<unsigned long long> stat;
+    DevBuf<int> err;
+    DevBuf<double> err_rel;
+    cudaStream_t s = nullptr;
+};
+
+struct phi_mgrit {
+    std::unique_ptr<Mgrit> g;
+};
+
+extern "C" {
+
+const char* phi_last_error(void) { return g_err.c_str(); }
+
+void phi_default_solver_config(phi_solver_config* c) {
+    c->rel_tol = 1e-12;
+    c->max_iter = 400;
+    c->fixed_cycles = 0;
+    c->pmg.ilut_tau = 1e-13;
+    c->pmg.ilut_fill = 0;
+    c->pmg.nu_pre = c->pmg.nu_post = 1;
+    c->pmg.gs_pre = c->pmg.gs_post = 2;
+}
+
+void phi_default_mgrit_config(phi_mgrit_config* c) {
+    c->cycle = 0;
+    c->relax = 1;
+    c->m = 2;
+    c->halt_tol = 1e-10;
+    c->max_iter = 50;
+    c->coarse_floor = 8;
+}
+
+void phi_default_problem(phi_problem* p) {
+    std::memset(p, 0, sizeof *p);
+    p->kappa = 1.0;
+    p->t_final = 0.1;
+    p->theta = 1.0;
+    p->n_time_steps = 64;
+    p->source_kind = PHI_SOURCE_CONSTANT;
+    p->source_param = 1.0;
+    p->init_kind = PHI_INIT_ZERO;
+}
+
+int phi_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int phi_set_device(int device) {
+    return guarded([&] { PHI_CUDA(cudaSetDevice(device)); });
+}
+
+int phi_synchronize(void) {
+    return guarded([&] { PHI_CUDA(cudaDeviceSynchronize()); });
+}
+
+// ---- disc -----------------------------------------------------------------
+int phi_disc_build(int degree, int mesh_exponent, phi_disc** out) {
+    return guarded([&] {
+        require_device();
+        auto* d = new phi_disc;
+        try {
+            d->d = Disc::build(degree, mesh_exponent);
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
+void phi_disc_free(phi_disc* d) { delete d; }
+
+int phi_disc_info(const phi_disc* d, int* info) {
+    return guarded([&] {
+        info[0] = d->d->n_p;
+        info[1] = d->d->n_1;
+        info[2] = (int)d->d->h.size();
+        info[3] = d->d->n_elements;
+        info[4] = d->d->degree;
+    });
+}
+
+int phi_disc_export(const phi_disc* d, int which, int* n_rows, int* n_cols, int* nnz, int* ro, int* ci,
+                    double* v) {
+    return guarded([&] { export_csr(d->csr_cache(which), n_rows, n_cols, nnz, ro, ci, v); });
+}
+
+int phi_disc_vector(const phi_disc* d, int which, double* out) {
+    return guarded([&] {
+        const auto& b = which == 0 ? d->d->inv_lp : d->d->inv_l1;
+        const auto h = b.download();
+        std::memcpy(out, h.data(), sizeof(double) * h.size());
+    });
+}
+
+// ---- hier -----------------------------------------------------------------
+int phi_hier_create(const phi_disc* d, double c, const phi_pmg_options* opt, phi_hier** out) {
+    return guarded([&] {
+        auto h = std::make_unique<phi_hier>();
+        h->h = std::make_unique<Hier>(d->d, c, to_opts(opt));
+        *out = h.release();
+    });
+}
+
+void phi_hier_free(phi_hier* h) { delete h; }
+
+int phi_hier_export(const phi_hier* h, int which, int* n_rows, int* n_cols, int* nnz, int* ro, int* ci,
+                    double* v) {
+    return guarded([&] {
+        if (which == 0)
+            export_csr(h->h->disc->to_csr(h->h->A), n_rows, n_cols, nnz, ro, ci, v);
+        else if (which == 1)
+            export_csr(h->h->L_host, n_rows, n_cols, nnz, ro, ci, v);
+        else if (which == 2)
+            export_csr(h->h->U_host, n_rows, n_cols, nnz, ro, ci, v);
+        else if (which >= 100 && which - 100 < (int)h->h->a_h.size())
+            export_csr(h->h->a_h_csr(which - 100), n_rows, n_cols, nnz, ro, ci, v);
+        else
+            throw InvalidArgument("phi_hier_export: bad selector");
+    });
+}
+
+int phi_hier_vcycle(phi_hier* h, const double* b, double* x, int nrhs, long long ld, int device_ptrs) {
+    return guarded([&] {
+        const int n = h->h->disc->n_p;
+        if (ld < n) throw InvalidArgument("vcycle: dimension mismatch");
+        SolverConfig cfg;
+        const DevHier H = h->h->view(cfg);
+        h->ws.ensure(H);
+        Batch bb, xb;
+        bb.in(b, nrhs, ld, n, device_ptrs, h->s);
+        xb.in(x, nrhs, ld, n, device_ptrs, h->s);
+        launch_vcycle(H, bb.ptr, bb.ld, xb.ptr, xb.ld, nrhs, h->ws.buf.get(), h->ws.stride, h->ws.slots, h->s);
+        xb.out(x, nrhs, ld, n, device_ptrs, h->s);
+        PHI_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int phi_hier_solve(phi_hier* h, const double* b, double* x, int nrhs, long long ld, double rel_tol,
+                   int max_iter, int fixed_cycles, int x0_empty, int* iters, int* converged, double* final_rel,
+                   int device_ptrs) {
+    return guarded([&] {
+        const int n = h->h->disc->n_p;
+        if (ld < n) throw InvalidArgument("solve: dimension mismatch");
+        SolverConfig cfg;
+        cfg.rel_tol = rel_tol;
+        cfg.max_iter = max_iter;
+        cfg.fixed_cycles = fixed_cycles;
+        const DevHier H = h->h->view(cfg);
+        h->ws.ensure(H);
+        Batch bb, xb;
+        bb.in(b, nrhs, ld, n, device_ptrs, h->s);
+        xb.in(x, nrhs, ld, n, device_ptrs, h->s);
+        DevBuf<int> it(nrhs), cv(nrhs);
+        DevBuf<double> fr(nrhs);
+        WaveArgs a{};
+        a.mode = kModeSolve;
+        a.epi = kEpiSolve;
+        a.n_tasks = nrhs;
+        a.task_len = 1;
+        a.n = n;
+        a.B = bb.ptr;
+        a.ldb = bb.ld;
+        a.X = xb.ptr;
+        a.ldx = xb.ld;
+        a.x0_empty = x0_empty;
+        a.iters_out = it.get();
+        a.conv_out = cv.get();
+        a.rel_out = fr.get();
+        launch_phi_wave(H, h->h->A.view(), a, h->ws.buf.get(), h->ws.stride, h->ws.slots, h->s);
+        xb.out(x, nrhs, ld, n, device_ptrs, h->s);
+        const auto hi = it.download(h->s);
+        const auto hc = cv.download(h->s);
+        const auto hf = fr.download(h->s);
+        for (int r = 0; r < nrhs; ++r) {
+            if (iters) iters[r] = hi[r];
+            if (converged) converged[r] = hc[r];
+            if (final_rel) final_rel[r] = hf[r];
+        }
+    });
+}
+
+int phi_hier_unit(phi_hier* h, int op, int arg, int arg2, const double* in, int n_in, double* out, int n_out) {
+    return guarded([&] {
+        SolverConfig cfg;
+        const DevHier H = h->h->view(cfg);
+        h->ws.ensure(H);
+        DevBuf<double> din(n_in), dout(n_out);
+        PHI_CUDA(cudaMemcpyAsync(din.get(), in, sizeof(double) * n_in, cudaMemcpyHostToDevice, h->s));
+        PHI_CUDA(cudaMemcpyAsync(dout.get(), out, sizeof(double) * n_out, cudaMemcpyHostToDevice, h->s));
+        launch_unit(H, op, arg, arg2, din.get(), dout.get(), h->ws.buf.get(), h->ws.stride, h->s);
+        PHI_CUDA(cudaMemcpyAsync(out, dout.get(), sizeof(double) * n_out, cudaMemcpyDeviceToHost, h->s));
+        PHI_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+// ---- stepper --------------------------------------------------------------
+int phi_stepper_create(const phi_disc* d, double kappa, double dt, double theta, const phi_solver_config* cfg,
+                       phi_stepper** out) {
+    return guarded([&] {
+        auto s = std::make_unique<phi_stepper>();
+        s->st = std::make_unique<Stepper>(d->d, kappa, dt, theta, to_cfg(cfg));
+        s->stat.alloc(2);
+        s->err.alloc(3);
+        s->err_rel.alloc(1);
+        *out = s.release();
+    });
+}
+
+void phi_stepper_free(phi_stepper* s) { delete s; }
+
+static void stepper_reset_err(phi_stepper* s) {
+    const std::vector<int> e0{0, INT_MAX, -1};
+    s->err.upload(e0, s->s);
+    s->stat.zero(s->s);
+}
+
+static void stepper_check(phi_stepper* s, const std::string& prefix) {
+    const auto e = s->err.download(s->s);
+    if (e[0]) {
+        const double rel = s->err_rel.download(s->s)[0];
+        throw NotConverged(prefix + "spatial solve did not converge (p-multigrid), residual " + std::to_string(rel));
+    }
+}
+
+int phi_stepper_step(phi_stepper* s, const double* u_prev, const double* load, double* x, int nrhs, long long ld,
+                     int guess_empty, int* iters, int device_ptrs) {
+    return guarded([&] {
+        const int n = s->st->disc->n_p;
+        if (ld < n) throw InvalidArgument("step: dimension mismatch");
+        s->ws.ensure(s->st->H);
+        stepper_reset_err(s);
+        Batch ub, lb, xb;
+        ub.in(u_prev, nrhs, ld, n, device_ptrs, s->s);
+        lb.in(load, nrhs, ld, n, device_ptrs, s->s);
+        xb.in(x, nrhs, ld, n, device_ptrs, s->s);
+        DevBuf<int> it(nrhs);
+        WaveArgs a{};
+        a.mode = kModeStep;
+        a.epi = kEpiSolve;
+        a.n_tasks = nrhs;
+        a.task_len = 1;
+        a.n = n;
+        a.UPREV = ub.ptr;
+        a.ldu = ub.ld;
+        a.LOADV = lb.ptr;
+        a.ldl = lb.ld;
+        a.X = xb.ptr;
+        a.ldx = xb.ld;
+        a.x0_empty = guess_empty;
+        a.iters_out = it.get();
+        a.stat = s->stat.get();
+        a.err = s->err.get();
+        a.err_rel = s->err_rel.get();
+        launch_phi_wave(s->st->H, s->st->Aminus.view(), a, s->ws.buf.get(), s->ws.stride, s->ws.slots, s->s);
+        xb.out(x, nrhs, ld, n, device_ptrs, s->s);
+        const auto hi = it.download(s->s);
+        if (iters)
+            for (int r = 0; r < nrhs; ++r) iters[r] = hi[r];
+        stepper_check(s, "");
+    });
+}
+
+int phi_sequential_integrate(phi_stepper* s, int nt, const double* u0, const double* loads, int load_steady,
+                             double* traj, long long* solves, long long* iterations) {
+    return guarded([&] {
+        const int n = s->st->disc->n_p;
+        if (nt < 1) throw InvalidArgument("ProblemSpec: nt must be >= 1");
+        s->ws.ensure(s->st->H);
+        stepper_reset_err(s);
+        DevBuf<double> U((size_t)(nt + 1) * n), L;
+        U.zero(s->s);
+        if (u0) PHI_CUDA(cudaMemcpyAsync(U.get(), u0, sizeof(double) * n, cudaMemcpyHostToDevice, s->s));
+        if (loads) {
+            const size_t cnt = load_steady ? (size_t)n : (size_t)n * nt;
+            L.alloc(cnt);
+            PHI_CUDA(cudaMemcpyAsync(L.get(), loads, sizeof(double) * cnt, cudaMemcpyHostToDevice, s->s));
+        }
+        const std::vector<int> k0{1};
+        DevBuf<int> dk0 = to_device(k0, s->s);
+        WaveArgs a{};
+        a.mode = kModeStep;
+        a.epi = kEpiStore;
+        a.n_tasks = 1;
+        a.task_len = nt;
+        a.task_k0 = dk0.get();
+        a.n = n;
+        a.U = U.get();
+        a.LOAD = loads ? L.get() : nullptr;
+        a.load_steady = load_steady;
+        a.guess_prev = 1;
+        a.stat = s->stat.get();
+        a.err = s->err.get();
+        a.err_rel = s->err_rel.get();
+        launch_phi_wave(s->st->H, s->st->Aminus.view(), a, s->ws.buf.get(), s->ws.stride, s->ws.slots, s->s);
+        PHI_CUDA(cudaMemcpyAsync(traj, U.get(), sizeof(double) * (size_t)(nt + 1) * n, cudaMemcpyDeviceToHost, s->s));
+        PHI_CUDA(cudaStreamSynchronize(s->s));
+        const auto st = s->stat.download(s->s);
+        if (solves) *solves = (long long)st[0];
+        if (iterations) *iterations = (long long)st[1];
+        const auto e = s->err.download(s->s);
+        if (e[0]) {
+            const double rel = s->err_rel.download(s->s)[0];
+            throw NotConverged("sequential_integrate: step " + std::to_string(e[1]) +
+                               ": spatial solve did not converge (p-multigrid), residual " + std::to_string(rel));
+        }
+    });
+}
+
+// ---- mgrit ----------------------------------------------------------------
+int phi_mgrit_create(const phi_disc* d, const phi_problem* ps, const phi_mgrit_config* cfg,
+                     const phi_solver_config* scfg, phi_mgrit** out) {
+    return guarded([&] {
+        ProblemOptions po;
+        po.kappa = ps->kappa;
+        po.t_final = ps->t_final;
+        po.theta = ps->theta;
+        po.n_time_steps = ps->n_time_steps;
+        po.source_kind = ps->source_kind;
+        po.source_param = ps->source_param;
+        po.init_kind = ps->init_kind;
+        const int n = d->d->n_p;
+        if (ps->init_kind == PHI_INIT_COEFFS) {
+            if (!ps->init_coeffs) throw InvalidArgument("init_coeffs missing");
+            po.init_coeffs.assign(ps->init_coeffs, ps->init_coeffs + n);
+        }
+        if (ps->load_terms) {
+            const size_t cnt = ps->load_terms_steady ? (size_t)n : (size_t)n * ps->n_time_steps;
+            po.load_terms.assign(ps->load_terms, ps->load_terms + cnt);
+            po.load_terms_steady = ps->load_terms_steady;
+        }
+        MgritOptions mo;
+        if (cfg) {
+            mo.cycle = cfg->cycle;
+            mo.relax = cfg->relax;
+            mo.m = cfg->m;
+            mo.halt_tol = cfg->halt_tol;
+            mo.max_iter = cfg->max_iter;
+            mo.coarse_floor = cfg->coarse_floor;
+        }
+        auto g = std::make_unique<phi_mgrit>();
+        g->g = std::make_unique<Mgrit>(d->d, po, mo, to_cfg(scfg));
+        *out = g.release();
+    });
+}
+
+void phi_mgrit_free(phi_mgrit* g) { delete g; }
+
+int phi_mgrit_levels(const phi_mgrit* g, int* steps, double* dts) {
+    const int L = g->g->n_levels();
+    for (int l = 0; l < L; ++l) {
+        if (steps) steps[l] = g->g->levels[l].steps;
+        if (dts) dts[l] = g->g->levels[l].dt;
+    }
+    return L;
+}
+
+int phi_mgrit_solve(phi_mgrit* g, phi_mgrit_result* res, double* history, int history_cap) {
+    return guarded([&] {
+        const MgritResultHost r = g->g->solve();
+        res->iterations = r.iterations;
+        res->converged = r.converged ? 1 : 0;
+        res->g_norm = r.g_norm;
+        res->final_relative_residual = r.final_relative_residual;
+        res->total_spatial_solves = r.total_spatial_solves;
+        res->mean_spatial_iterations = r.mean_spatial_iterations;
+        if (history)
+            for (int i = 0; i < (int)r.residual_history.size() && i < history_cap; ++i)
+                history[i] = r.residual_history[i];
+    });
+}
+
+int phi_mgrit_trajectory(const phi_mgrit* g, double* out) {
+    return guarded([&] {
+        const auto& lv = g->g->levels[0];
+        PHI_CUDA(cudaMemcpyAsync(out, lv.u.get(), sizeof(double) * lv.u.size(), cudaMemcpyDeviceToHost,
+                                 g->g->stream));
+        PHI_CUDA(cudaStreamSynchronize(g->g->stream));
+    });
+}
+
+int phi_mgrit_initial(const phi_mgrit* g, double* out) {
+    return guarded([&] {
+        const auto h = g->g->u0.download(g->g->stream);
+        std::memcpy(out, h.data(), sizeof(double) * h.size());
+    });
+}
+
+int phi_mgrit_initialize(phi_mgrit* g, double* g_norm) {
+    return guarded([&] {
+        g->g->initialize();
+        if (g_norm) *g_norm = g->g->g_norm;
+    });
+}
+
+int phi_mgrit_cycle(phi_mgrit* g, int level) {
+    return guarded([&] { g->g->mgrit_cycle(level); });
+}
+
+int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out) {
+    return guarded([&] { *out = g->g->residual_norm(level); });
+}
+
+long long phi_mgrit_launches(const phi_mgrit* g) { return g->g->launches; }
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+// Plain-old-data views of the device-resident operators, passed by value to the
+// kernels (they live in the kernel parameter bank: uniform, cached loads).
+#pragma once
+
+#include <cstdint>
+
+namespace phi {
+
+/// Tensor-product stencil operator ("blocked CSR" of a clamped-rectangle
+/// B-spline pattern, assembly.hpp:157-193 after Dirichlet elimination).
+/// Rows live on an ru x rv grid, columns on a cu x cv grid; row (iu, iv) holds
+/// columns (iu + du, iv + dv), du, dv in [lo, hi], clamped to the column grid.
+/// Column indices are implicit.  Values are stencil-major:
+///   vals[e * (ru*rv) + row],  e = (dv - lo) * (hi - lo + 1) + (du - lo)
+/// so a warp over consecutive rows reads one coalesced 256 B line per entry.
+/// The (dv, du)-ascending entry order is the reference CSR column order, so a
+/// sequential sum over e reproduces spmv (sparse.hpp:114-124) bit for bit.
+struct DevStencil {
+    int ru, rv, cu, cv, lo, hi;
+    const double* vals;
+};
+
+/// Generic CSR (sparse.hpp:17-22) -- used for the h-chain embeddings.
+struct DevCsr {
+    int n_rows, n_cols;
+    const int* ro;
+    const int* ci;
+    const double* v;
+};
+
+/// Level-scheduled, lane-interleaved triangular factor (see TriPlan).
+struct DevTri {
+    int n, n_levels;
+    const int* level_chunk;
+    const int* chunk_row0;
+    const int* chunk_nrows;
+    const int* chunk_base;
+    const int* rows;
+    const int* lens;
+    const int* cols;
+    const double* vals;
+    const double* diag;  // upper factor only
+};
+
+struct DevHLevel {
+    DevStencil a;    // M_l + c K_l, 9-point
+    DevCsr embed;    // level l+1 -> level l (empty on the coarsest)
+    DevCsr embed_t;  // its transpose (restriction rows, ascending fine index)
+    int n;
+};
+
+constexpr int kMaxH = 12;
+
+/// One p-multigrid hierarchy (PMultigridHierarchy, pmultigrid.hpp:215-324)
+/// plus the spatial solver settings of its ThetaStepper (theta.hpp:66-75).
+struct DevHier {
+    int n_p, n_1, n_h;
+    DevStencil A;   // A_p = M_p + c K_p
+    DevStencil T;   // transfer_p1 (rows order p, cols order 1)
+    DevStencil Tt;  // its transpose
+    const double* inv_lp;
+    const double* inv_l1;
+    DevTri L, U;
+    DevHLevel h[kMaxH];
+    const double* coarse_lu;
+    const int* coarse_piv;
+    int coarse_n;
+    int nu_pre, nu_post, gs_pre, gs_post;
+    double rel_tol;
+    int max_iter;
+    int fixed_cycles;
+};
+
+/// Work description of one batched wave of Phi applications (one CTA per
+/// right-hand side; see phi_kernels.cu).
+enum PhiMode : int { kModeStep = 0, kModeSolve = 1 };
+enum PhiEpi : int {
+    kEpiStore = 0,     // U[k] = x + g[k]                (step_into, mgrit.hpp:253-258)
+    kEpiRestrict = 1,  // CG[j] = x + g[k] - U[k]; CU[j] = 0   (mgrit.hpp:151-167)
+    kEpiResid = 2,     // SQ[k] = |x + g[k] - U[k]|^2          (mgrit.hpp:197-214)
+    kEpiNorm = 3,      // SQ[k] = |x|^2                        (mgrit.hpp:292-310)
+    kEpiSolve = 4      // X[task] = x                          (solve / step API)
+};
+
+struct WaveArgs {
+    int mode, epi;
+    int n_tasks, task_len;
+    const int* task_k0;  // per task: first time index k (step mode) or unused
+    int n;               // n_p
+    // level state, [k][n] row-major
+    double* U;
+    const double* G;
+    const double* LOAD;
+    int load_steady;
+    const double* AMINUS_X;  // unused placeholder
+    // restrict outputs
+    double* CG;
+    double* CU;
+    int m;
+    double* SQ;
+    // plain batched solve / step API (strided vectors)
+    const double* B;
+    long long ldb;
+    double* X;
+    long long ldx;
+    const double* UPREV;  // step API: u_prev rows
+    long long ldu;
+    const double* LOADV;  // step API: per-rhs load rows (nullable)
+    long long ldl;
+    int x0_empty;
+    int guess_prev;  // step mode on U: guess = U[k-1] (sequential_integrate) instead of U[k]
+    // per-task results (nullable)
+    int* iters_out;
+    int* conv_out;
+    double* rel_out;
+    // device counters
+    unsigned long long* stat;  // [0] solves, [1] iterations
+    int* err;                  // [0] flag, [1] first k, [2] level
+    double* err_rel;
+    int level;
+};
+
+}  // namespace phi

@@ -1,0 +1,584 @@
+// Host orchestration of the device engine (see engine.hpp).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <string>
+
+namespace phi {
+
+namespace {
+
+Tables1DDev upload_tables(const Tables1D& t, cudaStream_t s) {
+    Tables1DDev d;
+    d.host = t;
+    d.w.upload(t.weights, s);
+    d.vals.upload(t.vals, s);
+    d.ders.upload(t.ders, s);
+    return d;
+}
+
+void set_square(StencilBuf& a, int nr, int nc, int lo, int hi) {
+    a.ru = a.rv = nr;
+    a.cu = a.cv = nc;
+    a.lo = lo;
+    a.hi = hi;
+    a.vals.alloc(a.size());
+}
+
+HostCsr stencil_to_csr(const StencilBuf& a) {
+    const std::vector<double> v = a.vals.download();
+    HostCsr c;
+    c.n_rows = a.ru * a.rv;
+    c.n_cols = a.cu * a.cv;
+    const int w = a.hi - a.lo + 1;
+    const size_t n = a.n_rows();
+    for (int iv = 0; iv < a.rv; ++iv)
+        for (int iu = 0; iu < a.ru; ++iu) {
+            const int i = iu + a.ru * iv;
+            for (int dv = a.lo; dv <= a.hi; ++dv) {
+                if (iv + dv < 0 || iv + dv >= a.cv) continue;
+                for (int du = a.lo; du <= a.hi; ++du) {
+                    if (iu + du < 0 || iu + du >= a.cu) continue;
+                    c.col_indices.push_back((iu + du) + a.cu * (iv + dv));
+                    c.values.push_back(v[(size_t)((dv - a.lo) * w + (du - a.lo)) * n + i]);
+                }
+            }
+            c.row_offsets.push_back(c.nnz());
+        }
+    return c;
+}
+
+template <typename T>
+DevBuf<T> dev(const std::vector<T>& h, cudaStream_t s) {
+    DevBuf<T> d;
+    d.upload(h, s);
+    return d;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Disc
+// ---------------------------------------------------------------------------
+std::shared_ptr<Disc> Disc::build(int degree, int k, cudaStream_t s) {
+    if (degree < 1 || degree > 8) throw InvalidArgument("SpatialDiscretization: degree must be in [1, 8]");
+    if (k < 1) throw InvalidArgument("SpatialDiscretization: mesh exponent must be >= 1");
+    auto d = std::make_shared<Disc>();
+    d->degree = degree;
+    d->mesh_exponent = k;
+    d->n_elements = 1 << k;
+    const int nel = d->n_elements;
+    const int p = degree;
+
+    const Knots kvp = open_uniform_knots(p, nel);
+    d->tab_p = upload_tables(build_tables(kvp, p + 1), s);
+    d->nf_p = nel + p - 2;
+    d->n_p = d->nf_p * d->nf_p;
+    set_square(d->M, d->nf_p, d->nf_p, -p, p);
+    set_square(d->K, d->nf_p, d->nf_p, -p, p);
+    launch_assemble_mk(d->tab_p.view(), d->tab_p.view(), d->M.vals.get(), d->K.vals.get(), s);
+
+    // order-1 chain: halve while the mesh stays even and >= 8 (pmultigrid.hpp:119-133)
+    std::vector<Tables1DDev> tabs1;
+    int nl = nel;
+    for (;;) {
+        HLevel hl;
+        hl.n_elements = nl;
+        hl.nf = nl - 1;
+        hl.n = hl.nf * hl.nf;
+        tabs1.push_back(upload_tables(build_tables(open_uniform_knots(1, nl), 2), s));
+        set_square(hl.M, hl.nf, hl.nf, -1, 1);
+        set_square(hl.K, hl.nf, hl.nf, -1, 1);
+        launch_assemble_mk(tabs1.back().view(), tabs1.back().view(), hl.M.vals.get(), hl.K.vals.get(), s);
+        d->h.push_back(std::move(hl));
+        if (nl >= 8 && nl % 2 == 0)
+            nl /= 2;
+        else
+            break;
+    }
+    for (size_t l = 0; l + 1 < d->h.size(); ++l) {
+        HLevel& hl = d->h[l];
+        hl.E = p1_embedding_free(hl.n_elements);
+        hl.Et = transpose(hl.E);
+        hl.e_ro = dev(hl.E.row_offsets, s);
+        hl.e_ci = dev(hl.E.col_indices, s);
+        hl.e_v = dev(hl.E.values, s);
+        hl.et_ro = dev(hl.Et.row_offsets, s);
+        hl.et_ci = dev(hl.Et.col_indices, s);
+        hl.et_v = dev(hl.Et.values, s);
+    }
+    d->nf_1 = d->h[0].nf;
+    d->n_1 = d->h[0].n;
+
+    d->inv_lp.alloc(d->n_p);
+    d->inv_l1.alloc(d->n_1);
+    if (p == 1) {
+        // degenerate hierarchy: identity transfer, unit lumped masses (pmultigrid.hpp:139-143)
+        set_square(d->T, d->nf_p, d->nf_p, 0, 0);
+        set_square(d->Tt, d->nf_p, d->nf_p, 0, 0);
+        std::vector<double> ones(d->n_p, 1.0);
+        d->T.vals.upload(ones, s);
+        d->Tt.vals.upload(ones, s);
+        d->inv_lp.upload(ones, s);
+        d->inv_l1.upload(ones, s);
+    } else {
+        const LowTables lt = build_low_tables(open_uniform_knots(1, nel), d->tab_p.host);
+        DevBuf<double> low = dev(lt.vals, s);
+        set_square(d->T, d->nf_p, d->nf_1, -p, 1);
+        d->T.ru = d->T.rv = d->nf_p;
+        d->T.cu = d->T.cv = d->nf_1;
+        launch_assemble_transfer(d->tab_p.view(), d->tab_p.view(), low.get(), low.get(), d->T.vals.get(), s);
+        set_square(d->Tt, d->nf_1, d->nf_p, -1, p);
+        launch_stencil_transpose(d->T.view(), d->Tt.vals.get(), s);
+        DevBuf<int> bad(1);
+        bad.zero(s);
+        launch_lump_inv(d->M.vals.get(), p, nel, d->inv_lp.get(), bad.get(), s);
+        launch_lump_inv(d->h[0].M.vals.get(), 1, nel, d->inv_l1.get(), bad.get(), s);
+        if (bad.download(s)[0]) throw std::runtime_error("lump_mass: non-positive row sum");
+        PHI_CUDA(cudaStreamSynchronize(s));  // `low` goes out of scope
+    }
+
+    // sin(pi * node) at the order-p quadrature nodes, host libm (load assembly)
+    d->sin_host.resize(d->tab_p.host.nodes.size());
+    for (size_t i = 0; i < d->sin_host.size(); ++i) d->sin_host[i] = std::sin(M_PI * d->tab_p.host.nodes[i]);
+    d->sin_tab = dev(d->sin_host, s);
+    PHI_CUDA(cudaStreamSynchronize(s));
+    return d;
+}
+
+HostCsr Disc::to_csr(const StencilBuf& a) const { return stencil_to_csr(a); }
+
+void Disc::assemble_load(int kind, double c0, double c1, const double* coeffs_dev, double* out,
+                         cudaStream_t s) const {
+    launch_assemble_load(tab_p.view(), tab_p.view(), kind, c0, c1, sin_tab.get(), sin_tab.get(),
+                         coeffs_dev, out, s);
+}
+
+// ---------------------------------------------------------------------------
+// Hier
+// ---------------------------------------------------------------------------
+namespace {
+void upload_tri(const TriPlan& p, Hier::TriDev& d, cudaStream_t s) {
+    d.level_chunk = dev(p.level_chunk, s);
+    d.chunk_row0 = dev(p.chunk_row0, s);
+    d.chunk_nrows = dev(p.chunk_nrows, s);
+    d.chunk_base = dev(p.chunk_base, s);
+    d.rows = dev(p.rows, s);
+    d.lens = dev(p.lens, s);
+    d.cols = dev(p.cols.empty() ? std::vector<int>{0} : p.cols, s);
+    d.vals = dev(p.vals.empty() ? std::vector<double>{0.0} : p.vals, s);
+    if (!p.diag.empty()) d.diag = dev(p.diag, s);
+}
+DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
+    return DevTri{p.n, p.n_levels, d.level_chunk.get(), d.chunk_row0.get(), d.chunk_nrows.get(),
+                  d.chunk_base.get(), d.rows.get(), d.lens.get(), d.cols.get(), d.vals.get(), d.diag.get()};
+}
+}  // namespace
+
+Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_, cudaStream_t s)
+    : disc(std::move(disc_)), c(c_), opt(opt_) {
+    const Disc& d = *disc;
+    A.ru = A.rv = A.cu = A.cv = d.nf_p;
+    A.lo = d.M.lo;
+    A.hi = d.M.hi;
+    A.vals.alloc(A.size());
+    launch_axpby(d.M.vals.get(), c, d.K.vals.get(), A.vals.get(), A.size(), s);
+    const HostCsr ah = stencil_to_csr(A);
+    ilut_factor(ah, opt.ilut_tau, opt.ilut_fill, L_host, U_host);
+    Lp = plan_lower(L_host);
+    Up = plan_upper(U_host);
+    upload_tri(Lp, Ld, s);
+    upload_tri(Up, Ud, s);
+    for (const auto& hl : d.h) {
+        StencilBuf a;
+        a.ru = a.rv = a.cu = a.cv = hl.nf;
+        a.lo = -1;
+        a.hi = 1;
+        a.vals.alloc(a.size());
+        launch_axpby(hl.M.vals.get(), c, hl.K.vals.get(), a.vals.get(), a.size(), s);
+        a_h.push_back(std::move(a));
+    }
+    coarse = dense_lu_factor(stencil_to_csr(a_h.back()));
+    coarse_lu = dev(coarse.lu, s);
+    coarse_piv = dev(coarse.piv, s);
+    PHI_CUDA(cudaStreamSynchronize(s));
+}
+
+HostCsr Hier::a_h_csr(int l) const { return stencil_to_csr(a_h.at(l)); }
+
+DevHier Hier::view(const SolverConfig& cfg) const {
+    const Disc& d = *disc;
+    if ((int)d.h.size() > kMaxH) throw InvalidArgument("too many h-levels");
+    DevHier H{};
+    H.n_p = d.n_p;
+    H.n_1 = d.n_1;
+    H.n_h = (int)d.h.size();
+    H.A = A.view();
+    H.T = d.T.view();
+    H.Tt = d.Tt.view();
+    H.inv_lp = d.inv_lp.get();
+    H.inv_l1 = d.inv_l1.get();
+    H.L = tri_view(Lp, Ld);
+    H.U = tri_view(Up, Ud);
+    for (int l = 0; l < H.n_h; ++l) {
+        const auto& hl = d.h[l];
+        H.h[l].a = a_h[l].view();
+        H.h[l].n = hl.n;
+        if (l + 1 < H.n_h) {
+            H.h[l].embed = DevCsr{hl.E.n_rows, hl.E.n_cols, hl.e_ro.get(), hl.e_ci.get(), hl.e_v.get()};
+            H.h[l].embed_t = DevCsr{hl.Et.n_rows, hl.Et.n_cols, hl.et_ro.get(), hl.et_ci.get(), hl.et_v.get()};
+        }
+    }
+    H.coarse_lu = coarse_lu.get();
+    H.coarse_piv = coarse_piv.get();
+    H.coarse_n = coarse.n;
+    H.nu_pre = opt.nu_pre;
+    H.nu_post = opt.nu_post;
+    H.gs_pre = opt.gs_pre;
+    H.gs_post = opt.gs_post;
+    H.rel_tol = cfg.rel_tol;
+    H.max_iter = cfg.max_iter;
+    H.fixed_cycles = cfg.fixed_cycles;
+    return H;
+}
+
+void Workspace::ensure(const DevHier& H) {
+    const long long need = (long long)phi_ws_doubles(H);
+    const int want_slots = phi_max_slots(H);
+    if (need > stride || want_slots > slots) {
+        stride = std::max(stride, need);
+        slots = std::max(slots, want_slots);
+        buf.alloc((size_t)stride * slots);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stepper
+// ---------------------------------------------------------------------------
+Stepper::Stepper(std::shared_ptr<const Disc> disc_, double kappa_, double dt_, double theta_,
+                 const SolverConfig& cfg_, cudaStream_t s)
+    : disc(std::move(disc_)), kappa(kappa_), dt(dt_), theta(theta_), cfg(cfg_) {
+    hier = std::make_unique<Hier>(disc, kappa * dt * theta, cfg.pmg, s);
+    const Disc& d = *disc;
+    Aminus.ru = Aminus.rv = Aminus.cu = Aminus.cv = d.nf_p;
+    Aminus.lo = d.M.lo;
+    Aminus.hi = d.M.hi;
+    Aminus.vals.alloc(Aminus.size());
+    launch_axpby(d.M.vals.get(), -kappa * dt * (1.0 - theta), d.K.vals.get(), Aminus.vals.get(),
+                 Aminus.size(), s);
+    H = hier->view(cfg);
+    PHI_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+// Mgrit
+// ---------------------------------------------------------------------------
+Mgrit::Mgrit(std::shared_ptr<const Disc> disc_, const ProblemOptions& ps_, const MgritOptions& cfg_,
+             const SolverConfig& scfg_, cudaStream_t s)
+    : disc(std::move(disc_)), ps(ps_), cfg(cfg_), scfg(scfg_), stream(s) {
+    if (!(ps.kappa > 0.0)) throw InvalidArgument("ProblemSpec: kappa must be > 0");
+    if (!(ps.t_final > 0.0)) throw InvalidArgument("ProblemSpec: t_final must be > 0");
+    if (ps.n_time_steps < 1) throw InvalidArgument("ProblemSpec: nt must be >= 1");
+    if (!(ps.theta >= 0.0 && ps.theta <= 1.0)) throw InvalidArgument("ProblemSpec: theta must be in [0, 1]");
+    if (cfg.m < 2) throw InvalidArgument("MgritConfig: m must be >= 2");
+    if (cfg.max_iter < 1) throw InvalidArgument("MgritConfig: max_iter must be >= 1");
+    if (!(cfg.halt_tol > 0.0)) throw InvalidArgument("MgritConfig: tol must be > 0");
+    build_levels();
+    build_loads();
+    sq.alloc(levels[0].steps + 1);
+    stat.alloc(2);
+    err.alloc(3);
+    err_rel.alloc(1);
+    u0.alloc(disc->n_p);
+    for (auto& lv : levels) ws.ensure(lv.stepper->H);
+    PHI_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Mgrit::build_levels() {
+    const int m = cfg.m, nt = ps.n_time_steps;
+    if (nt >= m && nt % m != 0)
+        throw InvalidArgument("MGRIT: nt (" + std::to_string(nt) + ") not divisible by coarsening factor m (" +
+                              std::to_string(m) + ")");
+    std::vector<int> steps{nt};
+    for (;;) {
+        const int cur = steps.back();
+        if (cur % m != 0 || cur < m) break;
+        const int next = cur / m;
+        const bool first_coarse = steps.size() == 1;
+        if (!first_coarse && next + 1 <= cfg.coarse_floor) break;
+        steps.push_back(next);
+        if (cfg.cycle == 2) break;
+    }
+    const double dt0 = ps.t_final / nt;
+    const int n = disc->n_p;
+    levels.resize(steps.size());
+    for (size_t l = 0; l < steps.size(); ++l) {
+        Level& lv = levels[l];
+        lv.steps = steps[l];
+        lv.dt = dt0 * (nt / steps[l]);
+        lv.stepper = std::make_unique<Stepper>(disc, ps.kappa, lv.dt, ps.theta, scfg, stream);
+        lv.u.alloc((size_t)(lv.steps + 1) * n);
+        lv.g.alloc((size_t)(lv.steps + 1) * n);
+        const int J = lv.steps / m;
+        std::vector<int> kF(std::max(J, 1)), kR(std::max(J, 1)), kAll(std::max(lv.steps, 1));
+        for (int j = 0; j < J; ++j) {
+            kF[j] = j * m + 1;
+            kR[j] = (j + 1) * m;
+        }
+        for (int k = 1; k <= lv.steps; ++k) kAll[k - 1] = k;
+        lv.kF = dev(kF, stream);
+        lv.kR = dev(kR, stream);
+        lv.kAll = dev(kAll, stream);
+    }
+}
+
+void Mgrit::build_loads() {
+    const int n = disc->n_p, steps = ps.n_time_steps;
+    const double dt = ps.t_final / steps;
+    has_loads = false;
+    loads_steady = false;
+    if (!ps.load_terms.empty()) {
+        has_loads = true;
+        loads_steady = ps.load_terms_steady != 0;
+        const size_t want = loads_steady ? (size_t)n : (size_t)n * steps;
+        if (ps.load_terms.size() != want) throw InvalidArgument("load_terms: dimension mismatch");
+        loads.upload(ps.load_terms, stream);
+        return;
+    }
+    // LoadSchedule::build (theta.hpp:167-193)
+    if (ps.source_kind == 0) {
+        if (ps.source_param == 0.0) return;  // SourceTerm::zero
+        has_loads = loads_steady = true;
+        loads.alloc(n);
+        disc->assemble_load(0, ps.source_param, 0.0, nullptr, loads.get(), stream);
+        launch_scale(loads.get(), dt, n, stream);
+    } else if (ps.source_kind == 2) {
+        has_loads = loads_steady = true;
+        loads.alloc(n);
+        disc->assemble_load(2, ps.source_param, 0.0, nullptr, loads.get(), stream);
+        launch_scale(loads.get(), dt, n, stream);
+    } else if (ps.source_kind == 1) {
+        has_loads = true;
+        loads.alloc((size_t)n * steps);
+        // F_k = dt (theta f(t_k) + (1 - theta) f(t_{k-1})) from raw assemblies
+        DevBuf<double> prev(n), cur(n);
+        disc->assemble_load(1, ps.source_param, std::exp(-(0 * dt)), nullptr, prev.get(), stream);
+        for (int k = 1; k <= steps; ++k) {
+            double* fk = loads.get() + (size_t)(k - 1) * n;
+            disc->assemble_load(1, ps.source_param, std::exp(-(k * dt)), nullptr, cur.get(), stream);
+            launch_copy(fk, cur.get(), n, stream);
+            launch_theta_combine(fk, prev.get(), dt * ps.theta, dt * (1.0 - ps.theta), n, stream);
+            std::swap(prev, cur);
+        }
+        PHI_CUDA(cudaStreamSynchronize(stream));
+    } else {
+        throw InvalidArgument("unknown source kind");
+    }
+}
+
+void Mgrit::project_initial() {
+    const int n = disc->n_p;
+    if (ps.init_kind == 0) {
+        u0.zero(stream);
+        return;
+    }
+    DevBuf<double> b(n), work(4 * (size_t)n), coeffs;
+    DevBuf<int> res(2);
+    if (ps.init_kind == 1) {
+        disc->assemble_load(3, 0.0, 0.0, nullptr, b.get(), stream);
+    } else if (ps.init_kind == 2) {
+        if ((int)ps.init_coeffs.size() != n) throw InvalidArgument("init_coeffs: dimension mismatch");
+        coeffs.upload(ps.init_coeffs, stream);
+        disc->assemble_load(4, 0.0, 0.0, coeffs.get(), b.get(), stream);
+    } else {
+        throw InvalidArgument("unknown initial kind");
+    }
+    const DevStencil M = disc->M.view();
+    const int p = disc->degree, w = 2 * p + 1;
+    const double* diag = disc->M.vals.get() + (size_t)(p * w + p) * n;  // center entries
+    launch_cg(M, diag, b.get(), u0.get(), work.get(), 1e-13, 2000, res.get(), stream);
+    launches += 2;
+    const auto r = res.download(stream);
+    if (r[0] < 0) throw std::runtime_error("cg_solve: breakdown, matrix not SPD");
+    if (r[0] != 1) throw std::runtime_error("project_initial: mass solve did not converge");
+}
+
+void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, double* CG, double* CU) {
+    Level& lv = levels[l];
+    WaveArgs a{};
+    a.mode = mode;
+    a.epi = epi;
+    a.n_tasks = n_tasks;
+    a.task_len = len;
+    a.task_k0 = k0;
+    a.n = disc->n_p;
+    a.U = lv.u.get();
+    a.G = lv.g.get();
+    a.LOAD = (l == 0 && has_loads) ? loads.get() : nullptr;
+    a.load_steady = loads_steady ? 1 : 0;
+    a.CG = CG;
+    a.CU = CU;
+    a.m = cfg.m;
+    a.SQ = sq.get();
+    a.stat = stat.get();
+    a.err = err.get();
+    a.err_rel = err_rel.get();
+    a.level = l;
+    a.x0_empty = mode == kModeSolve ? 1 : 0;  // g-norm solves start from zero (mgrit.hpp:301)
+    launch_phi_wave(lv.stepper->H, lv.stepper->Aminus.view(), a, ws.buf.get(), ws.stride, ws.slots, stream);
+    ++launches;
+}
+
+void Mgrit::check_errors() {
+    const auto e = err.download(stream);
+    if (e[0]) {
+        const double rel = err_rel.download(stream)[0];
+        throw NotConverged("MGRIT level " + std::to_string(e[2]) + ", time step " + std::to_string(e[1]) +
+                           ": spatial solve did not converge (p-multigrid), residual " + std::to_string(rel));
+    }
+}
+
+// mgrit.hpp:122-141; with FCF the first F sweep also covers the C-point of its
+// interval (same operations in the same order per point).
+void Mgrit::f_relax(int l, bool with_c) {
+    Level& lv = levels[l];
+    const int J = lv.steps / cfg.m;
+    wave(l, kModeStep, kEpiStore, J, lv.kF.get(), with_c ? cfg.m : cfg.m - 1);
+}
+
+void Mgrit::c_relax(int l) {
+    Level& lv = levels[l];
+    wave(l, kModeStep, kEpiStore, lv.steps / cfg.m, lv.kR.get(), 1);
+}
+
+void Mgrit::restrict_residual(int l) {
+    Level& f = levels[l];
+    Level& c = levels[l + 1];
+    const int n = disc->n_p;
+    const int J = f.steps / cfg.m;
+    launch_restrict_first(f.g.get(), f.u.get(), c.g.get(), c.u.get(), n, stream);
+    ++launches;
+    wave(l, kModeStep, kEpiRestrict, J, f.kR.get(), 1, c.g.get(), c.u.get());
+}
+
+void Mgrit::interpolate_and_correct(int l) {
+    Level& f = levels[l];
+    Level& c = levels[l + 1];
+    launch_inject(c.u.get(), f.u.get(), disc->n_p, f.steps / cfg.m, cfg.m, stream);
+    ++launches;
+    f_relax(l, false);
+}
+
+void Mgrit::coarsest_solve(int l) {
+    Level& lv = levels[l];
+    launch_copy(lv.u.get(), lv.g.get(), disc->n_p, stream);
+    ++launches;
+    wave(l, kModeStep, kEpiStore, 1, lv.kAll.get(), lv.steps);
+}
+
+void Mgrit::cycle_impl(int l, bool f_schedule) {
+    if (l + 1 == n_levels()) {
+        coarsest_solve(l);
+        return;
+    }
+    if (cfg.relax == 1) {
+        f_relax(l, true);   // F + C
+        f_relax(l, false);  // F
+    } else {
+        f_relax(l, false);
+    }
+    restrict_residual(l);
+    cycle_impl(l + 1, f_schedule);
+    interpolate_and_correct(l);
+    if (f_schedule && l + 2 < n_levels()) cycle_impl(l, false);
+}
+
+void Mgrit::mgrit_cycle(int l) { cycle_impl(l, cfg.cycle == 1); }
+
+double Mgrit::residual_norm(int l) {
+    Level& lv = levels[l];
+    const int n = disc->n_p;
+    launch_resid0(lv.g.get(), lv.u.get(), sq.get(), n, stream);
+    ++launches;
+    wave(l, kModeStep, kEpiResid, lv.steps, lv.kAll.get(), 1);
+    std::vector<double> h(lv.steps + 1);
+    PHI_CUDA(cudaMemcpyAsync(h.data(), sq.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, stream));
+    PHI_CUDA(cudaStreamSynchronize(stream));
+    check_errors();
+    double total = 0.0;
+    for (double s : h) total += s;  // fixed order (mgrit.hpp:211-212)
+    return std::sqrt(total);
+}
+
+double Mgrit::compute_g_norm() {
+    Level& lv0 = levels[0];
+    const int n = disc->n_p;
+    std::vector<double> g0(n);
+    PHI_CUDA(cudaMemcpyAsync(g0.data(), lv0.g.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+    PHI_CUDA(cudaStreamSynchronize(stream));
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total += g0[i] * g0[i];
+    if (has_loads) {
+        PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (lv0.steps + 1), stream));
+        if (loads_steady) {
+            wave(0, kModeSolve, kEpiNorm, 1, lv0.kAll.get(), 1);
+            double v = 0.0;
+            PHI_CUDA(cudaMemcpyAsync(&v, sq.get() + 1, sizeof(double), cudaMemcpyDeviceToHost, stream));
+            PHI_CUDA(cudaStreamSynchronize(stream));
+            check_errors();
+            total += lv0.steps * v;
+        } else {
+            wave(0, kModeSolve, kEpiNorm, lv0.steps, lv0.kAll.get(), 1);
+            std::vector<double> h(lv0.steps + 1);
+            PHI_CUDA(cudaMemcpyAsync(h.data(), sq.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                                     stream));
+            PHI_CUDA(cudaStreamSynchronize(stream));
+            check_errors();
+            for (double s : h) total += s;
+        }
+    }
+    return std::sqrt(total);
+}
+
+void Mgrit::initialize() {
+    const int n = disc->n_p;
+    for (auto& lv : levels) {
+        lv.u.zero(stream);
+        lv.g.zero(stream);
+    }
+    project_initial();
+    launch_copy(levels[0].g.get(), u0.get(), n, stream);
+    launch_copy(levels[0].u.get(), u0.get(), n, stream);
+    launches += 2;
+    stat.zero(stream);
+    const std::vector<int> e0{0, INT_MAX, -1};
+    err.upload(e0, stream);
+    g_norm = compute_g_norm();
+}
+
+MgritResultHost Mgrit::solve() {
+    launches = 0;
+    initialize();
+    MgritResultHost res;
+    res.g_norm = g_norm;
+    const double denom = g_norm > 0.0 ? g_norm : 1.0;
+    for (int it = 1; it <= cfg.max_iter; ++it) {
+        mgrit_cycle(0);
+        const double rel = residual_norm(0) / denom;
+        res.residual_history.push_back(rel);
+        res.iterations = it;
+        if (rel <= cfg.halt_tol) {
+            res.converged = true;
+            break;
+        }
+    }
+    res.final_relative_residual = res.residual_history.back();
+    const auto st = stat.download(stream);
+    res.total_spatial_solves = (long long)st[0];
+    res.mean_spatial_iterations = st[0] > 0 ? (double)st[1] / (double)st[0] : 0.0;
+    return res;
+}
+
+}  // namespace phi

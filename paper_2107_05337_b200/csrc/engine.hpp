@@ -1,0 +1,211 @@
+// Host-side engine objects mirroring the reference's operator API
+// (proj/include/miga): SpatialDiscretization, PMultigridHierarchy,
+// ThetaStepper and MgritSolver.  They own device-resident operators and
+// launch the kernels in phi_kernels.cu / assembly.cu.  All compute runs on the
+// GPU; the host only builds the ILUT factors / coarse LU / solve schedules and
+// drives the MGRIT control flow.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "device_types.cuh"
+#include "phi_kernels.cuh"
+#include "setup_host.hpp"
+
+namespace phi {
+
+struct StencilBuf {
+    int ru = 0, rv = 0, cu = 0, cv = 0, lo = 0, hi = 0;
+    DevBuf<double> vals;
+    DevStencil view() const { return DevStencil{ru, rv, cu, cv, lo, hi, vals.get()}; }
+    size_t n_rows() const { return (size_t)ru * rv; }
+    size_t width() const { return (size_t)(hi - lo + 1); }
+    size_t size() const { return n_rows() * width() * width(); }
+};
+
+struct Tables1DDev {
+    Tables1D host;
+    DevBuf<double> w, vals, ders;
+    DevTables1D view() const { return DevTables1D{host.p, host.nq, host.nel, w.get(), vals.get(), ders.get()}; }
+};
+
+/// SpatialDiscretization::build (pmultigrid.hpp:94-158), unit square, on device.
+class Disc {
+public:
+    static std::shared_ptr<Disc> build(int degree, int mesh_exponent, cudaStream_t s = nullptr);
+
+    int degree = 0, mesh_exponent = 0, n_elements = 0;
+    int nf_p = 0, n_p = 0;  // free dofs per direction / total, order p
+    int nf_1 = 0, n_1 = 0;  // order 1 on the fine mesh
+    StencilBuf M, K;        // order p, free rows, offsets [-p, p]
+    StencilBuf T, Tt;       // transfer p->1 and its transpose
+    DevBuf<double> inv_lp, inv_l1;
+
+    struct HLevel {
+        int n_elements = 0, nf = 0, n = 0;
+        StencilBuf M, K;
+        HostCsr E, Et;  // embedding from the next coarser level (empty on the coarsest)
+        DevBuf<int> e_ro, e_ci, et_ro, et_ci;
+        DevBuf<double> e_v, et_v;
+    };
+    std::vector<HLevel> h;
+
+    Tables1DDev tab_p;               // order-p tables (nq = p + 1) for load assembly
+    DevBuf<double> sin_tab;          // sin(pi * node) per (element, q), host libm
+    std::vector<double> sin_host;
+
+    /// Free-dof CSR of a stencil matrix (download), reference layout.
+    HostCsr to_csr(const StencilBuf& a) const;
+    /// Load vector (free dofs) on device: see launch_assemble_load kinds.
+    void assemble_load(int kind, double c0, double c1, const double* coeffs_dev, double* out,
+                       cudaStream_t s) const;
+};
+
+struct HierOptions {  // PMultigridOptions (pmultigrid.hpp:161-168)
+    double ilut_tau = 1e-13;
+    int ilut_fill = 0;
+    int nu_pre = 1, nu_post = 1, gs_pre = 2, gs_post = 2;
+};
+
+struct SolverConfig {  // SpatialSolverConfig (theta.hpp:66-75), pmg kind
+    double rel_tol = 1e-12;
+    int max_iter = 400;
+    int fixed_cycles = 0;
+    HierOptions pmg;
+};
+
+/// Batch workspace (one slot per resident CTA) shared by objects on one stream.
+struct Workspace {
+    DevBuf<double> buf;
+    long long stride = 0;
+    int slots = 0;
+    void ensure(const DevHier& H);
+};
+
+/// PMultigridHierarchy(disc, c, opt) (pmultigrid.hpp:215-324) on device.
+class Hier {
+public:
+    Hier(std::shared_ptr<const Disc> disc, double c, const HierOptions& opt, cudaStream_t s = nullptr);
+    std::shared_ptr<const Disc> disc;
+    double c = 0.0;
+    HierOptions opt;
+    StencilBuf A;                       // M + c K
+    std::vector<StencilBuf> a_h;        // per h-level
+    HostCsr L_host, U_host;             // ILUT factors (host copy)
+    TriPlan Lp, Up;
+    struct TriDev {
+        DevBuf<int> level_chunk, chunk_row0, chunk_nrows, chunk_base, rows, lens, cols;
+        DevBuf<double> vals, diag;
+    } Ld, Ud;
+    DenseLUHost coarse;
+    DevBuf<double> coarse_lu;
+    DevBuf<int> coarse_piv;
+
+    DevHier view(const SolverConfig& cfg) const;
+    HostCsr a_h_csr(int l) const;
+};
+
+/// ThetaStepper (theta.hpp:92-146): Phi(u) = (M + k dt th K)^-1 ((M - k dt (1-th) K) u + load).
+class Stepper {
+public:
+    Stepper(std::shared_ptr<const Disc> disc, double kappa, double dt, double theta,
+            const SolverConfig& cfg, cudaStream_t s = nullptr);
+    std::shared_ptr<const Disc> disc;
+    double kappa, dt, theta;
+    SolverConfig cfg;
+    std::unique_ptr<Hier> hier;
+    StencilBuf Aminus;
+    DevHier H;
+};
+
+struct MgritOptions {  // MgritConfig (mgrit.hpp:17-31)
+    int cycle = 0;  // 0 V, 1 F, 2 two-level
+    int relax = 1;  // 0 F, 1 FCF
+    int m = 2;
+    double halt_tol = 1e-10;
+    int max_iter = 50;
+    int coarse_floor = 8;
+};
+
+struct ProblemOptions {  // ProblemSpec (theta.hpp:42-62) + source / initial kinds
+    double kappa = 1.0, t_final = 0.1, theta = 1.0;
+    int n_time_steps = 64;
+    int source_kind = 0;  // 0 constant, 1 amp e^-t sin sin (transient), 2 amp sin sin (steady)
+    double source_param = 1.0;
+    int init_kind = 0;  // 0 zero, 1 sin sin, 2 spline coefficients
+    std::vector<double> init_coeffs;
+    // optional caller-provided level-0 load terms (steps x n) -- drop-in path
+    std::vector<double> load_terms;
+    int load_terms_steady = 0;
+};
+
+struct MgritResultHost {
+    int iterations = 0;
+    bool converged = false;
+    double g_norm = 0.0, final_relative_residual = 0.0;
+    std::vector<double> residual_history;
+    long long total_spatial_solves = 0;
+    double mean_spatial_iterations = 0.0;
+};
+
+/// MgritSolver (mgrit.hpp:50-320) with the space-time state resident on device.
+class Mgrit {
+public:
+    Mgrit(std::shared_ptr<const Disc> disc, const ProblemOptions& ps, const MgritOptions& cfg,
+          const SolverConfig& scfg, cudaStream_t s = nullptr);
+    MgritResultHost solve();
+    void initialize();
+    void mgrit_cycle(int l);
+    double residual_norm(int l);
+    int n_levels() const { return (int)levels.size(); }
+
+    struct Level {
+        int steps = 0;
+        double dt = 0.0;
+        std::unique_ptr<Stepper> stepper;
+        DevBuf<double> u, g;
+        DevBuf<int> kF, kR, kAll;
+    };
+    std::vector<Level> levels;
+    std::shared_ptr<const Disc> disc;
+    ProblemOptions ps;
+    MgritOptions cfg;
+    SolverConfig scfg;
+    cudaStream_t stream = nullptr;
+    Workspace ws;
+    DevBuf<double> loads;  // level-0 terms: steady (n) or transient (steps x n)
+    bool has_loads = false, loads_steady = false;
+    DevBuf<double> sq;
+    DevBuf<unsigned long long> stat;
+    DevBuf<int> err;
+    DevBuf<double> err_rel;
+    DevBuf<double> u0;
+    double g_norm = 0.0;
+    long long launches = 0;  // kernels launched by the solve (bench evidence)
+
+private:
+    void build_levels();
+    void build_loads();
+    void project_initial();
+    double compute_g_norm();
+    void wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, double* CG = nullptr,
+              double* CU = nullptr);
+    void check_errors();
+    void f_relax(int l, bool with_c);
+    void c_relax(int l);
+    void restrict_residual(int l);
+    void interpolate_and_correct(int l);
+    void coarsest_solve(int l);
+    void cycle_impl(int l, bool f_schedule);
+};
+
+/// Sequential Phi-march on device (sequential_integrate, theta.hpp:216-237):
+/// traj[0] = u0, traj[k] = Phi(traj[k-1]) with guess traj[k-1].
+struct SequentialResult {
+    long long solves = 0, iterations = 0;
+};
+
+}  // namespace phi

@@ -1,0 +1,74 @@
+// Host-callable launchers for the Phi kernels (phi_kernels.cu) and the device
+// assembly kernels (assembly.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "common.hpp"
+#include "device_types.cuh"
+
+namespace phi {
+
+constexpr int kPhiThreads = 256;
+// Triangular-solve dependency array kept in shared memory up to this size
+// (n_p <= 25,600 rows: configs 1-3); above it the global-memory variant runs.
+constexpr size_t kPhiSmemZMaxBytes = 200 * 1024;
+
+size_t phi_ws_doubles(const DevHier& H);
+bool phi_smem_z(const DevHier& H);
+size_t phi_smem_bytes(const DevHier& H);
+int phi_max_slots(const DevHier& H);
+
+void launch_phi_wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws,
+                     long long ws_stride, int max_slots, cudaStream_t s);
+void launch_vcycle(const DevHier& H, const double* B, long long ldb, double* X, long long ldx, int nrhs,
+                   double* ws, long long ws_stride, int max_slots, cudaStream_t s);
+void launch_unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
+                 long long ws_stride, cudaStream_t s);
+void launch_cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
+               double rel_tol, int max_iter, int* result, cudaStream_t s);
+void launch_restrict_first(const double* fg, const double* fu, double* cg, double* cu, int n,
+                           cudaStream_t s);
+void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s);
+void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s);
+void launch_copy(double* dst, const double* src, size_t n, cudaStream_t s);
+
+// ---- device assembly (assembly.cu) ---------------------------------------
+/// 1D tables on the device for one direction (see Tables1D).
+struct DevTables1D {
+    int p, nq, nel;
+    const double* w;      // [e*nq + q]
+    const double* vals;   // [(e*nq + q)*(p+1) + a]
+    const double* ders;
+};
+
+/// Galerkin mass / stiffness of the degree-p tensor basis, free rows,
+/// stencil-major with offsets [-p, p]^2 and FULL-grid column validity
+/// (boundary columns kept for lumping).  Either output may be null.
+void launch_assemble_mk(const DevTables1D& tu, const DevTables1D& tv, double* mass, double* stiff,
+                        cudaStream_t s);
+/// Row-sum lumped mass (assembly.hpp:437-446) of the full matrix restricted to
+/// free rows, inverted: inv[i] = 1 / sum_j M(i, j).  Returns status via flag.
+void launch_lump_inv(const double* mass, int p, int nel, double* inv, int* bad, cudaStream_t s);
+/// Mixed order-p / order-1 transfer (assembly.hpp:376-433), free rows/cols,
+/// offsets [-p, 1]^2.
+void launch_assemble_transfer(const DevTables1D& tu, const DevTables1D& tv, const double* low_u,
+                              const double* low_v, double* t, cudaStream_t s);
+/// Transpose a stencil operator (rows on grid R with offsets [lo, hi]) into one
+/// with rows on the column grid and offsets [-hi, -lo].
+void launch_stencil_transpose(const DevStencil& a, double* out, cudaStream_t s);
+/// out = a + c * b elementwise (sparse_add on a shared pattern, sparse.hpp:148-178).
+void launch_axpby(const double* a, double c, const double* b, double* out, size_t n, cudaStream_t s);
+/// Load vector (assembly.hpp:365-371 + restrict_vector) for free dofs.
+/// kind: 0 constant(c0); 1 ((c0 * c1) * sx) * sy  [amp * exp(-t) * sin * sin];
+/// 2 (c0 * sx) * sy [amp * sin * sin]; 3 sx * sy; 4 spline with free coeffs.
+void launch_assemble_load(const DevTables1D& tu, const DevTables1D& tv, int kind, double c0, double c1,
+                          const double* sx, const double* sy, const double* coeffs, double* out,
+                          cudaStream_t s);
+/// f_k = f_k * (dt*theta) + (dt*(1-theta)) * f_{k-1}   (theta.hpp:186-191)
+void launch_theta_combine(double* fk, const double* fkm1, double a, double b, int n, cudaStream_t s);
+void launch_scale(double* v, double a, size_t n, cudaStream_t s);
+
+}  // namespace phi

@@ -1,0 +1,427 @@
+// Host setup for the engine.  Every routine restates the reference algorithm it
+// cites in the same floating-point evaluation order (compiled with
+// -ffp-contract=off), so the device operators built from these tables are
+// bit-identical to the reference's.
+#include "setup_host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <queue>
+#include <string>
+
+namespace phi {
+
+GaussRule gauss_legendre_01(int n) {
+    if (n < 1) throw InvalidArgument("gauss_legendre_01: n must be >= 1");
+    GaussRule r;
+    r.nodes.resize(n);
+    r.weights.resize(n);
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < n; ++i) {
+        double x = std::cos(pi * (i + 0.75) / (n + 0.5));
+        double dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = x;
+            for (int k = 2; k <= n; ++k) {
+                const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n * (x * p1 - p0) / (x * x - 1.0);
+            const double dx = p1 / dp;
+            x -= dx;
+            if (std::abs(dx) < 1e-15) break;
+        }
+        r.nodes[i] = 0.5 * (1.0 - x);
+        r.weights[i] = 1.0 / ((1.0 - x * x) * dp * dp);
+    }
+    return r;
+}
+
+int Knots::find_span(double xi) const {
+    if (xi >= t[n_basis]) return n_basis - 1;
+    auto it = std::upper_bound(t.begin() + degree, t.begin() + n_basis + 1, xi);
+    return static_cast<int>(it - t.begin()) - 1;
+}
+
+Knots open_uniform_knots(int degree, int n_elements) {
+    if (degree < 1) throw InvalidArgument("open_uniform_knots: degree must be >= 1");
+    if (n_elements < 1) throw InvalidArgument("open_uniform_knots: n_elements must be >= 1");
+    Knots kv;
+    kv.degree = degree;
+    kv.n_basis = n_elements + degree;
+    kv.t.resize(kv.n_basis + degree + 1);
+    const double a = 0.0, b = 1.0;
+    const double h = (b - a) / n_elements;
+    for (int i = 0; i <= degree; ++i) {
+        kv.t[i] = a;
+        kv.t[kv.t.size() - 1 - i] = b;
+    }
+    for (int i = 1; i < n_elements; ++i) kv.t[degree + i] = a + i * h;
+    return kv;
+}
+
+namespace {
+
+// Triangular Cox-de Boor on one span (NURBS-book A2.2 form).
+void basis_on_span(const Knots& kv, int span, double xi, int deg, double* out) {
+    const auto& t = kv.t;
+    double left[32] = {0}, right[32] = {0};
+    out[0] = 1.0;
+    for (int j = 1; j <= deg; ++j) {
+        left[j] = xi - t[span + 1 - j];
+        right[j] = t[span + j] - xi;
+        double saved = 0.0;
+        for (int r = 0; r < j; ++r) {
+            const double tmp = out[r] / (right[r + 1] + left[j - r]);
+            out[r] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        out[j] = saved;
+    }
+}
+
+// Values and first derivatives on the span of xi (spline.hpp:104-130).
+int values_and_derivs(const Knots& kv, double xi, double* vals, double* ders) {
+    const int p = kv.degree;
+    const int span = kv.find_span(xi);
+    for (int a = 0; a <= p; ++a) vals[a] = ders[a] = 0.0;
+    basis_on_span(kv, span, xi, p, vals);
+    double lower[32] = {0};
+    basis_on_span(kv, span, xi, p - 1, lower);
+    const auto& t = kv.t;
+    for (int r = 0; r <= p; ++r) {
+        const int i = span - p + r;
+        double d = 0.0;
+        if (r >= 1) {
+            const double den = t[i + p] - t[i];
+            if (den > 0.0) d += lower[r - 1] / den;
+        }
+        if (r <= p - 1) {
+            const double den = t[i + p + 1] - t[i + 1];
+            if (den > 0.0) d -= lower[r] / den;
+        }
+        ders[r] = p * d;
+    }
+    return span - p;
+}
+
+}  // namespace
+
+Tables1D build_tables(const Knots& kv, int nq) {
+    Tables1D tb;
+    tb.p = kv.degree;
+    tb.nq = nq;
+    const GaussRule rule = gauss_legendre_01(nq);
+    std::vector<int> spans;
+    for (int s = kv.degree; s < kv.n_basis; ++s)
+        if (kv.t[s + 1] > kv.t[s]) spans.push_back(s);
+    tb.nel = static_cast<int>(spans.size());
+    for (int s : spans) {
+        const double a = kv.t[s], b = kv.t[s + 1];
+        for (int i = 0; i < nq; ++i) {
+            tb.nodes.push_back(a + rule.nodes[i] * (b - a));
+            tb.weights.push_back(rule.weights[i] * (b - a));
+        }
+    }
+    const int p = tb.p;
+    tb.vals.resize(static_cast<size_t>(tb.nel) * nq * (p + 1));
+    tb.ders.resize(tb.vals.size());
+    tb.first.resize(tb.nel);
+    for (int e = 0; e < tb.nel; ++e)
+        for (int q = 0; q < nq; ++q) {
+            const size_t base = (static_cast<size_t>(e) * nq + q) * (p + 1);
+            tb.first[e] = values_and_derivs(kv, tb.nodes[e * nq + q], &tb.vals[base], &tb.ders[base]);
+        }
+    return tb;
+}
+
+LowTables build_low_tables(const Knots& low, const Tables1D& high) {
+    LowTables lt;
+    const int n = high.nel * high.nq;
+    lt.vals.resize(static_cast<size_t>(n) * 2);
+    lt.first.resize(n);
+    for (int i = 0; i < n; ++i) {
+        double v[2], d[2];
+        lt.first[i] = values_and_derivs(low, high.nodes[i], v, d);
+        lt.vals[2 * i] = v[0];
+        lt.vals[2 * i + 1] = v[1];
+    }
+    return lt;
+}
+
+HostCsr p1_embedding_free(int nel_f) {
+    if (nel_f % 2 != 0) throw InvalidArgument("p1_embedding_full: fine element count must be even");
+    const int nf = nel_f + 1, nc = nel_f / 2 + 1;
+    const int nff = nf - 2, ncf = nc - 2;  // free nodes per direction
+    auto entries = [](int i, int* idx, double* w) {
+        if (i % 2 == 0) {
+            idx[0] = i / 2;
+            w[0] = 1.0;
+            return 1;
+        }
+        idx[0] = (i - 1) / 2;
+        w[0] = 0.5;
+        idx[1] = (i + 1) / 2;
+        w[1] = 0.5;
+        return 2;
+    };
+    HostCsr e;
+    e.n_rows = nff * nff;
+    e.n_cols = ncf * ncf;
+    for (int iv = 1; iv <= nff; ++iv) {
+        int jvs[2], jus[2];
+        double wvs[2], wus[2];
+        const int nv = entries(iv, jvs, wvs);
+        for (int iu = 1; iu <= nff; ++iu) {
+            const int nu = entries(iu, jus, wus);
+            // (jv, ju) ascending == ascending global / free column index
+            for (int a = 0; a < nv; ++a) {
+                if (jvs[a] < 1 || jvs[a] > ncf) continue;
+                for (int b = 0; b < nu; ++b) {
+                    if (jus[b] < 1 || jus[b] > ncf) continue;
+                    e.col_indices.push_back((jus[b] - 1) + ncf * (jvs[a] - 1));
+                    e.values.push_back(wus[b] * wvs[a]);
+                }
+            }
+            e.row_offsets.push_back(e.nnz());
+        }
+    }
+    return e;
+}
+
+HostCsr transpose(const HostCsr& a) {
+    HostCsr t;
+    t.n_rows = a.n_cols;
+    t.n_cols = a.n_rows;
+    t.row_offsets.assign(a.n_cols + 1, 0);
+    for (int c : a.col_indices) ++t.row_offsets[c + 1];
+    for (int i = 0; i < a.n_cols; ++i) t.row_offsets[i + 1] += t.row_offsets[i];
+    t.col_indices.resize(a.col_indices.size());
+    t.values.resize(a.values.size());
+    std::vector<int> next(t.row_offsets.begin(), t.row_offsets.end() - 1);
+    for (int i = 0; i < a.n_rows; ++i)
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) {
+            const int pos = next[a.col_indices[e]]++;
+            t.col_indices[pos] = i;
+            t.values[pos] = a.values[e];
+        }
+    return t;
+}
+
+void ilut_factor(const HostCsr& a, double tau, int fill_limit, HostCsr& lower, HostCsr& upper) {
+    const int n = a.n_rows;
+    if (a.n_rows != a.n_cols) throw InvalidArgument("ilut_factor: matrix not square");
+    if (fill_limit <= 0) fill_limit = (a.nnz() + n - 1) / std::max(n, 1);
+    lower = HostCsr{};
+    upper = HostCsr{};
+    lower.n_rows = lower.n_cols = upper.n_rows = upper.n_cols = n;
+    lower.col_indices.reserve(a.nnz());
+    lower.values.reserve(a.nnz());
+    upper.col_indices.reserve(a.nnz() + n);
+    upper.values.reserve(a.nnz() + n);
+
+    std::vector<double> w(n, 0.0);
+    std::vector<char> active(n, 0);
+    std::vector<int> touched;
+    std::priority_queue<int, std::vector<int>, std::greater<int>> pending;
+    struct Ent {
+        int col;
+        double val;
+    };
+    std::vector<Ent> lpart, upart;
+    // strict total order: larger magnitude first, then smaller column
+    auto larger = [](const Ent& x, const Ent& y) {
+        const double ax = std::abs(x.val), ay = std::abs(y.val);
+        if (ax != ay) return ax > ay;
+        return x.col < y.col;
+    };
+    auto keep = [&](std::vector<Ent>& part) {
+        if (static_cast<int>(part.size()) > fill_limit) {
+            std::partial_sort(part.begin(), part.begin() + fill_limit, part.end(), larger);
+            part.resize(fill_limit);
+        }
+        std::sort(part.begin(), part.end(), [](const Ent& x, const Ent& y) { return x.col < y.col; });
+    };
+
+    for (int i = 0; i < n; ++i) {
+        double row_norm_sq = 0.0;
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) {
+            const int j = a.col_indices[e];
+            const double v = a.values[e];
+            row_norm_sq += v * v;
+            w[j] = v;
+            if (!active[j]) {
+                active[j] = 1;
+                touched.push_back(j);
+                if (j < i) pending.push(j);
+            }
+        }
+        const double drop = tau * std::sqrt(row_norm_sq);
+        while (!pending.empty()) {
+            const int k = pending.top();
+            pending.pop();
+            const int urow = upper.row_offsets[k];
+            const double beta = w[k] / upper.values[urow];
+            if (std::abs(beta) < drop) {
+                w[k] = 0.0;
+                continue;
+            }
+            w[k] = beta;
+            for (int e = urow + 1; e < upper.row_offsets[k + 1]; ++e) {
+                const int j = upper.col_indices[e];
+                if (!active[j]) {
+                    active[j] = 1;
+                    touched.push_back(j);
+                    w[j] = 0.0;
+                    if (j < i) pending.push(j);
+                }
+                w[j] -= beta * upper.values[e];
+            }
+        }
+        lpart.clear();
+        upart.clear();
+        double diag = 0.0;
+        bool diag_present = false;
+        for (int j : touched) {
+            const double v = w[j];
+            w[j] = 0.0;
+            active[j] = 0;
+            if (j == i) {
+                diag = v;
+                diag_present = true;
+            } else if (v != 0.0 && std::abs(v) >= drop) {
+                (j < i ? lpart : upart).push_back({j, v});
+            }
+        }
+        touched.clear();
+        if (!diag_present || diag == 0.0)
+            throw std::runtime_error("ilut_factor: zero pivot in row " + std::to_string(i));
+        keep(lpart);
+        keep(upart);
+        for (const auto& e : lpart) {
+            lower.col_indices.push_back(e.col);
+            lower.values.push_back(e.val);
+        }
+        lower.row_offsets.push_back(lower.nnz());
+        upper.col_indices.push_back(i);
+        upper.values.push_back(diag);
+        for (const auto& e : upart) {
+            upper.col_indices.push_back(e.col);
+            upper.values.push_back(e.val);
+        }
+        upper.row_offsets.push_back(upper.nnz());
+    }
+}
+
+DenseLUHost dense_lu_factor(const HostCsr& a) {
+    if (a.n_rows != a.n_cols) throw InvalidArgument("DenseLU: matrix not square");
+    DenseLUHost f;
+    const int n = a.n_rows;
+    f.n = n;
+    f.lu.assign(static_cast<size_t>(n) * n, 0.0);
+    auto at = [&](int i, int j) -> double& { return f.lu[static_cast<size_t>(i) * n + j]; };
+    for (int i = 0; i < n; ++i)
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) at(i, a.col_indices[e]) = a.values[e];
+    std::vector<int> perm(n);
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int k = 0; k < n; ++k) {
+        int pivot = k;
+        double best = std::abs(at(k, k));
+        for (int i = k + 1; i < n; ++i) {
+            const double v = std::abs(at(i, k));
+            if (v > best) {
+                best = v;
+                pivot = i;
+            }
+        }
+        if (best == 0.0) throw std::runtime_error("DenseLU: singular matrix");
+        if (pivot != k) {
+            for (int j = 0; j < n; ++j) std::swap(at(k, j), at(pivot, j));
+            std::swap(perm[k], perm[pivot]);
+        }
+        const double d = at(k, k);
+        for (int i = k + 1; i < n; ++i) {
+            const double m = at(i, k) / d;
+            at(i, k) = m;
+            if (m == 0.0) continue;
+            for (int j = k + 1; j < n; ++j) at(i, j) -= m * at(k, j);
+        }
+    }
+    f.piv = perm;
+    return f;
+}
+
+namespace {
+
+TriPlan make_plan(const HostCsr& m, bool upper) {
+    TriPlan p;
+    const int n = m.n_rows;
+    p.n = n;
+    std::vector<int> level(n, 0);
+    int max_level = -1;
+    auto row_level = [&](int i) {
+        int lv = 0;
+        const int b = m.row_offsets[i] + (upper ? 1 : 0);
+        for (int e = b; e < m.row_offsets[i + 1]; ++e) lv = std::max(lv, level[m.col_indices[e]] + 1);
+        level[i] = lv;
+        max_level = std::max(max_level, lv);
+    };
+    if (upper)
+        for (int i = n - 1; i >= 0; --i) row_level(i);
+    else
+        for (int i = 0; i < n; ++i) row_level(i);
+    p.n_levels = max_level + 1;
+    // bucket rows by level; within a level keep solve order
+    std::vector<std::vector<int>> by_level(p.n_levels);
+    if (upper)
+        for (int i = n - 1; i >= 0; --i) by_level[level[i]].push_back(i);
+    else
+        for (int i = 0; i < n; ++i) by_level[level[i]].push_back(i);
+    p.level_chunk.push_back(0);
+    for (int lv = 0; lv < p.n_levels; ++lv) {
+        const auto& rs = by_level[lv];
+        for (size_t c0 = 0; c0 < rs.size(); c0 += 32) {
+            const int nr = static_cast<int>(std::min<size_t>(32, rs.size() - c0));
+            int maxlen = 0;
+            for (int l = 0; l < nr; ++l) {
+                const int i = rs[c0 + l];
+                const int len = m.row_offsets[i + 1] - m.row_offsets[i] - (upper ? 1 : 0);
+                maxlen = std::max(maxlen, len);
+            }
+            p.chunk_row0.push_back(static_cast<int>(p.rows.size()));
+            p.chunk_nrows.push_back(nr);
+            p.chunk_base.push_back(static_cast<int>(p.cols.size()));
+            const size_t base = p.cols.size();
+            p.cols.resize(base + static_cast<size_t>(maxlen) * nr, 0);
+            p.vals.resize(base + static_cast<size_t>(maxlen) * nr, 0.0);
+            for (int l = 0; l < nr; ++l) {
+                const int i = rs[c0 + l];
+                const int b = m.row_offsets[i] + (upper ? 1 : 0);
+                const int len = m.row_offsets[i + 1] - b;
+                p.rows.push_back(i);
+                p.lens.push_back(len);
+                p.max_row_len = std::max(p.max_row_len, len);
+                for (int e = 0; e < len; ++e) {
+                    p.cols[base + static_cast<size_t>(e) * nr + l] = m.col_indices[b + e];
+                    p.vals[base + static_cast<size_t>(e) * nr + l] = m.values[b + e];
+                }
+            }
+        }
+        p.level_chunk.push_back(static_cast<int>(p.chunk_row0.size()));
+    }
+    p.n_chunks = static_cast<int>(p.chunk_row0.size());
+    if (upper) {
+        p.diag.resize(n);
+        for (int i = 0; i < n; ++i) p.diag[i] = m.values[m.row_offsets[i]];
+    }
+    return p;
+}
+
+}  // namespace
+
+TriPlan plan_lower(const HostCsr& lower) { return make_plan(lower, false); }
+TriPlan plan_upper(const HostCsr& upper) { return make_plan(upper, true); }
+
+}  // namespace phi

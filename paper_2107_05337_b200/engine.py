@@ -1,0 +1,408 @@
+"""Python mirror of the reference operator API over the engine's C ABI.
+
+Class and method names follow ``/root/reference/proj/include/miga``
+(``SpatialDiscretization``, ``PMultigridHierarchy``, ``ThetaStepper``,
+``MgritSolver``, ``sequential_integrate``) so the parity tests read like the
+reference's own Catch2 suites.  Everything below calls
+``_lib/libphi_engine.so`` (include/phi_engine.h); there is no Python or CPU
+compute path: if the library or the GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libphi_engine.so")
+
+PHI_OK, PHI_ERR_INVALID, PHI_ERR_NOT_CONVERGED, PHI_ERR_CUDA, PHI_ERR_RUNTIME = range(5)
+SOURCE_CONSTANT, SOURCE_SIN_EXP, SOURCE_SIN = 0, 1, 2
+INIT_ZERO, INIT_SIN, INIT_COEFFS = 0, 1, 2
+CYCLE_V, CYCLE_F, CYCLE_TWO_LEVEL = 0, 1, 2
+RELAX_F, RELAX_FCF = 0, 1
+
+# every symbol include/phi_engine.h declares (checked by tests/test_capi_symbols.py)
+EXPORTED = [
+    "phi_last_error", "phi_default_solver_config", "phi_default_mgrit_config", "phi_default_problem",
+    "phi_device_count", "phi_set_device", "phi_synchronize", "phi_disc_build", "phi_disc_free",
+    "phi_disc_info", "phi_disc_export", "phi_disc_vector", "phi_hier_create", "phi_hier_free",
+    "phi_hier_export", "phi_hier_vcycle", "phi_hier_solve", "phi_hier_unit", "phi_stepper_create",
+    "phi_stepper_free", "phi_stepper_step", "phi_sequential_integrate", "phi_mgrit_create",
+    "phi_mgrit_free", "phi_mgrit_levels", "phi_mgrit_solve", "phi_mgrit_trajectory",
+    "phi_mgrit_initial", "phi_mgrit_initialize", "phi_mgrit_cycle", "phi_mgrit_residual_norm",
+    "phi_mgrit_launches",
+]
+
+
+class EngineError(RuntimeError):
+    """Raised for PHI_ERR_CUDA / PHI_ERR_RUNTIME."""
+
+
+class NotConvergedError(RuntimeError):
+    """PHI_ERR_NOT_CONVERGED (the reference's runtime_error from theta.hpp:116-118)."""
+
+
+class PmgOptions(C.Structure):
+    _fields_ = [("ilut_tau", C.c_double), ("ilut_fill", C.c_int), ("nu_pre", C.c_int),
+                ("nu_post", C.c_int), ("gs_pre", C.c_int), ("gs_post", C.c_int)]
+
+
+class SolverConfig(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("max_iter", C.c_int), ("fixed_cycles", C.c_int),
+                ("pmg", PmgOptions)]
+
+
+class MgritConfig(C.Structure):
+    _fields_ = [("cycle", C.c_int), ("relax", C.c_int), ("m", C.c_int), ("halt_tol", C.c_double),
+                ("max_iter", C.c_int), ("coarse_floor", C.c_int)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("kappa", C.c_double), ("t_final", C.c_double), ("theta", C.c_double),
+                ("n_time_steps", C.c_int), ("source_kind", C.c_int), ("source_param", C.c_double),
+                ("init_kind", C.c_int), ("init_coeffs", C.c_void_p), ("load_terms", C.c_void_p),
+                ("load_terms_steady", C.c_int)]
+
+
+class MgritResultC(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("g_norm", C.c_double),
+                ("final_relative_residual", C.c_double), ("total_spatial_solves", C.c_longlong),
+                ("mean_spatial_iterations", C.c_double)]
+
+
+_lib = None
+_vp, _i, _d, _ll = C.c_void_p, C.c_int, C.c_double, C.c_longlong
+
+
+def lib():
+    """Load the engine library (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EngineError(f"{LIB_PATH} not built: run `python -m paper_2107_05337_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        L.phi_last_error.restype = C.c_char_p
+        L.phi_default_solver_config.argtypes = [_vp]
+        L.phi_default_solver_config.restype = None
+        L.phi_default_mgrit_config.argtypes = [_vp]
+        L.phi_default_mgrit_config.restype = None
+        L.phi_default_problem.argtypes = [_vp]
+        L.phi_default_problem.restype = None
+        L.phi_set_device.argtypes = [_i]
+        L.phi_disc_build.argtypes = [_i, _i, _vp]
+        L.phi_disc_free.argtypes = [_vp]
+        L.phi_disc_free.restype = None
+        L.phi_disc_info.argtypes = [_vp, _vp]
+        L.phi_disc_export.argtypes = [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.phi_disc_vector.argtypes = [_vp, _i, _vp]
+        L.phi_hier_create.argtypes = [_vp, _d, _vp, _vp]
+        L.phi_hier_free.argtypes = [_vp]
+        L.phi_hier_free.restype = None
+        L.phi_hier_export.argtypes = [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.phi_hier_vcycle.argtypes = [_vp, _vp, _vp, _i, _ll, _i]
+        L.phi_hier_solve.argtypes = [_vp, _vp, _vp, _i, _ll, _d, _i, _i, _i, _vp, _vp, _vp, _i]
+        L.phi_hier_unit.argtypes = [_vp, _i, _i, _i, _vp, _i, _vp, _i]
+        L.phi_stepper_create.argtypes = [_vp, _d, _d, _d, _vp, _vp]
+        L.phi_stepper_free.argtypes = [_vp]
+        L.phi_stepper_free.restype = None
+        L.phi_stepper_step.argtypes = [_vp, _vp, _vp, _vp, _i, _ll, _i, _vp, _i]
+        L.phi_sequential_integrate.argtypes = [_vp, _i, _vp, _vp, _i, _vp, _vp, _vp]
+        L.phi_mgrit_create.argtypes = [_vp, _vp, _vp, _vp, _vp]
+        L.phi_mgrit_free.argtypes = [_vp]
+        L.phi_mgrit_free.restype = None
+        L.phi_mgrit_levels.argtypes = [_vp, _vp, _vp]
+        L.phi_mgrit_solve.argtypes = [_vp, _vp, _vp, _i]
+        L.phi_mgrit_trajectory.argtypes = [_vp, _vp]
+        L.phi_mgrit_initial.argtypes = [_vp, _vp]
+        L.phi_mgrit_initialize.argtypes = [_vp, _vp]
+        L.phi_mgrit_cycle.argtypes = [_vp, _i]
+        L.phi_mgrit_residual_norm.argtypes = [_vp, _i, _vp]
+        L.phi_mgrit_launches.argtypes = [_vp]
+        L.phi_mgrit_launches.restype = _ll
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == PHI_OK:
+        return
+    msg = lib().phi_last_error().decode()
+    if rc == PHI_ERR_INVALID:
+        raise ValueError(msg)
+    if rc == PHI_ERR_NOT_CONVERGED:
+        raise NotConvergedError(msg)
+    raise EngineError(msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_vp)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def default_solver_config(**kw) -> SolverConfig:
+    c = SolverConfig()
+    lib().phi_default_solver_config(C.byref(c))
+    for k, v in kw.items():
+        if k in ("ilut_tau", "ilut_fill", "nu_pre", "nu_post", "gs_pre", "gs_post"):
+            setattr(c.pmg, k, v)
+        else:
+            setattr(c, k, v)
+    return c
+
+
+@dataclass
+class CSR:
+    """Mirror of miga::SparseMatrix (sparse.hpp:17-22)."""
+
+    n_rows: int
+    n_cols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_indices.size)
+
+
+def _fetch(fn, h, which) -> CSR:
+    nr, nc, nnz = _i(), _i(), _i()
+    _check(fn(h, which, C.byref(nr), C.byref(nc), C.byref(nnz), None, None, None))
+    ro = np.zeros(nr.value + 1, np.int32)
+    ci = np.zeros(nnz.value, np.int32)
+    v = np.zeros(nnz.value)
+    _check(fn(h, which, None, None, None, _p(ro), _p(ci), _p(v)))
+    return CSR(nr.value, nc.value, ro, ci, v)
+
+
+class SpatialDiscretization:
+    """SpatialDiscretization::build(unit_square, degree, mesh_exponent) (pmultigrid.hpp:94-158),
+    assembled on the device."""
+
+    def __init__(self, handle):
+        self.h = handle
+        info = np.zeros(5, np.int32)
+        _check(lib().phi_disc_info(self.h, _p(info)))
+        self.n_free, self.n_free_1, self.n_h_levels, self.n_elements, self.degree = map(int, info)
+
+    @classmethod
+    def build(cls, degree: int, mesh_exponent: int) -> "SpatialDiscretization":
+        h = _vp()
+        _check(lib().phi_disc_build(degree, mesh_exponent, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.phi_disc_free(self.h)
+            self.h = None
+
+    def csr(self, which: int) -> CSR:
+        return _fetch(lib().phi_disc_export, self.h, which)
+
+    def vec(self, which: int) -> np.ndarray:
+        out = np.zeros(self.n_free if which == 0 else self.n_free_1)
+        _check(lib().phi_disc_vector(self.h, which, _p(out)))
+        return out
+
+    def operators(self) -> dict:
+        return {
+            "mass_p": self.csr(0), "stiff_p": self.csr(1), "transfer": self.csr(2),
+            "inv_lumped_p": self.vec(0), "inv_lumped_1": self.vec(1),
+            "h_mass": [self.csr(100 + l) for l in range(self.n_h_levels)],
+            "h_stiff": [self.csr(200 + l) for l in range(self.n_h_levels)],
+            "h_embed": [self.csr(300 + l) for l in range(self.n_h_levels - 1)],
+        }
+
+
+class PMultigridHierarchy:
+    """PMultigridHierarchy(disc, c, opt) (pmultigrid.hpp:215-324), device resident."""
+
+    def __init__(self, disc: SpatialDiscretization, c: float, nu_pre=1, nu_post=1, gs_pre=2,
+                 gs_post=2, ilut_tau=1e-13, ilut_fill=0):
+        self.disc = disc
+        self.n = disc.n_free
+        opt = PmgOptions(ilut_tau, ilut_fill, nu_pre, nu_post, gs_pre, gs_post)
+        self.h = _vp()
+        _check(lib().phi_hier_create(disc.h, c, C.byref(opt), C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.phi_hier_free(self.h)
+            self.h = None
+
+    def csr(self, which: int) -> CSR:
+        return _fetch(lib().phi_hier_export, self.h, which)
+
+    def vcycle(self, b, x) -> np.ndarray:
+        b = _f64(b)
+        x = np.array(x, dtype=np.float64, copy=True, order="C")
+        nrhs = 1 if b.ndim == 1 else b.shape[0]
+        _check(lib().phi_hier_vcycle(self.h, _p(b), _p(x), nrhs, self.n, 0))
+        return x
+
+    def solve(self, b, x0=None, rel_tol=1e-12, max_iter=400, fixed_cycles=0):
+        b = _f64(b)
+        nrhs = 1 if b.ndim == 1 else b.shape[0]
+        x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64, copy=True, order="C")
+        it = np.zeros(nrhs, np.int32)
+        cv = np.zeros(nrhs, np.int32)
+        fr = np.zeros(nrhs)
+        _check(lib().phi_hier_solve(self.h, _p(b), _p(x), nrhs, self.n, rel_tol, max_iter,
+                                    fixed_cycles, int(x0 is None), _p(it), _p(cv), _p(fr), 0))
+        if b.ndim == 1:
+            return {"x": x, "iterations": int(it[0]), "converged": bool(cv[0]),
+                    "final_relative_residual": float(fr[0])}
+        return {"x": x, "iterations": it, "converged": cv.astype(bool),
+                "final_relative_residual": fr}
+
+    def _unit(self, op, vin, n_out, out=None, arg=0, arg2=0):
+        vin = _f64(vin)
+        o = np.zeros(n_out) if out is None else np.array(out, dtype=np.float64, copy=True)
+        _check(lib().phi_hier_unit(self.h, op, arg, arg2, _p(vin), vin.size, _p(o), o.size))
+        return o
+
+    def spmv(self, x):
+        return self._unit(0, x, self.n)
+
+    def ilut_apply(self, r):
+        return self._unit(1, r, self.n)
+
+    def restrict_to_linear(self, r):
+        return self._unit(2, r, self.disc.n_free_1)
+
+    def prolong_add(self, e1, x):
+        return self._unit(3, e1, self.n, out=x)
+
+    def prolong_from_linear(self, e1):
+        return self._unit(3, e1, self.n, out=np.zeros(self.n))
+
+    def hmg_wcycle(self, b1, x1=None):
+        return self._unit(4, b1, len(b1), out=np.zeros(len(b1)) if x1 is None else x1)
+
+    def gauss_seidel_sweep(self, level, b, x, backward=False):
+        return self._unit(5, b, len(b), out=x, arg=level, arg2=int(backward))
+
+
+class ThetaStepper:
+    """ThetaStepper(disc, kappa, dt, theta, cfg) (theta.hpp:92-146)."""
+
+    def __init__(self, disc: SpatialDiscretization, kappa: float, dt: float, theta: float,
+                 cfg: SolverConfig | None = None):
+        self.disc = disc
+        self.n = disc.n_free
+        cfg = cfg or default_solver_config()
+        self.h = _vp()
+        _check(lib().phi_stepper_create(disc.h, kappa, dt, theta, C.byref(cfg), C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.phi_stepper_free(self.h)
+            self.h = None
+
+    def step(self, u_prev, load=None, guess=None):
+        """Batched: u_prev (nrhs, n) or (n,); returns Phi(u_prev) + load."""
+        u = _f64(u_prev)
+        nrhs = 1 if u.ndim == 1 else u.shape[0]
+        ld = None if load is None else _f64(np.broadcast_to(load, u.shape))
+        x = np.zeros_like(u) if guess is None else np.array(np.broadcast_to(guess, u.shape),
+                                                              dtype=np.float64, order="C")
+        it = np.zeros(nrhs, np.int32)
+        _check(lib().phi_stepper_step(self.h, _p(u), _p(ld), _p(x), nrhs, self.n,
+                                      int(guess is None), _p(it), 0))
+        return x
+
+    def sequential_integrate(self, nt, u0=None, loads=None, load_steady=False):
+        traj = np.zeros((nt + 1, self.n))
+        u0 = None if u0 is None else _f64(u0)
+        loads = None if loads is None else _f64(loads)
+        s, it = _ll(), _ll()
+        _check(lib().phi_sequential_integrate(self.h, nt, _p(u0), _p(loads), int(load_steady),
+                                              _p(traj), C.byref(s), C.byref(it)))
+        return traj, s.value, it.value
+
+
+@dataclass
+class MgritResult:
+    """MgritResult (mgrit.hpp:33-42), free-dof trajectory."""
+
+    iterations: int
+    converged: bool
+    g_norm: float
+    final_relative_residual: float
+    total_spatial_solves: int
+    mean_spatial_iterations: float
+    residual_history: np.ndarray = field(repr=False)
+
+
+class MgritSolver:
+    """MgritSolver(disc, ps, cfg, scfg) (mgrit.hpp:50-320); space-time state on device."""
+
+    def __init__(self, disc: SpatialDiscretization, nt: int, *, kappa=1.0, t_final=0.1, theta=1.0,
+                 source_kind=SOURCE_CONSTANT, source_param=1.0, init_kind=INIT_ZERO,
+                 init_coeffs=None, load_terms=None, load_terms_steady=False, cycle=CYCLE_V,
+                 relax=RELAX_FCF, m=2, halt_tol=1e-10, max_iter=50, coarse_floor=8,
+                 solver: SolverConfig | None = None):
+        self.disc = disc
+        self.nt = nt
+        self.max_iter = max_iter
+        self._coeffs = None if init_coeffs is None else _f64(init_coeffs)
+        self._loads = None if load_terms is None else _f64(load_terms)
+        ps = Problem(kappa, t_final, theta, nt, source_kind, source_param, init_kind,
+                     None if self._coeffs is None else self._coeffs.ctypes.data,
+                     None if self._loads is None else self._loads.ctypes.data, int(load_terms_steady))
+        cfg = MgritConfig(cycle, relax, m, halt_tol, max_iter, coarse_floor)
+        scfg = solver or default_solver_config()
+        self.h = _vp()
+        _check(lib().phi_mgrit_create(disc.h, C.byref(ps), C.byref(cfg), C.byref(scfg),
+                                      C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.phi_mgrit_free(self.h)
+            self.h = None
+
+    def levels(self):
+        steps = np.zeros(32, np.int32)
+        dts = np.zeros(32)
+        L = lib().phi_mgrit_levels(self.h, _p(steps), _p(dts))
+        return [int(s) for s in steps[:L]], [float(d) for d in dts[:L]]
+
+    def solve(self) -> MgritResult:
+        r = MgritResultC()
+        hist = np.zeros(self.max_iter)
+        _check(lib().phi_mgrit_solve(self.h, C.byref(r), _p(hist), hist.size))
+        return MgritResult(r.iterations, bool(r.converged), r.g_norm, r.final_relative_residual,
+                           r.total_spatial_solves, r.mean_spatial_iterations,
+                           hist[: r.iterations].copy())
+
+    def trajectory(self) -> np.ndarray:
+        out = np.zeros((self.nt + 1, self.disc.n_free))
+        _check(lib().phi_mgrit_trajectory(self.h, _p(out)))
+        return out
+
+    def initial(self) -> np.ndarray:
+        out = np.zeros(self.disc.n_free)
+        _check(lib().phi_mgrit_initial(self.h, _p(out)))
+        return out
+
+    def initialize(self) -> float:
+        g = _d()
+        _check(lib().phi_mgrit_initialize(self.h, C.byref(g)))
+        return g.value
+
+    def mgrit_cycle(self, level=0) -> None:
+        _check(lib().phi_mgrit_cycle(self.h, level))
+
+    def residual_norm(self, level=0) -> float:
+        v = _d()
+        _check(lib().phi_mgrit_residual_norm(self.h, level, C.byref(v)))
+        return v.value
+
+    def launches(self) -> int:
+        return int(lib().phi_mgrit_launches(self.h))
