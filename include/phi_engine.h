@@ -163,6 +163,10 @@ int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out);
 /* kernel launches issued by the last solve() (bench evidence) */
 long long phi_mgrit_launches(const phi_mgrit* g);
 
+/* Developer knob (not part of the reference API): warps used by the sync-free
+ * triangular solves / Gauss-Seidel sweeps and the readiness-poll back-off. */
+int phi_dev_tuning(int tri_warps, int gs_warps, int sleep_ns);
+
 #ifdef __cplusplus
 }
 #endif

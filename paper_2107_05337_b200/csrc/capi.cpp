@@ -547,4 +547,10 @@ int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out) {
 
 long long phi_mgrit_launches(const phi_mgrit* g) { return g->g->launches; }
 
+int phi_dev_tuning(int tri_warps, int gs_warps, int sleep_ns) {
+    return guarded([&] { phi_set_tuning(tri_warps, gs_warps, sleep_ns); });
+}
+
+int phi_dev_trace(long long* out, int n) { return phi_read_trace(out, n); }
+
 }  // extern "C"

@@ -28,18 +28,12 @@ struct DevCsr {
     const double* v;
 };
 
-/// Level-scheduled, lane-interleaved triangular factor (see TriPlan).
+/// Level-scheduled triangular factor as a TMA block stream (TriStream).
 struct DevTri {
-    int n, n_levels;
-    const int* level_chunk;
-    const int* chunk_row0;
-    const int* chunk_nrows;
-    const int* chunk_base;
-    const int* rows;
-    const int* lens;
-    const int* cols;
-    const double* vals;
-    const double* diag;  // upper factor only
+    int n, n_levels, n_blocks;
+    int max_block_bytes, max_items;
+    int prime[6];                 // (off16, bytes) of the first 3 blocks
+    const unsigned char* stream;  // 16-byte aligned
 };
 
 struct DevHLevel {
@@ -69,6 +63,18 @@ struct DevHier {
     double rel_tol;
     int max_iter;
     int fixed_cycles;
+};
+
+/// Shared-memory placement of the latency-critical vectors of one CTA (offsets
+/// in doubles into dynamic shared memory; -1 = global workspace).
+struct SmemPlan {
+    int ring_off;          // triangular-factor block ring (TMA staging)
+    int slot_bytes;        // bytes per ring slot
+    int prod_off;          // triangular-solve product scratch
+    int dot_off;           // ordered-dot scratch
+    int z_off;             // in-place triangular-solve vector (n_p + 1)
+    int lvl_off[kMaxH];    // per h-level: b, x, x2, r (4 n_l)
+    int total;             // doubles
 };
 
 /// Work description of one batched wave of Phi applications (one CTA per
@@ -114,6 +120,7 @@ struct WaveArgs {
     int* conv_out;
     double* rel_out;
     // device counters
+    int* wave_max;             // max p-MG cycles of any point in this launch (nullable)
     unsigned long long* stat;  // [0] solves, [1] iterations
     int* err;                  // [0] flag, [1] first k, [2] level
     double* err_rel;

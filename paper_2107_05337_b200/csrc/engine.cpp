@@ -161,19 +161,24 @@ void Disc::assemble_load(int kind, double c0, double c1, const double* coeffs_de
 // ---------------------------------------------------------------------------
 namespace {
 void upload_tri(const TriPlan& p, Hier::TriDev& d, cudaStream_t s) {
-    d.level_chunk = dev(p.level_chunk, s);
-    d.chunk_row0 = dev(p.chunk_row0, s);
-    d.chunk_nrows = dev(p.chunk_nrows, s);
-    d.chunk_base = dev(p.chunk_base, s);
-    d.rows = dev(p.rows, s);
-    d.lens = dev(p.lens, s);
-    d.cols = dev(p.cols.empty() ? std::vector<int>{0} : p.cols, s);
-    d.vals = dev(p.vals.empty() ? std::vector<double>{0.0} : p.vals, s);
-    if (!p.diag.empty()) d.diag = dev(p.diag, s);
+    const TriStream ts = make_tri_stream(p);
+    static_assert(2 * (kTriSlots - 1) == 6, "DevTri::prime size");
+    d.stream = dev(ts.stream, s);  // cudaMalloc: 256-byte aligned
+    d.n_blocks = ts.n_blocks;
+    d.max_block_bytes = ts.max_block_bytes;
+    d.max_items = ts.max_items;
+    for (int k = 0; k < 6; ++k) d.prime[k] = ts.prime[k];
 }
 DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
-    return DevTri{p.n, p.n_levels, d.level_chunk.get(), d.chunk_row0.get(), d.chunk_nrows.get(),
-                  d.chunk_base.get(), d.rows.get(), d.lens.get(), d.cols.get(), d.vals.get(), d.diag.get()};
+    DevTri t{};
+    t.n = p.n;
+    t.n_levels = p.n_levels;
+    t.n_blocks = d.n_blocks;
+    t.max_block_bytes = d.max_block_bytes;
+    t.max_items = d.max_items;
+    for (int k = 0; k < 6; ++k) t.prime[k] = d.prime[k];
+    t.stream = d.stream.get();
+    return t;
 }
 }  // namespace
 

@@ -97,8 +97,9 @@ public:
     HostCsr L_host, U_host;             // ILUT factors (host copy)
     TriPlan Lp, Up;
     struct TriDev {
-        DevBuf<int> level_chunk, chunk_row0, chunk_nrows, chunk_base, rows, lens, cols;
-        DevBuf<double> vals, diag;
+        DevBuf<unsigned char> stream;
+        int n_blocks = 0, max_block_bytes = 0, max_items = 0;
+        int prime[6] = {0, 0, 0, 0, 0, 0};
     } Ld, Ud;
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;

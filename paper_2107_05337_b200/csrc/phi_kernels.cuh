@@ -12,14 +12,16 @@
 namespace phi {
 
 constexpr int kPhiThreads = 256;
-// Triangular-solve dependency array kept in shared memory up to this size
-// (n_p <= 25,600 rows: configs 1-3); above it the global-memory variant runs.
-constexpr size_t kPhiSmemZMaxBytes = 200 * 1024;
+// Dynamic shared memory one Phi CTA may use for its latency-critical vectors
+// (one CTA per SM; 227 KB is the sm_100 per-block maximum).
+constexpr size_t kPhiSmemBudgetBytes = 220 * 1024;
 
 size_t phi_ws_doubles(const DevHier& H);
-bool phi_smem_z(const DevHier& H);
+SmemPlan phi_smem_plan(const DevHier& H);
 size_t phi_smem_bytes(const DevHier& H);
 int phi_max_slots(const DevHier& H);
+void phi_set_tuning(int tri_warps, int gs_warps, int sleep_ns);
+int phi_read_trace(long long* out, int n);
 
 void launch_phi_wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws,
                      long long ws_stride, int max_slots, cudaStream_t s);

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <functional>
 #include <queue>
 #include <string>
@@ -382,20 +383,23 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
     p.level_chunk.push_back(0);
     for (int lv = 0; lv < p.n_levels; ++lv) {
         const auto& rs = by_level[lv];
-        for (size_t c0 = 0; c0 < rs.size(); c0 += 32) {
-            const int nr = static_cast<int>(std::min<size_t>(32, rs.size() - c0));
+        for (size_t c0 = 0; c0 < rs.size(); c0 += kTriRows) {
+            const int nr = static_cast<int>(std::min<size_t>(kTriRows, rs.size() - c0));
             int maxlen = 0;
             for (int l = 0; l < nr; ++l) {
                 const int i = rs[c0 + l];
                 const int len = m.row_offsets[i + 1] - m.row_offsets[i] - (upper ? 1 : 0);
                 maxlen = std::max(maxlen, len);
             }
-            p.chunk_row0.push_back(static_cast<int>(p.rows.size()));
-            p.chunk_nrows.push_back(nr);
-            p.chunk_base.push_back(static_cast<int>(p.cols.size()));
+            // pad to a whole number (>= 1) of kTriRing-entry blocks
+            const int span = std::max(1, (maxlen + kTriRing - 1) / kTriRing) * kTriRing;
             const size_t base = p.cols.size();
-            p.cols.resize(base + static_cast<size_t>(maxlen) * nr, 0);
-            p.vals.resize(base + static_cast<size_t>(maxlen) * nr, 0.0);
+            p.chunk_meta.push_back(static_cast<int>(p.rows.size()));
+            p.chunk_meta.push_back(nr);
+            p.chunk_meta.push_back(static_cast<int>(base));
+            p.chunk_meta.push_back(span);
+            p.cols.resize(base + static_cast<size_t>(span) * nr, n);  // dummy column n
+            p.vals.resize(base + static_cast<size_t>(span) * nr, 0.0);
             for (int l = 0; l < nr; ++l) {
                 const int i = rs[c0 + l];
                 const int b = m.row_offsets[i] + (upper ? 1 : 0);
@@ -409,9 +413,9 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
                 }
             }
         }
-        p.level_chunk.push_back(static_cast<int>(p.chunk_row0.size()));
+        p.level_chunk.push_back(static_cast<int>(p.chunk_meta.size() / 4));
     }
-    p.n_chunks = static_cast<int>(p.chunk_row0.size());
+    p.n_chunks = static_cast<int>(p.chunk_meta.size() / 4);
     if (upper) {
         p.diag.resize(n);
         for (int i = 0; i < n; ++i) p.diag[i] = m.values[m.row_offsets[i]];
@@ -423,5 +427,65 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
 
 TriPlan plan_lower(const HostCsr& lower) { return make_plan(lower, false); }
 TriPlan plan_upper(const HostCsr& upper) { return make_plan(upper, true); }
+
+TriStream make_tri_stream(const TriPlan& p) {
+    struct Blk {
+        int chunk, span, bytes;
+    };
+    std::vector<Blk> blocks;
+    for (int c = 0; c < p.n_chunks; ++c) {
+        const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1];
+        int maxlen = 0;
+        for (int l = 0; l < nr; ++l) maxlen = std::max(maxlen, p.lens[row0 + l]);
+        const int span = std::max(2, (maxlen + 1) / 2 * 2);  // even: keeps vals 8-byte aligned
+        const int bytes = (kTriBlockPrefix + 12 * nr * span + 15) / 16 * 16;
+        blocks.push_back({c, span, bytes});
+    }
+    TriStream ts;
+    ts.n_blocks = static_cast<int>(blocks.size());
+    std::vector<size_t> off;
+    size_t total = 0;
+    for (const Blk& k : blocks) {
+        off.push_back(total);
+        total += k.bytes;
+        ts.max_block_bytes = std::max(ts.max_block_bytes, k.bytes);
+        ts.max_items = std::max(ts.max_items, k.span * p.chunk_meta[4 * k.chunk + 1]);
+    }
+    ts.stream.assign(total + 16, 0);
+    ts.prime.assign(2 * (kTriSlots - 1), 0);
+    for (int k = 0; k < kTriSlots - 1 && k < ts.n_blocks; ++k) {
+        ts.prime[2 * k] = static_cast<int>(off[k] / 16);
+        ts.prime[2 * k + 1] = blocks[k].bytes;
+    }
+    for (size_t k = 0; k < blocks.size(); ++k) {
+        const Blk& B = blocks[k];
+        const int c = B.chunk;
+        const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
+        unsigned char* dst = ts.stream.data() + off[k];
+        int hdr[8] = {nr, B.span, row0, 0, 0, 0, 0, 0};
+        const size_t nxt = k + kTriSlots - 1;
+        if (nxt < blocks.size()) {
+            hdr[3] = static_cast<int>(off[nxt] / 16);
+            hdr[4] = blocks[nxt].bytes;
+        }
+        std::memcpy(dst, hdr, sizeof hdr);
+        int* rws = reinterpret_cast<int*>(dst + 32);
+        double* dg = reinterpret_cast<double*>(dst + 64);
+        for (int l = 0; l < nr; ++l) {
+            rws[l] = p.rows[row0 + l];
+            dg[l] = p.diag.empty() ? 1.0 : p.diag[p.rows[row0 + l]];
+        }
+        int* cols = reinterpret_cast<int*>(dst + kTriBlockPrefix);
+        double* vals = reinterpret_cast<double*>(dst + kTriBlockPrefix + 4 * nr * B.span);
+        for (int e = 0; e < B.span; ++e)
+            for (int l = 0; l < nr; ++l) {
+                const bool real = e < p.lens[row0 + l];
+                const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * nr + l;
+                cols[e * nr + l] = real ? p.cols[src] : p.n;  // neutral dummy: z[n] = +0.0
+                vals[e * nr + l] = real ? p.vals[src] : 0.0;
+            }
+    }
+    return ts;
+}
 
 }  // namespace phi

@@ -33,7 +33,7 @@ EXPORTED = [
     "phi_stepper_free", "phi_stepper_step", "phi_sequential_integrate", "phi_mgrit_create",
     "phi_mgrit_free", "phi_mgrit_levels", "phi_mgrit_solve", "phi_mgrit_trajectory",
     "phi_mgrit_initial", "phi_mgrit_initialize", "phi_mgrit_cycle", "phi_mgrit_residual_norm",
-    "phi_mgrit_launches",
+    "phi_mgrit_launches", "phi_dev_tuning",
 ]
 
 
@@ -122,6 +122,7 @@ def lib():
         L.phi_mgrit_residual_norm.argtypes = [_vp, _i, _vp]
         L.phi_mgrit_launches.argtypes = [_vp]
         L.phi_mgrit_launches.restype = _ll
+        L.phi_dev_tuning.argtypes = [_i, _i, _i]
         _lib = L
     return _lib
 
@@ -143,6 +144,11 @@ def _p(a):
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def dev_tuning(tri_warps=16, gs_warps=16, sleep_ns=0) -> None:
+    """Developer knob for the sync-free sweeps (see include/phi_engine.h)."""
+    _check(lib().phi_dev_tuning(tri_warps, gs_warps, sleep_ns))
 
 
 def default_solver_config(**kw) -> SolverConfig:
