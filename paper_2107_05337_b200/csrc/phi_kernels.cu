@@ -241,6 +241,7 @@ __device__ __noinline__ void gs_sweep_impl(const DevStencil& A, const double* __
                                            bool backward) {
     const unsigned b_s = SM ? sh_addr(b) : 0u, x_s = SM ? sh_addr(x) : 0u;
     const int nu = A.ru, nv = A.rv, n = nu * nv;
+    const double* __restrict__ av = A.vals;  // cached: A lives in the param space
     const int T = (nu - 1) + 2 * (nv - 1);
     const int tid = threadIdx.x;
     auto row_of = [&](int t, int q, int& iu, int& iv) {
@@ -253,31 +254,30 @@ __device__ __noinline__ void gs_sweep_impl(const DevStencil& A, const double* __
         iv = backward ? nv - 1 - v : v;
         return iu + nu * iv;
     };
+    // Unconditional loads: the stencil-major array stores +0.0 for entries
+    // outside the grid, so no select (which would wait on the fresh load) is
+    // needed, and +0 * +0 leaves the row sum bit-identical.
     auto fetch = [&](int t, double* a) {
         int iu = 0, iv = 0;
-        const int i = t <= T ? row_of(t, tid, iu, iv) : -1;
+        int i = t <= T ? row_of(t, tid, iu, iv) : -1;
+        if (i < 0) i = 0;
 #pragma unroll
-        for (int e = 0; e < 9; ++e) {
-            const int dv = e / 3 - 1, du = e % 3 - 1;
-            const bool ok = i >= 0 && iu + du >= 0 && iu + du < nu && iv + dv >= 0 && iv + dv < nv;
-            a[e] = ok ? __ldg(A.vals + (size_t)e * n + i) : 0.0;
-        }
+        for (int e = 0; e < 9; ++e) a[e] = __ldg(av + (size_t)e * n + i);
     };
     // two register buffers, alternated by a 2x-unrolled wavefront loop, so a
     // prefetched row is never copied (a copy would wait on the fresh load)
     double abuf0[9], abuf1[9];
     auto process = [&](int t, double (&a)[9]) {
+        long long* tr = (c_tune.trace && tid == 0 && t < 1024) ? c_tune.trace + (size_t)NW * 1024 * 2 + (size_t)t * 4
+                                                               : nullptr;
+        if (tr) tr[0] = clock64();
         int iu = 0, iv = 0;
         for (int q = tid;; q += NT) {
             const int i = row_of(t, q, iu, iv);
             if (i < 0) break;
             if (q != tid) {  // rows beyond the first NT of a wavefront: no prefetch
 #pragma unroll
-                for (int e = 0; e < 9; ++e) {
-                    const int dv = e / 3 - 1, du = e % 3 - 1;
-                    const bool ok = iu + du >= 0 && iu + du < nu && iv + dv >= 0 && iv + dv < nv;
-                    a[e] = ok ? __ldg(A.vals + (size_t)e * n + i) : 0.0;
-                }
+                for (int e = 0; e < 9; ++e) a[e] = __ldg(av + (size_t)e * n + i);
             }
             double xv[9];
 #pragma unroll
@@ -294,13 +294,16 @@ __device__ __noinline__ void gs_sweep_impl(const DevStencil& A, const double* __
 #pragma unroll
             for (int e = 0; e < 9; ++e)
                 if (e != 4) s = s - p[e];
+            if (tr && q == tid) tr[1] = clock64() + (long long)(s == 12345.678);  // s is ready
             const double xi = s / a[4];
             if (SM)
                 asm volatile("st.shared.f64 [%0], %1;" ::"r"(x_s + 8u * i), "d"(xi) : "memory");
             else
                 x[i] = xi;
+            if (tr && q == tid) tr[2] = clock64() + (long long)(xi == 12345.678);
         }
         __syncthreads();
+        if (tr) tr[3] = clock64();
     };
     // two register buffers alternated by a 2x-unrolled wavefront loop: a
     // prefetched row is consumed in place, never copied (a copy would wait on
@@ -372,8 +375,11 @@ __device__ __noinline__ void tri_solve_impl(const DevTri& T, double* zg, int z_o
             bulk_fetch(ring + k * slot_bytes, T.stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
                        bar + 8u * k);
     }
+    // cached: T lives in the kernel parameter space (generic loads otherwise)
+    const int n_blocks = T.n_blocks;
+    const unsigned char* __restrict__ stream = T.stream;
     __syncthreads();
-    for (int b = 0; b < T.n_blocks; ++b) {
+    for (int b = 0; b < n_blocks; ++b) {
         const int slot = b % kTriSlots;
         mbar_wait(bar + 8u * slot, (unsigned)(b / kTriSlots) & 1u);
         const unsigned blk = ring + slot * slot_bytes;
@@ -385,7 +391,7 @@ __device__ __noinline__ void tri_solve_impl(const DevTri& T, double* zg, int z_o
             const int next_bytes = lds_s32(blk + 16);
             // block b + kTriSlots - 1 refills the slot released by the last barrier
             if (next_bytes > 0)
-                bulk_fetch(ring + ((b + kTriSlots - 1) % kTriSlots) * slot_bytes, T.stream + (size_t)next_off * 16,
+                bulk_fetch(ring + ((b + kTriSlots - 1) % kTriSlots) * slot_bytes, stream + (size_t)next_off * 16,
                            next_bytes, bar + 8u * ((b + kTriSlots - 1) % kTriSlots));
         }
         const int items = nr * span;
