@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: MGRIT time-to-tolerance of the B200 Phi engine (BASELINE.json metric).
+
+One "step" = one full ``MgritSolver::solve()`` (mgrit.hpp:93-118): IC
+projection, g-norm solves and MGRIT iterations to the 1e-10 halting
+tolerance -- the reference's own timing window (bench.hpp:146-149).  The
+metric is DOF*timesteps/s = n_free * Nt / time-to-tol, whole job over all
+ranks.  Default workload: BASELINE config 2 (p=3, h=2^-6, Nt=1000, two-level
+m=8, transient 2 pi^2 e^-t sin sin source, seeded U[-1,1] spline initial
+coefficients), fp64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl phi|reference]
+
+For N > 1 (torchrun) every rank solves its own independent copy of the
+space-time problem (replicas; the time-sharded NCCL MGRIT driver is not used
+by this bench line), so the scaling is weak.  The reference arm
+(--impl reference) runs the unmodified reference (oracle/_ref, compiled from
+/root/reference) with all host threads on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[0..3]; two-level where the reference builds two levels
+    "c1": dict(p=2, k=4, nt=100, m=4, cycle=2, source_kind=0, source_param=0.0, init_kind=1),
+    "c2": dict(p=3, k=6, nt=1000, m=8, cycle=2, source_kind=1, source_param=2 * np.pi ** 2, init_kind=2),
+    "c3": dict(p=4, k=7, nt=2500, m=4, cycle=0, source_kind=0, source_param=0.0, init_kind=2),
+    "c4": dict(p=5, k=8, nt=10000, m=8, cycle=0, source_kind=1, source_param=2 * np.pi ** 2, init_kind=0),
+}
+SEED = 12345
+
+
+def n_free(cfg):
+    return (2 ** cfg["k"] + cfg["p"] - 2) ** 2
+
+
+def init_coeffs(cfg, rank=0):
+    if cfg["init_kind"] != 2:
+        return None
+    return np.random.default_rng(SEED + rank).uniform(-1.0, 1.0, n_free(cfg))
+
+
+def workload_name(name, cfg):
+    return (f"config{name[1]}: MGRIT p={cfg['p']} h=2^-{cfg['k']} Nt={cfg['nt']} m={cfg['m']} "
+            f"{'two-level' if cfg['cycle'] == 2 else 'V-cycle'} FCF, p-MG V(1,1) ILUT, fp64")
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (reference compiled from /root/reference; oracle restatement as fallback)
+# ---------------------------------------------------------------------------
+def ref_solver(cfg, workers):
+    from oracle import oracle as O
+    return O.RefMgrit(cfg["p"], cfg["k"], cfg["nt"], source_kind=cfg["source_kind"],
+                      source_param=cfg["source_param"], init_kind=cfg["init_kind"],
+                      init_coeffs=init_coeffs(cfg), cycle=cfg["cycle"], m=cfg["m"], workers=workers)
+
+
+def cpu_baseline(cfg):
+    """Reference MGRIT solve() on the box's host cores, bounded sample."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    if not O.ref_available():
+        return {"value": None, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    n, nt = n_free(cfg), cfg["nt"]
+    rm = ref_solver(cfg, cores)
+    if nt * n <= 5_000_000:
+        r = rm.solve()
+        wall = r["wall"]
+        sample = f"full MGRIT solve() ({r['iterations']} iterations), workers={cores}"
+    else:  # too long for the CPU: init + one cycle, extrapolated by the iteration count
+        t_init, t_cyc, _ = rm.partial(1)
+        iters = 8
+        wall = t_init + iters * t_cyc
+        sample = f"initialize() + 1 MGRIT cycle, extrapolated to {iters} iterations, workers={cores}"
+    return {"value": n * nt / wall, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+            "sample": sample, "seconds": wall}
+
+
+def run_reference(args, cfg, name):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    from oracle import oracle as O
+    base = {"metric": "MGRIT time-to-tol, DOF*timesteps/s", "unit": "DOF*timesteps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "impl": "reference", "dtype": "f64", "data": "synthetic (seeded)",
+            "config": {"workload": workload_name(name, cfg), "parallelism": f"{cores} CPU threads"},
+            "vs_baseline": None}
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmiga_ref.so not built"}))
+        return
+    n, nt = n_free(cfg), cfg["nt"]
+    rm = ref_solver(cfg, cores)
+    for _ in range(args.warmup):
+        rm.partial(1)  # warm caches / thread pool; bounded
+    times = []
+    full = nt * n <= 5_000_000
+    for _ in range(args.steps):
+        if full:
+            times.append(rm.solve()["wall"])
+        else:
+            ti, tc, _ = rm.partial(1)
+            times.append(ti + 8 * tc)
+    t = float(np.mean(times))
+    v = n * nt / t
+    base.update({"value": v, "ms_per_step": t * 1e3,
+                 "cpu_baseline": {"value": v, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+                                  "sample": "full MGRIT solve()" if full else
+                                  "initialize() + 1 cycle, extrapolated to 8 iterations"},
+                 "e2e": {"value": v, "unit": "DOF*timesteps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(base), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_phi(args, cfg, name):
+    rank, world, local = dist_env()
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import paper_2107_05337_b200 as P
+    from paper_2107_05337_b200.engine import lib
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    lib().phi_set_device(local)
+
+    n, nt = n_free(cfg), cfg["nt"]
+    coeffs = init_coeffs(cfg, rank)
+    disc = P.SpatialDiscretization.build(cfg["p"], cfg["k"])
+    sol = P.MgritSolver(disc, nt, source_kind=cfg["source_kind"], source_param=cfg["source_param"],
+                        init_kind=cfg["init_kind"], init_coeffs=coeffs, cycle=cfg["cycle"], m=cfg["m"])
+
+    def timed(fn):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        out = fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / 1e3, out
+
+    for _ in range(args.warmup):
+        res = sol.solve()
+
+    # ---- device-resident timed region (value)
+    clocks = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    times, launches = [], 0
+    for _ in range(args.steps):
+        t, res = timed(sol.solve)
+        times.append(t)
+        launches += sol.launches()
+    clk = clocks.stop()
+    barrier(world)
+    t_step = allreduce_max(float(np.mean(times)), world)
+    value = world * n * nt / t_step
+
+    # ---- end to end through the public API with host buffers
+    e2e_steps = max(1, min(args.steps, 2))
+    pinned_in = torch.empty(n, dtype=torch.float64).pin_memory() if coeffs is not None else None
+    pinned_out = torch.empty((nt + 1) * n, dtype=torch.float64).pin_memory()
+    out_np = pinned_out.numpy().reshape(nt + 1, n)
+    from paper_2107_05337_b200.engine import _check, _p
+    import ctypes as C
+
+    def e2e_step():
+        if pinned_in is not None:
+            pinned_in.numpy()[:] = coeffs
+            sol._coeffs = pinned_in.numpy()
+            _check(lib().phi_mgrit_set_init_coeffs(sol.h, C.c_void_p(pinned_in.data_ptr())))
+        r = sol.solve()
+        _check(lib().phi_mgrit_trajectory(sol.h, C.c_void_p(pinned_out.data_ptr())))
+        return r
+
+    barrier(world)
+    e2e_t = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_t.append(time.perf_counter() - t0)
+    t_e2e = allreduce_max(float(np.mean(e2e_t)), world)
+    e2e = {"value": world * n * nt / t_e2e, "unit": "DOF*timesteps/s",
+           "h2d_bytes_per_step": int(8 * n if coeffs is not None else 0),
+           "d2h_bytes_per_step": int(8 * n * (nt + 1)), "ms_per_step": t_e2e * 1e3}
+
+    # ---- roofline of the dominant kernel (phi_wave_kernel), profiled solve
+    sol.set_profile(True)
+    sol.solve()
+    n_waves, wave_ms, wave_bytes = sol.wave_report()
+    sol.set_profile(False)
+    peak, peak_kind = peaks()
+    achieved = wave_bytes / (wave_ms * 1e-3) / 1e9 if wave_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(name)
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "phi_wave_kernel (fused batched Phi solve)", "bound": "hbm", "achieved": achieved,
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "waves": n_waves, "kernel_ms_per_step": wave_ms,
+                "algorithmic_bytes_per_step": wave_bytes,
+                "note": "latency-bound: ILUT level sets and Gauss-Seidel wavefronts are dependent chains"}
+
+    line = {"metric": "MGRIT time-to-tol, DOF*timesteps/s", "value": value, "unit": "DOF*timesteps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] spline coefficients, analytic source)",
+            "config": {"workload": workload_name(name, cfg), "n_free": n, "Nt": nt,
+                       "mgrit_iterations": res.iterations, "spatial_solves": res.total_spatial_solves,
+                       "mean_pmg_cycles": res.mean_spatial_iterations,
+                       "parallelism": f"{world} independent time-parallel solves (replicas)",
+                       "l2": "working set resident; solve() is latency-bound (not flushed)"},
+            "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", 1)))
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="phi", choices=["phi", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, args.config)
+    else:
+        run_phi(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    main()

@@ -162,10 +162,21 @@ int phi_mgrit_cycle(phi_mgrit* g, int level);
 int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out);
 /* kernel launches issued by the last solve() (bench evidence) */
 long long phi_mgrit_launches(const phi_mgrit* g);
+/* replace the spline coefficients of a PHI_INIT_COEFFS problem (host array,
+ * n_free); takes effect at the next solve() / initialize() */
+int phi_mgrit_set_init_coeffs(phi_mgrit* g, const double* coeffs);
+/* per-launch profiling of the Phi waves: when enabled, solve() records CUDA
+ * events around every wave; phi_mgrit_wave_report returns the wave count and
+ * the summed kernel time (ms) and algorithmic bytes (DESIGN.md byte model) */
+int phi_mgrit_profile(phi_mgrit* g, int enable);
+int phi_mgrit_wave_report(phi_mgrit* g, double* ms, double* bytes);
 
 /* Developer knob (not part of the reference API): warps used by the sync-free
  * triangular solves / Gauss-Seidel sweeps and the readiness-poll back-off. */
 int phi_dev_tuning(int tri_warps, int gs_warps, int sleep_ns);
+/* Developer timing trace (enabled by phi_dev_tuning(.., .., -1)): copies up to
+ * n clock64 stamps into out, returns the count. */
+int phi_dev_trace(long long* out, int n);
 
 #ifdef __cplusplus
 }

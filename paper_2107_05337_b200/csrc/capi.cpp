@@ -547,6 +547,20 @@ int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out) {
 
 long long phi_mgrit_launches(const phi_mgrit* g) { return g->g->launches; }
 
+int phi_mgrit_set_init_coeffs(phi_mgrit* g, const double* coeffs) {
+    return guarded([&] { g->g->set_init_coeffs(coeffs); });
+}
+
+int phi_mgrit_profile(phi_mgrit* g, int enable) {
+    return guarded([&] { g->g->profile = enable != 0; });
+}
+
+int phi_mgrit_wave_report(phi_mgrit* g, double* ms, double* bytes) {
+    int n = 0;
+    const int rc = guarded([&] { n = g->g->wave_report(ms, bytes); });
+    return rc == PHI_OK ? n : -rc;
+}
+
 int phi_dev_tuning(int tri_warps, int gs_warps, int sleep_ns) {
     return guarded([&] { phi_set_tuning(tri_warps, gs_warps, sleep_ns); });
 }

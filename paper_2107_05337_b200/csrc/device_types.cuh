@@ -120,7 +120,7 @@ struct WaveArgs {
     int* conv_out;
     double* rel_out;
     // device counters
-    int* wave_max;             // max p-MG cycles of any point in this launch (nullable)
+    int* wave_max;             // per-launch stats (nullable): [0] max cycles, [1] sum, [2] points
     unsigned long long* stat;  // [0] solves, [1] iterations
     int* err;                  // [0] flag, [1] first k, [2] level
     double* err_rel;

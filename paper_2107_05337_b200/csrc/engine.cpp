@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 
@@ -432,7 +434,18 @@ void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, 
     a.err_rel = err_rel.get();
     a.level = l;
     a.x0_empty = mode == kModeSolve ? 1 : 0;  // g-norm solves start from zero (mgrit.hpp:301)
+    const bool rec = profile && recs.size() * 3 < wstats.size();
+    if (rec) {
+        WaveRec r{};
+        r.level = l;
+        PHI_CUDA(cudaEventCreate(&r.start));
+        PHI_CUDA(cudaEventCreate(&r.stop));
+        a.wave_max = wstats.get() + 3 * recs.size();
+        PHI_CUDA(cudaEventRecord(r.start, stream));
+        recs.push_back(r);
+    }
     launch_phi_wave(lv.stepper->H, lv.stepper->Aminus.view(), a, ws.buf.get(), ws.stride, ws.slots, stream);
+    if (rec) PHI_CUDA(cudaEventRecord(recs.back().stop, stream));
     ++launches;
 }
 
@@ -563,8 +576,79 @@ void Mgrit::initialize() {
     g_norm = compute_g_norm();
 }
 
+void Mgrit::set_init_coeffs(const double* host) {
+    if (ps.init_kind != 2) throw InvalidArgument("set_init_coeffs: problem has no coefficient initial condition");
+    std::copy(host, host + disc->n_p, ps.init_coeffs.begin());
+}
+
+namespace {
+// nnz of a stencil operator's valid (in-grid) entries = reference CSR nnz
+long long stencil_nnz(const DevStencil& A) {
+    long long s = 0;
+    for (int iv = 0; iv < A.rv; ++iv) {
+        const int dv = std::min(A.hi, A.cv - 1 - iv) - std::max(A.lo, -iv) + 1;
+        for (int iu = 0; iu < A.ru; ++iu) s += (long long)dv * (std::min(A.hi, A.cu - 1 - iu) - std::max(A.lo, -iu) + 1);
+    }
+    return s;
+}
+}  // namespace
+
+// Algorithmic bytes: 8 B per stored nonzero of the reference
+// operators read once per wave-phase (the batch shares them) plus 8 B per
+// vector entry read or written once per right-hand side.
+int Mgrit::wave_report(double* ms, double* bytes) {
+    *ms = 0.0;
+    *bytes = 0.0;
+    if (recs.empty()) return 0;
+    std::vector<int> st(3 * recs.size());
+    PHI_CUDA(cudaMemcpy(st.data(), wstats.get(), sizeof(int) * st.size(), cudaMemcpyDeviceToHost));
+    const Disc& d = *disc;
+    const double n = d.n_p, n1 = d.n_1;
+    for (size_t k = 0; k < recs.size(); ++k) {
+        float t = 0.f;
+        PHI_CUDA(cudaEventElapsedTime(&t, recs[k].start, recs[k].stop));
+        *ms += t;
+        const Stepper& S = *levels[recs[k].level].stepper;
+        const Hier& H = *S.hier;
+        const double nnzA = (double)stencil_nnz(H.A.view());
+        double vmat = 3 * nnzA + 2.0 * (H.L_host.nnz() + H.U_host.nnz()) + 2.0 * stencil_nnz(d.T.view());
+        double vvec = 18 * n + 3 * n + (n + n1) + (n1 + 2 * n);
+        const int nh = (int)d.h.size();
+        for (int l = 0; l + 1 < nh; ++l) {
+            const double visits = std::ldexp(1.0, l);
+            const double nl = d.h[l].n, nc = d.h[l + 1].n;
+            vmat += visits * (5.0 * stencil_nnz(H.a_h[l].view()) + 2.0 * d.h[l].E.nnz());
+            vvec += visits * (4 * 3 * nl + 3 * nl + (nl + nc) + nc + (nc + 2 * nl));
+        }
+        vmat += std::ldexp(1.0, nh - 1) * (double)H.coarse.n * H.coarse.n;
+        const double cmax = st[3 * k], csum = st[3 * k + 1], pts = st[3 * k + 2];
+        if (std::getenv("PHI_WAVE_DEBUG"))
+            std::fprintf(stderr, "wave %zu level %d: %.3f ms, points %d, cycles sum %d max %d\n", k, recs[k].level,
+                         t, (int)pts, (int)csum, (int)cmax);
+        const double mat = nnzA /* A- */ + (1 + cmax) * nnzA + cmax * vmat;
+        const double vec = pts * (5 * n + 3 * n) + (pts + csum) * 4 * n + csum * vvec;
+        *bytes += 8.0 * (mat + vec);
+    }
+    for (auto& r : recs) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    const int nw = (int)recs.size();
+    recs.clear();
+    return nw;
+}
+
 MgritResultHost Mgrit::solve() {
     launches = 0;
+    for (auto& r : recs) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    recs.clear();
+    if (profile) {
+        if (wstats.size() == 0) wstats.alloc(3 * 8192);
+        wstats.zero(stream);
+    }
     initialize();
     MgritResultHost res;
     res.g_norm = g_norm;

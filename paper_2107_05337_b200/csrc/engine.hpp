@@ -187,6 +187,20 @@ public:
     double g_norm = 0.0;
     long long launches = 0;  // kernels launched by the solve (bench evidence)
 
+    // Optional per-launch profile of the Phi waves (CUDA events on the engine
+    // stream + device counters of p-MG cycles), for the bench's roofline.
+    bool profile = false;
+    struct WaveRec {
+        cudaEvent_t start, stop;
+        int level;
+    };
+    std::vector<WaveRec> recs;
+    DevBuf<int> wstats;  // 3 ints per recorded wave: max cycles, sum cycles, points
+    /// Sum of wave kernel times (ms) and of their algorithmic bytes (DESIGN.md
+    /// section 5 byte model) over the last solve(); returns the wave count.
+    int wave_report(double* ms, double* bytes);
+    void set_init_coeffs(const double* host);
+
 private:
     void build_levels();
     void build_loads();

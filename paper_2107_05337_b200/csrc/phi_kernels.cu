@@ -642,7 +642,11 @@ __device__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs
             atomicAdd(a.stat, 1ULL);
             atomicAdd(a.stat + 1, (unsigned long long)iters);
         }
-        if (a.wave_max) atomicMax(a.wave_max, iters);
+        if (a.wave_max) {
+            atomicMax(a.wave_max, iters);
+            atomicAdd(a.wave_max + 1, iters);
+            atomicAdd(a.wave_max + 2, 1);
+        }
         if (a.iters_out) a.iters_out[task] = iters;
         if (a.conv_out) a.conv_out[task] = conv;
         if (a.rel_out) a.rel_out[task] = rel;

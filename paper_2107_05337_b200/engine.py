@@ -33,7 +33,8 @@ EXPORTED = [
     "phi_stepper_free", "phi_stepper_step", "phi_sequential_integrate", "phi_mgrit_create",
     "phi_mgrit_free", "phi_mgrit_levels", "phi_mgrit_solve", "phi_mgrit_trajectory",
     "phi_mgrit_initial", "phi_mgrit_initialize", "phi_mgrit_cycle", "phi_mgrit_residual_norm",
-    "phi_mgrit_launches", "phi_dev_tuning",
+    "phi_mgrit_launches", "phi_mgrit_set_init_coeffs", "phi_mgrit_profile", "phi_mgrit_wave_report",
+    "phi_dev_tuning", "phi_dev_trace",
 ]
 
 
@@ -123,6 +124,10 @@ def lib():
         L.phi_mgrit_launches.argtypes = [_vp]
         L.phi_mgrit_launches.restype = _ll
         L.phi_dev_tuning.argtypes = [_i, _i, _i]
+        L.phi_dev_trace.argtypes = [_vp, _i]
+        L.phi_mgrit_set_init_coeffs.argtypes = [_vp, _vp]
+        L.phi_mgrit_profile.argtypes = [_vp, _i]
+        L.phi_mgrit_wave_report.argtypes = [_vp, _vp, _vp]
         _lib = L
     return _lib
 
@@ -412,3 +417,18 @@ class MgritSolver:
 
     def launches(self) -> int:
         return int(lib().phi_mgrit_launches(self.h))
+
+    def set_init_coeffs(self, coeffs) -> None:
+        self._coeffs = _f64(coeffs)
+        _check(lib().phi_mgrit_set_init_coeffs(self.h, _p(self._coeffs)))
+
+    def set_profile(self, enable: bool) -> None:
+        _check(lib().phi_mgrit_profile(self.h, int(enable)))
+
+    def wave_report(self):
+        """(waves, kernel ms, algorithmic bytes) of the last profiled solve()."""
+        ms, by = _d(), _d()
+        n = lib().phi_mgrit_wave_report(self.h, C.byref(ms), C.byref(by))
+        if n < 0:
+            _check(-n)
+        return n, ms.value, by.value
