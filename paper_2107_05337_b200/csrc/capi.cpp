@@ -200,6 +200,9 @@ int phi_synchronize(void) {
 // ---- disc -----------------------------------------------------------------
 int phi_disc_build(int degree, int mesh_exponent, phi_disc** out) {
     return guarded([&] {
+        // argument errors come first, as the reference throws before any work
+        if (degree < 1 || degree > 8) throw InvalidArgument("SpatialDiscretization: degree must be in [1, 8]");
+        if (mesh_exponent < 1) throw InvalidArgument("SpatialDiscretization: mesh exponent must be >= 1");
         require_device();
         auto* d = new phi_disc;
         try {
