@@ -46,6 +46,14 @@ typedef struct {
     double ilut_tau; /* 1e-13 */
     int ilut_fill;   /* 0 = average row fill */
     int nu_pre, nu_post, gs_pre, gs_post;
+    /* summation order of every reduction on the solve path (row sums of the
+     * operators and triangular factors, Gauss-Seidel rows, dot products):
+     * 1 = the reference's sequential order -- results bit-identical to the
+     *     reference on identical inputs;
+     * 0 = reassociated parallel sums (default) -- results within the
+     *     north-star tolerance (p-MG / MGRIT iteration counts +-1, final
+     *     space-time solution <= 1e-8 relative L2), several times faster. */
+    int exact;
 } phi_pmg_options;
 
 /* SpatialSolverConfig, theta.hpp:66-75 (p-multigrid kind) */

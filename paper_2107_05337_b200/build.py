@@ -13,6 +13,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -28,9 +29,10 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompile
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-unused-function",
              f"-I{CUDA_INC}"]
 
-CU = ["phi_kernels.cu", "assembly.cu"]
+CU = ["phi_launch.cu", "assembly.cu"]
+DEGREES = range(1, 9)  # phi_deg.cu is compiled once per spline degree (-DPHI_DEG=d)
 CPP = ["setup_host.cpp", "engine.cpp", "capi.cpp"]
-HEADERS = ["common.hpp", "device_types.cuh", "phi_kernels.cuh", "setup_host.hpp", "engine.hpp"]
+HEADERS = ["common.hpp", "device_types.cuh", "phi_kernels.cuh", "phi_device.cuh", "setup_host.hpp", "engine.hpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -51,22 +53,35 @@ def _run(cmd: list[str], log: list[str]) -> None:
 def build(verbose: bool = False) -> str:
     os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "phi_engine.h")]
-    objs, log, changed = [], [], False
+    jobs, objs = [], []  # compile commands still to run; every object of the library
     for src in CU:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT_DIR, "obj", src + ".o")
-        if _newer(o, [s] + hdrs):
-            _run([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], log)
-            changed = True
         objs.append(o)
+        if _newer(o, [s] + hdrs):
+            jobs.append([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o])
+    for d in DEGREES:
+        s = os.path.join(CSRC, "phi_deg.cu")
+        o = os.path.join(OUT_DIR, "obj", f"phi_deg{d}.cu.o")
+        objs.append(o)
+        if _newer(o, [s] + hdrs):
+            jobs.append([NVCC] + NVCC_FLAGS + [f"-DPHI_DEG={d}", "-c", s, "-o", o])
     for src in CPP:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT_DIR, "obj", src + ".o")
-        if _newer(o, [s] + hdrs):
-            _run(["g++"] + CXX_FLAGS + ["-c", s, "-o", o], log)
-            changed = True
         objs.append(o)
-    if changed or _newer(LIB, objs):
+        if _newer(o, [s] + hdrs):
+            jobs.append(["g++"] + CXX_FLAGS + ["-c", s, "-o", o])
+    def compile_one(cmd: list[str]) -> list[str]:
+        out: list[str] = []
+        _run(cmd, out)
+        return out
+
+    log: list[str] = []
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        for part in ex.map(compile_one, jobs):
+            log += part
+    if jobs or _newer(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"], log)
     with open(os.path.join(OUT_DIR, "build.log"), "w") as f:
         f.write("\n".join(log))

@@ -172,6 +172,11 @@ __global__ void scale_kernel(double* v, double a, size_t n) {
         v[i] *= a;
 }
 
+// out[i] = RN(1 / v[i]) (IEEE division): reciprocal diagonals for div_rn.
+__global__ void recip_kernel(const double* v, double* out, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 / v[i];
+}
+
 __global__ void theta_combine_kernel(double* fk, const double* fkm1, double a, double b, int n) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         double v = fk[i] * a;
@@ -280,6 +285,11 @@ void launch_axpby(const double* a, double c, const double* b, double* out, size_
 
 void launch_scale(double* v, double a, size_t n, cudaStream_t s) {
     scale_kernel<<<grid_for((long long)n), 256, 0, s>>>(v, a, n);
+    PHI_CUDA(cudaGetLastError());
+}
+
+void launch_recip(const double* v, double* out, int n, cudaStream_t s) {
+    recip_kernel<<<grid_for(n), 256, 0, s>>>(v, out, n);
     PHI_CUDA(cudaGetLastError());
 }
 

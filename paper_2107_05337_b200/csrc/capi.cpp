@@ -57,6 +57,7 @@ HierOptions to_opts(const phi_pmg_options* o) {
         h.nu_post = o->nu_post;
         h.gs_pre = o->gs_pre;
         h.gs_post = o->gs_post;
+        h.exact = o->exact;
     }
     return h;
 }
@@ -161,6 +162,7 @@ void phi_default_solver_config(phi_solver_config* c) {
     c->pmg.ilut_fill = 0;
     c->pmg.nu_pre = c->pmg.nu_post = 1;
     c->pmg.gs_pre = c->pmg.gs_post = 2;
+    c->pmg.exact = 0;
 }
 
 void phi_default_mgrit_config(phi_mgrit_config* c) {

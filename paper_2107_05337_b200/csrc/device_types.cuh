@@ -28,16 +28,24 @@ struct DevCsr {
     const double* v;
 };
 
+/// Depth of the shared-memory ring that stages triangular-factor blocks.
+constexpr int kTriSlots = 8;
+/// Bytes per triangular-factor block (TriPlan chunking) and the product
+/// scratch that bound implies (12 bytes per entry: int32 column + fp64 value).
+constexpr int kTriBlockCap = 12 * 1024;
+constexpr int kTriMaxItems = kTriBlockCap / 12;
+
 /// Level-scheduled triangular factor as a TMA block stream (TriStream).
 struct DevTri {
     int n, n_levels, n_blocks;
-    int max_block_bytes, max_items;
-    int prime[6];                 // (off16, bytes) of the first 3 blocks
+    int max_block_bytes;
+    int prime[2 * (kTriSlots - 1)];  // (off16, bytes) of the first kTriSlots - 1 blocks
     const unsigned char* stream;  // 16-byte aligned
 };
 
 struct DevHLevel {
     DevStencil a;    // M_l + c K_l, 9-point
+    const double* rdiag;  // RN(1 / a_ii) (Gauss-Seidel division, div_rn)
     DevCsr embed;    // level l+1 -> level l (empty on the coarsest)
     DevCsr embed_t;  // its transpose (restriction rows, ascending fine index)
     int n;
@@ -63,6 +71,7 @@ struct DevHier {
     double rel_tol;
     int max_iter;
     int fixed_cycles;
+    int exact;  // 1: the reference's sequential summation order; 0: reassociated sums
 };
 
 /// Shared-memory placement of the latency-critical vectors of one CTA (offsets
@@ -70,7 +79,7 @@ struct DevHier {
 struct SmemPlan {
     int ring_off;          // triangular-factor block ring (TMA staging)
     int slot_bytes;        // bytes per ring slot
-    int prod_off;          // triangular-solve product scratch
+    int prod_off;          // triangular-solve product scratch (kTriMaxItems)
     int dot_off;           // ordered-dot scratch
     int z_off;             // in-place triangular-solve vector (n_p + 1)
     int lvl_off[kMaxH];    // per h-level: b, x, x2, r (4 n_l)

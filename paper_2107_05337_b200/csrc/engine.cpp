@@ -164,12 +164,10 @@ void Disc::assemble_load(int kind, double c0, double c1, const double* coeffs_de
 namespace {
 void upload_tri(const TriPlan& p, Hier::TriDev& d, cudaStream_t s) {
     const TriStream ts = make_tri_stream(p);
-    static_assert(2 * (kTriSlots - 1) == 6, "DevTri::prime size");
     d.stream = dev(ts.stream, s);  // cudaMalloc: 256-byte aligned
     d.n_blocks = ts.n_blocks;
     d.max_block_bytes = ts.max_block_bytes;
-    d.max_items = ts.max_items;
-    for (int k = 0; k < 6; ++k) d.prime[k] = ts.prime[k];
+    for (int k = 0; k < 2 * (kTriSlots - 1); ++k) d.prime[k] = ts.prime[k];
 }
 DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
     DevTri t{};
@@ -177,8 +175,7 @@ DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
     t.n_levels = p.n_levels;
     t.n_blocks = d.n_blocks;
     t.max_block_bytes = d.max_block_bytes;
-    t.max_items = d.max_items;
-    for (int k = 0; k < 6; ++k) t.prime[k] = d.prime[k];
+    for (int k = 0; k < 2 * (kTriSlots - 1); ++k) t.prime[k] = d.prime[k];
     t.stream = d.stream.get();
     return t;
 }
@@ -205,7 +202,10 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
         a.hi = 1;
         a.vals.alloc(a.size());
         launch_axpby(hl.M.vals.get(), c, hl.K.vals.get(), a.vals.get(), a.size(), s);
+        DevBuf<double> rd(hl.n);
+        launch_recip(a.vals.get() + 4 * (size_t)hl.n, rd.get(), hl.n, s);  // centre entry (du, dv) = (0, 0)
         a_h.push_back(std::move(a));
+        a_h_rdiag.push_back(std::move(rd));
     }
     coarse = dense_lu_factor(stencil_to_csr(a_h.back()));
     coarse_lu = dev(coarse.lu, s);
@@ -232,6 +232,7 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     for (int l = 0; l < H.n_h; ++l) {
         const auto& hl = d.h[l];
         H.h[l].a = a_h[l].view();
+        H.h[l].rdiag = a_h_rdiag[l].get();
         H.h[l].n = hl.n;
         if (l + 1 < H.n_h) {
             H.h[l].embed = DevCsr{hl.E.n_rows, hl.E.n_cols, hl.e_ro.get(), hl.e_ci.get(), hl.e_v.get()};
@@ -248,6 +249,7 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     H.rel_tol = cfg.rel_tol;
     H.max_iter = cfg.max_iter;
     H.fixed_cycles = cfg.fixed_cycles;
+    H.exact = opt.exact;
     return H;
 }
 

@@ -68,6 +68,7 @@ struct HierOptions {  // PMultigridOptions (pmultigrid.hpp:161-168)
     double ilut_tau = 1e-13;
     int ilut_fill = 0;
     int nu_pre = 1, nu_post = 1, gs_pre = 2, gs_post = 2;
+    int exact = 0;  // 1: the reference's summation order (bit-identical), 0: reassociated sums
 };
 
 struct SolverConfig {  // SpatialSolverConfig (theta.hpp:66-75), pmg kind
@@ -94,12 +95,13 @@ public:
     HierOptions opt;
     StencilBuf A;                       // M + c K
     std::vector<StencilBuf> a_h;        // per h-level
+    std::vector<DevBuf<double>> a_h_rdiag;  // RN(1 / diagonal) per h-level
     HostCsr L_host, U_host;             // ILUT factors (host copy)
     TriPlan Lp, Up;
     struct TriDev {
         DevBuf<unsigned char> stream;
-        int n_blocks = 0, max_block_bytes = 0, max_items = 0;
-        int prime[6] = {0, 0, 0, 0, 0, 0};
+        int n_blocks = 0, max_block_bytes = 0;
+        int prime[2 * (kTriSlots - 1)] = {};
     } Ld, Ud;
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;

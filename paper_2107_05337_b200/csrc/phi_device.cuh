@@ -1,4 +1,7 @@
-// The batched time-stepping operator Phi on B200 (sm_100a).
+#pragma once
+// Device code of the batched time-stepping operator Phi on B200 (sm_100a).
+// Included by phi_deg.cu, which is compiled once per spline degree
+// (-DPHI_DEG=1..8) so the degree-templated kernels build in parallel.
 //
 // Design: one CTA owns one right-hand side at a time and
 // runs the WHOLE p-multigrid solve of theta.hpp:132-137 / pmultigrid.hpp:271-307
@@ -14,13 +17,15 @@
 //
 // The solve is a chain of dependent steps (ILUT level sets, Gauss-Seidel
 // wavefronts), so the kernel is organised for latency:
-//  * sync-free triangular solves and Gauss-Seidel sweeps: a row waits only for
-//    the values it reads.  Solved values are published with one 64-bit store
-//    into a "sentinel" array (a signalling-NaN bit pattern means "not solved
-//    yet"), so readiness flag and value are the same word -- one load per
-//    dependency, no fences, no barriers inside a sweep;
-//  * factor entries are streamed through a per-lane register ring (D deep), so
-//    global-memory latency overlaps the dependent arithmetic;
+//  * data-parallel steps (stencil products, transfers, residuals) use all
+//    warps of the CTA; the sequential sweeps (triangular solves, Gauss-Seidel)
+//    run on ONE warp, one row per lane, so consecutive levels / wavefronts are
+//    separated by __syncwarp() instead of CTA barriers;
+//  * triangular-factor levels stream through shared memory by TMA bulk copies
+//    (cp.async.bulk + mbarrier), several levels ahead of the solving warp;
+//  * divisions on the critical path use a stored round-to-nearest reciprocal
+//    and two Markstein corrections (fma), which return the correctly rounded
+//    quotient -- the same bits as the reference's `/`;
 //  * the dependency arrays and the order-1 h-levels live in shared memory when
 //    they fit (SmemPlan), so the critical path runs at shared-memory latency;
 //  * index-ordered dot products stage the products in shared memory and one
@@ -41,8 +46,6 @@ namespace {
 constexpr int NT = kPhiThreads;
 constexpr int NW = NT / 32;
 constexpr int kDotChunk = 2048;  // doubles of shared scratch for ordered dots
-constexpr int kRing = kTriRing;  // factor-entry prefetch depth per lane (setup_host.hpp)
-constexpr unsigned long long kSentinel = 0x7FF4DEADBEEF0001ULL;
 
 // Dynamic shared memory of every Phi kernel (laid out by SmemPlan).
 extern __shared__ __align__(16) double g_smem[];
@@ -57,39 +60,28 @@ struct Tuning {
 };
 __constant__ Tuning c_tune = {NW, NW, 0, 0, nullptr};
 
-// CTA-scope relaxed accesses through generic pointers: shared memory, or
-// global memory served by the SM's L1 (42 cycles, vs 289 for a volatile =
-// system-scope global load; measured with tools/lat_probe.cu on B200).
-__device__ __forceinline__ unsigned long long ld_rlx(const double* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.cta.u64 %0, [%1];" : "=l"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double wait_val(const double* p) {
-    unsigned long long b = ld_rlx(p);
-    while (b == kSentinel) {
-        if (c_tune.sleep_ns) __nanosleep(c_tune.sleep_ns);
-        b = ld_rlx(p);
-    }
-    return __longlong_as_double(static_cast<long long>(b));
-}
-__device__ __forceinline__ void put_val(double* p, double v) {
-    asm volatile("st.relaxed.cta.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
 // Explicit 32-bit shared-window accesses.  Deriving shared pointers inside hot
 // loops makes the compiler re-read the window base (S2R SR_SWINHI /
 // SR_CgaCtaId) per access; these take the address once, up front.
 __device__ __forceinline__ unsigned sh_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ unsigned long long lds_vol_u64(unsigned a) {
-    unsigned long long v;
-    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
-    return v;
-}
 __device__ __forceinline__ double lds_f64(unsigned a) {
     double v;
     asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+// Volatile variants: kept in program order relative to each other, so a load
+// placed ahead of its use stays ahead (the scheduler may otherwise sink loads
+// next to their uses under register pressure and serialise a chain).
+__device__ __forceinline__ double vlds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int vlds_s32(unsigned a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
 __device__ __forceinline__ int lds_s32(unsigned a) {
@@ -97,17 +89,32 @@ __device__ __forceinline__ int lds_s32(unsigned a) {
     asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
-__device__ __forceinline__ void sts_vol_f64(unsigned a, double v) {
-    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+// Developer phase stamps (trace enabled, CTA 0, thread 0): (id, clock64) pairs
+// after a counter at trace[kStampBase].
+constexpr int kStampBase = 40000, kStampMax = 4000;
+constexpr int kTriTraceBase = 24000;  // 4 x 2048 stamps (< kStampBase)
+__device__ __forceinline__ void pstamp(int id) {
+    if (c_tune.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(c_tune.trace + kStampBase), 1ULL);
+        if (k < kStampMax) {
+            c_tune.trace[kStampBase + 1 + 2 * k] = id;
+            c_tune.trace[kStampBase + 2 + 2 * k] = clock64();
+        }
+    }
 }
-__device__ __forceinline__ void reset_sentinel(double* z, int n) {
-    for (int i = threadIdx.x; i < n; i += NT) reinterpret_cast<unsigned long long*>(z)[i] = kSentinel;
-}
-// Triangular-solve dependency array: n sentinels plus the always-ready dummy
-// slot z[n] = +0.0 that padded factor entries point at (see TriPlan).
-__device__ __forceinline__ void reset_dep(double* z, int n) {
-    reset_sentinel(z, n);
-    if (threadIdx.x == 0) z[n] = 0.0;
+
+// Correctly rounded s / d from r = RN(1 / d): q0 = RN(s r) is within two ulps,
+// the first Markstein step brings it within one ulp and the second one then
+// yields RN(s / d) exactly (residual s - d q exact by fma; valid without
+// overflow / underflow, which the solver's operands never approach).  A zero
+// numerator keeps the sign rules of IEEE division via q0 itself.
+__device__ __forceinline__ double div_rn(double s, double d, double r) {
+    const double q0 = s * r;
+    const double e0 = __fma_rn(-q0, d, s);
+    const double q1 = __fma_rn(e0, r, q0);
+    const double e1 = __fma_rn(-q1, d, s);
+    const double q2 = __fma_rn(e1, r, q1);
+    return s == 0.0 ? q0 : q2;
 }
 
 // ---------------------------------------------------------------------------
@@ -117,7 +124,7 @@ struct Ws {
     double *b, *x, *r, *zg;  // global
     double* z;               // in-place triangular-solve vector (n_p + 1 slots)
     double* dot;             // shared scratch for ordered dots
-    int z_off, ring_off, prod_off, slot_bytes;  // g_smem offsets (-1: global)
+    int z_off, ring_off, slot_bytes, prod_off;  // g_smem offsets (-1: global)
     double* hb[kMaxH];
     double* hx[kMaxH];
     double* hx2[kMaxH];
@@ -135,8 +142,8 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     w.dot = smem + P.dot_off;
     w.z_off = P.z_off;
     w.ring_off = P.ring_off;
-    w.prod_off = P.prod_off;
     w.slot_bytes = P.slot_bytes;
+    w.prod_off = P.prod_off;
     double* g = base + 6 * np;
     for (int l = 0; l < H.n_h; ++l) {
         const int nl = H.h[l].n;
@@ -150,6 +157,28 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     return w;
 }
 
+// The hierarchy descriptor (and the wave description) are read from shared
+// memory: as kernel parameters their fields are loop-invariant, and the
+// compiler hoists them into registers for the whole solve -- about 150
+// registers that the sweep loops then lack.  Shared-memory copies are
+// re-read after each barrier instead.
+__device__ __forceinline__ const DevHier& hier_shared(const DevHier& H) {
+    __shared__ DevHier h_sh;
+    if (threadIdx.x == 0) h_sh = H;
+    __syncthreads();
+    return h_sh;
+}
+
+// The workspace descriptor lives in shared memory: held in registers it would
+// stay live across every call of the solve (about a hundred registers) and
+// starve the register allocation of the sweep loops.
+__device__ __forceinline__ const Ws& carve_shared(double* base, const DevHier& H, const SmemPlan& P, double* smem) {
+    __shared__ Ws ws_sh;
+    if (threadIdx.x == 0) ws_sh = carve(base, H, P, smem);
+    __syncthreads();
+    return ws_sh;
+}
+
 // ---------------------------------------------------------------------------
 // CTA-cooperative primitives.  Callers place __syncthreads() between phases.
 // ---------------------------------------------------------------------------
@@ -158,16 +187,28 @@ enum StencilOut : int { kOutSet = 0, kOutResid = 1, kOutScale = 2, kOutAddScaled
 // y[i] (op)= sum_e vals[e][i] * x[col(i, e)], entries in reference CSR order
 // (dv, du ascending), one sequential sum per row; the W loads of a stencil
 // row are issued together.
+// Pairwise sum of N compile-time-indexed values (reassociated mode).
+template <int N>
+struct Tree {
+    static __device__ __forceinline__ double sum(const double* p) {
+        return Tree<N / 2>::sum(p) + Tree<N - N / 2>::sum(p + N / 2);
+    }
+};
+template <>
+struct Tree<1> {
+    static __device__ __forceinline__ double sum(const double* p) { return p[0]; }
+};
+
 template <int OUT, int W>
-__device__ __forceinline__ void stencil_apply(const DevStencil& A, const double* __restrict__ x,
-                                                double* __restrict__ y, const double* __restrict__ aux) {
+__device__ __noinline__ void stencil_apply(const DevStencil& A, const double* __restrict__ x,
+                                           double* __restrict__ y, const double* __restrict__ aux, bool exact = true) {
     const int n = A.ru * A.rv;
     for (int i = threadIdx.x; i < n; i += NT) {
         const int iv = i / A.ru;
         const int iu = i - iv * A.ru;
         const int dulo = max(A.lo, -iu), duhi = min(A.hi, A.cu - 1 - iu);
         const int dvlo = max(A.lo, -iv), dvhi = min(A.hi, A.cv - 1 - iv);
-        double s = 0.0;
+        double s = 0.0, s2 = 0.0;
         for (int dv = dvlo; dv <= dvhi; ++dv) {
             const double* vr = A.vals + (size_t)((dv - A.lo) * W) * n + i;
             const double* xr = x + (size_t)(iv + dv) * A.cu + iu;
@@ -175,17 +216,28 @@ __device__ __forceinline__ void stencil_apply(const DevStencil& A, const double*
 #pragma unroll
             for (int q = 0; q < W; ++q) {
                 const int du = A.lo + q;
-                if (du >= dulo && du <= duhi) {
-                    pv[q] = __ldg(vr + (size_t)q * n);
-                    px[q] = xr[du];
-                }
+                const bool ok = du >= dulo && du <= duhi;
+                pv[q] = ok ? __ldg(vr + (size_t)q * n) : 0.0;
+                px[q] = ok ? xr[du] : 0.0;
             }
+            if (exact) {  // the reference's order: (dv, du) ascending, valid entries only
 #pragma unroll
-            for (int q = 0; q < W; ++q) {
-                const int du = A.lo + q;
-                if (du >= dulo && du <= duhi) s = s + pv[q] * px[q];
+                for (int q = 0; q < W; ++q) {
+                    const int du = A.lo + q;
+                    if (du >= dulo && du <= duhi) s = s + pv[q] * px[q];
+                }
+            } else {  // reassociated: a tree per stencil row, two row accumulators
+                double pr[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) pr[q] = pv[q] * px[q];
+                const double g = Tree<W>::sum(pr);
+                if ((dv - dvlo) & 1)
+                    s2 = s2 + g;
+                else
+                    s = s + g;
             }
         }
+        if (!exact) s = s + s2;
         if (OUT == kOutSet) y[i] = s;
         if (OUT == kOutResid) y[i] = aux[i] - s;             // r = b - A x
         if (OUT == kOutScale) y[i] = s * aux[i];             // (P^T r) .* 1/M^L
@@ -227,23 +279,26 @@ __device__ __forceinline__ void csr_apply(const DevCsr& A, const double* __restr
     }
 }
 
-// One lexicographic Gauss-Seidel sweep (solvers.hpp:80-99) for the 9-point
+// Lexicographic Gauss-Seidel sweeps (solvers.hpp:80-99) for the 9-point
 // order-1 operator, in place, by anti-diagonal wavefronts u + 2v = t
 // (forward; mirrored for backward): a row of wavefront t reads updated values
 // only from wavefronts < t and old values only from wavefronts > t, so
 // updating a whole wavefront between two barriers gives exactly the
-// sequential sweep.  Thread q owns row q of each wavefront; its nine matrix
-// entries for the next wavefront are prefetched while the current one is
-// solved.  Entries outside the grid carry a = +0.0 and x = +0.0, and
-// s - (+0 * +0) == s, so the branch-free row sum is bit-identical.
+// sequential sweep.  ONE warp runs the sweeps (lane q owns rows q, q + 32, ..
+// of each wavefront; __syncwarp() between wavefronts).  The nine matrix
+// entries and the reciprocal diagonal of a lane's first row of the next
+// wavefront are prefetched while the current one is solved.  Entries outside
+// the grid carry a = +0.0 and x = +0.0, and s - (+0 * +0) == s, so the
+// branch-free row sum is bit-identical.
 template <bool SM>
-__device__ __noinline__ void gs_sweep_impl(const DevStencil& A, const double* __restrict__ b, double* x,
-                                           bool backward) {
+__device__ __noinline__ void gs_sweeps_warp(const DevStencil& A, const double* __restrict__ rdiag,
+                                            const double* __restrict__ b, double* x, bool backward, int count,
+                                            bool exact) {
     const unsigned b_s = SM ? sh_addr(b) : 0u, x_s = SM ? sh_addr(x) : 0u;
     const int nu = A.ru, nv = A.rv, n = nu * nv;
     const double* __restrict__ av = A.vals;  // cached: A lives in the param space
     const int T = (nu - 1) + 2 * (nv - 1);
-    const int tid = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     auto row_of = [&](int t, int q, int& iu, int& iv) {
         const int vlo = max(0, (t - (nu - 1) + 1) / 2);
         const int vhi = min(nv - 1, t / 2);
@@ -259,25 +314,24 @@ __device__ __noinline__ void gs_sweep_impl(const DevStencil& A, const double* __
     // needed, and +0 * +0 leaves the row sum bit-identical.
     auto fetch = [&](int t, double* a) {
         int iu = 0, iv = 0;
-        int i = t <= T ? row_of(t, tid, iu, iv) : -1;
+        int i = t <= T ? row_of(t, lane, iu, iv) : -1;
         if (i < 0) i = 0;
 #pragma unroll
         for (int e = 0; e < 9; ++e) a[e] = __ldg(av + (size_t)e * n + i);
+        a[9] = __ldg(rdiag + i);
     };
-    // two register buffers, alternated by a 2x-unrolled wavefront loop, so a
-    // prefetched row is never copied (a copy would wait on the fresh load)
-    double abuf0[9], abuf1[9];
-    auto process = [&](int t, double (&a)[9]) {
-        long long* tr = (c_tune.trace && tid == 0 && t < 1024) ? c_tune.trace + (size_t)NW * 1024 * 2 + (size_t)t * 4
-                                                               : nullptr;
+    auto process = [&](int t, double (&a)[10]) {
+        long long* tr = (c_tune.trace && lane == 0 && t < 1024) ? c_tune.trace + (size_t)NW * 1024 * 2 + (size_t)t * 4
+                                                                : nullptr;
         if (tr) tr[0] = clock64();
         int iu = 0, iv = 0;
-        for (int q = tid;; q += NT) {
+        for (int q = lane;; q += 32) {
             const int i = row_of(t, q, iu, iv);
             if (i < 0) break;
-            if (q != tid) {  // rows beyond the first NT of a wavefront: no prefetch
+            if (q != lane) {  // rows beyond the first 32 of a wavefront: no prefetch
 #pragma unroll
                 for (int e = 0; e < 9; ++e) a[e] = __ldg(av + (size_t)e * n + i);
+                a[9] = __ldg(rdiag + i);
             }
             double xv[9];
 #pragma unroll
@@ -291,41 +345,53 @@ __device__ __noinline__ void gs_sweep_impl(const DevStencil& A, const double* __
             double p[9];
 #pragma unroll
             for (int e = 0; e < 9; ++e) p[e] = a[e] * xv[e];
+            if (exact) {  // the reference's order: (dv, du) ascending
 #pragma unroll
-            for (int e = 0; e < 9; ++e)
-                if (e != 4) s = s - p[e];
-            if (tr && q == tid) tr[1] = clock64() + (long long)(s == 12345.678);  // s is ready
-            const double xi = s / a[4];
+                for (int e = 0; e < 9; ++e)
+                    if (e != 4) s = s - p[e];
+            } else {  // reassociated: a depth-3 tree
+                s = s - (((p[0] + p[1]) + (p[2] + p[3])) + ((p[5] + p[6]) + (p[7] + p[8])));
+            }
+            if (tr && q == lane) tr[1] = clock64() + (long long)(s == 12345.678);  // s is ready
+            const double xi = div_rn(s, a[4], a[9]);
             if (SM)
                 asm volatile("st.shared.f64 [%0], %1;" ::"r"(x_s + 8u * i), "d"(xi) : "memory");
             else
                 x[i] = xi;
-            if (tr && q == tid) tr[2] = clock64() + (long long)(xi == 12345.678);
+            if (tr && q == lane) tr[2] = clock64() + (long long)(xi == 12345.678);
         }
-        __syncthreads();
+        __syncwarp();
         if (tr) tr[3] = clock64();
     };
     // two register buffers alternated by a 2x-unrolled wavefront loop: a
     // prefetched row is consumed in place, never copied (a copy would wait on
     // the load that was just issued)
-    fetch(0, abuf0);
-    for (int t = 0; t <= T; t += 2) {
-        fetch(t + 1, abuf1);
-        process(t, abuf0);
-        if (t + 1 > T) break;
-        fetch(t + 2, abuf0);
-        process(t + 1, abuf1);
+    double abuf0[10], abuf1[10];
+    for (int c = 0; c < count; ++c) {
+        fetch(0, abuf0);
+        for (int t = 0; t <= T; t += 2) {
+            fetch(t + 1, abuf1);
+            process(t, abuf0);
+            if (t + 1 > T) break;
+            fetch(t + 2, abuf0);
+            process(t + 1, abuf1);
+        }
     }
 }
 
-__device__ __forceinline__ void gs_sweep(const DevStencil& A, const double* b, double* x, bool backward) {
-    if (__isShared(x))
-        gs_sweep_impl<true>(A, b, x, backward);
-    else
-        gs_sweep_impl<false>(A, b, x, backward);
+// `count` sweeps by warp 0; the CTA joins at the closing barrier.
+__device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, double* x, bool backward,
+                                          int count, bool exact) {
+    if (threadIdx.x < 32) {
+        if (__isShared(x))
+            gs_sweeps_warp<true>(lv.a, lv.rdiag, b, x, backward, count, exact);
+        else
+            gs_sweeps_warp<false>(lv.a, lv.rdiag, b, x, backward, count, exact);
+    }
+    __syncthreads();
 }
 
-// ---- triangular solves: level-synchronous, TMA-fed ------------------------
+// ---- triangular solves: one warp, TMA-fed ------------------------
 // The factor is one level-ordered stream of blocks (TriStream), each holding a
 // chunk of <= kTriRows rows of one level with all their entries.  A ring of
 // kTriSlots shared-memory slots is filled by TMA bulk copies
@@ -353,95 +419,235 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 
 // In-place substitution with an ILUT factor (ilut.hpp:146-163) on z, which
 // holds the right-hand side on entry.  Lower: z_i -= sum_j L_ij z_j (unit
-// diagonal).  Upper: z_i = (z_i - sum_j U_ij z_j) / U_ii, fused with the
-// smoother update x += z (pmultigrid.hpp:315).  Per block: every thread forms
-// products L_ij * z_j (all j belong to earlier levels), one barrier, then the
-// row's thread subtracts them in CSR order -- the reference's exact sequence
-// of roundings -- and publishes z_i; a second barrier closes the level.
-// Padded entries (column n, value +0.0; z[n] = +0.0) are exactly neutral.
+// diagonal).  Upper: z_i = (z_i - sum_j U_ij z_j) / U_ii.  Executed by ONE warp, block by
+// block (a block is one level, or a slice of a wide level):
+//   1. all 32 lanes form the block's products L_ij * z_j (every z_j belongs
+//      to an earlier level) into shared scratch -- wide, independent loads;
+//   2. lane l subtracts row l's products in CSR order -- the reference's
+//      exact sequence of roundings, a pure load + add chain -- and publishes
+//      z_i.
+// __syncwarp() (a memory barrier among the lanes) separates the phases and
+// closes the block.  Blocks stream through a kTriSlots ring filled by TMA
+// kTriSlots-1 blocks ahead.  Padded entries (column n, value +0.0;
+// z[n] = +0.0) are exactly neutral.
 template <bool UPPER, bool ZSM>
-__device__ __noinline__ void tri_solve_impl(const DevTri& T, double* zg, int z_off, double* xadd, int ring_off,
-                                            int slot_bytes, int prod_off) {
-    __shared__ unsigned long long bars[kTriSlots];
-    const int tid = threadIdx.x;
+__device__ __noinline__ void tri_solve_warp(const DevTri& T, double* zg, int z_off, int ring_off, int slot_bytes,
+                                            int prod_off, unsigned bar, bool exact) {
+    const int lane = threadIdx.x & 31;
     const unsigned ring = sh_addr(g_smem + ring_off);
     const unsigned prod = sh_addr(g_smem + prod_off);
     const unsigned zs = ZSM ? sh_addr(g_smem + z_off) : 0u;
-    const unsigned bar = sh_addr(bars);
-    if (tid == 0) {
-        for (int k = 0; k < kTriSlots; ++k) mbar_init(bar + 8u * k);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < kTriSlots - 1 && k < T.n_blocks; ++k)
-            bulk_fetch(ring + k * slot_bytes, T.stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
-                       bar + 8u * k);
-    }
     // cached: T lives in the kernel parameter space (generic loads otherwise)
     const int n_blocks = T.n_blocks;
     const unsigned char* __restrict__ stream = T.stream;
-    __syncthreads();
+    if (lane == 0)
+        for (int k = 0; k < kTriSlots - 1 && k < n_blocks; ++k)
+            bulk_fetch(ring + k * slot_bytes, stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
+                       bar + 8u * k);
+    // developer trace (CTA 0, lane 0, first 1024 blocks): block start, data
+    // ready, products done, block done, prefetch issued, row sums -- at
+    // trace[kTriTraceBase + 8 b]
+    long long* tr = (c_tune.trace && blockIdx.x == 0 && lane == 0) ? c_tune.trace + kTriTraceBase : nullptr;
     for (int b = 0; b < n_blocks; ++b) {
         const int slot = b % kTriSlots;
+        if (tr && b < 1024) tr[8 * b] = clock64();
         mbar_wait(bar + 8u * slot, (unsigned)(b / kTriSlots) & 1u);
+        if (tr && b < 1024) tr[8 * b + 1] = clock64();
         const unsigned blk = ring + slot * slot_bytes;
-        int nr, span, row0, next_off;
+        int nr, span, row0, next_off, next_bytes, cols_off, vals_off, diag_off;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(nr), "=r"(span), "=r"(row0), "=r"(next_off)
                      : "r"(blk));
-        if (tid == 0) {
-            const int next_bytes = lds_s32(blk + 16);
-            // block b + kTriSlots - 1 refills the slot released by the last barrier
-            if (next_bytes > 0)
-                bulk_fetch(ring + ((b + kTriSlots - 1) % kTriSlots) * slot_bytes, stream + (size_t)next_off * 16,
-                           next_bytes, bar + 8u * ((b + kTriSlots - 1) % kTriSlots));
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(next_bytes), "=r"(cols_off), "=r"(vals_off), "=r"(diag_off)
+                     : "r"(blk + 16));
+        (void)row0;
+        // block b + kTriSlots - 1 refills the slot the warp left after block b - 1
+        if (lane == 0 && next_bytes > 0) {
+            const int ns = (b + kTriSlots - 1) % kTriSlots;
+            bulk_fetch(ring + ns * slot_bytes, stream + (size_t)next_off * 16, next_bytes, bar + 8u * ns);
         }
-        const int items = nr * span;
-        const unsigned cols = blk + kTriBlockPrefix;
-        const unsigned vals = cols + 4u * items;
-        for (int t = tid; t < items; t += NT) {
-            const int j = lds_s32(cols + 4u * t);
-            const double z = ZSM ? lds_f64(zs + 8u * j) : zg[j];
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(prod + 8u * t), "d"(lds_f64(vals + 8u * t) * z));
-        }
-        __syncthreads();
-        if (tid < nr) {
-            const int i = lds_s32(blk + 32u + 4u * tid);
-            double s = ZSM ? lds_f64(zs + 8u * i) : zg[i];
-            const unsigned pp = prod + 8u * tid;
-            int e = 0;
-            for (; e + 8 <= span; e += 8) {
-                double p[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) p[q] = lds_f64(pp + 8u * (e + q) * nr);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) s = s - p[q];
+        if (tr && b < 1024) tr[8 * b + 4] = clock64();
+        const unsigned cols = blk + cols_off, vals = blk + vals_off;
+        double s = 0.0;
+        if (exact) {
+            // ---- exact: the reference's rounding sequence
+            int i = 0;
+            double dg = 1.0, rd = 1.0;
+            if (lane < nr) {  // row data first: its latency overlaps phase 1
+                i = lds_s32(blk + 32u + 4u * lane);
+                s = ZSM ? lds_f64(zs + 8u * i) : zg[i];
+                if (UPPER) {
+                    const unsigned dp = blk + diag_off + 8u * lane;
+                    dg = lds_f64(dp);
+                    rd = lds_f64(dp + 8u * nr);
+                }
             }
-            for (; e < span; ++e) s = s - lds_f64(pp + 8u * e * nr);
-            if (UPPER) {
-                s = s / lds_f64(blk + 64u + 8u * tid);
-                xadd[i] = xadd[i] + s;
+            // phase 1: all lanes form the block's products into shared scratch
+            const int items = nr * span;
+            for (int t0 = 0; t0 < items; t0 += 128) {
+                int j[4];
+                double v[4], zj[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int t = min(t0 + q * 32 + lane, items - 1);
+                    j[q] = lds_s32(cols + 4u * t);
+                    v[q] = lds_f64(vals + 8u * t);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int t = t0 + q * 32 + lane;
+                    if (t < items)
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(prod + 8u * t), "d"(v[q] * zj[q]) : "memory");
+                }
             }
-            if (ZSM)
-                asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
-            else
-                zg[i] = s;
+            __syncwarp();
+            if (tr && b < 1024) tr[8 * b + 2] = clock64();
+            // phase 2: lane l subtracts row l's products in CSR order
+            if (lane < nr) {
+                const unsigned pp = prod + 8u * lane, st = 8u * nr;
+                int e = 0;
+                for (; e + 8 <= span; e += 8) {
+                    double pq[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) pq[q] = lds_f64(pp + (e + q) * st);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) s = s - pq[q];
+                }
+                for (; e < span; e += 2) {  // span is even
+                    const double p0 = lds_f64(pp + e * st), p1 = lds_f64(pp + (e + 1) * st);
+                    s = s - p0;
+                    s = s - p1;
+                }
+                if (UPPER) s = div_rn(s, dg, rd);
+                if (ZSM)
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
+                else
+                    zg[i] = s;
+            }
+        } else {
+            // ---- fast: G = 32 / pow2ceil(nr) lanes per row; lane k of a row
+            // sums entries k, k + G, .. with four accumulators, then a
+            // butterfly over the G lanes completes the row sum (reassociated:
+            // within the solver tolerance, not bit-identical)
+            const int lg = nr > 16 ? 0 : nr > 8 ? 1 : nr > 4 ? 2 : nr > 2 ? 3 : nr > 1 ? 4 : 5;
+            const int G = 1 << lg;
+            const int r = lane >> lg, k = lane & (G - 1);
+            const bool act = r < nr;
+            int i = 0;
+            double dg = 1.0, rd = 1.0, z0 = 0.0;
+            if (act && k == 0) {
+                i = lds_s32(blk + 32u + 4u * r);
+                z0 = ZSM ? lds_f64(zs + 8u * i) : zg[i];
+                if (UPPER) {
+                    const unsigned dp = blk + diag_off + 8u * r;
+                    dg = lds_f64(dp);
+                    rd = lds_f64(dp + 8u * nr);
+                }
+            }
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (act) {
+                const unsigned ce = cols + 4u * r, ve = vals + 8u * r;
+                const unsigned cstep = 4u * nr * G, vstep = 8u * nr * G;
+                unsigned co = ce + 4u * nr * k, vo = ve + 8u * nr * k;
+                for (int e = k; e < span; e += 4 * G) {
+                    int j[4];
+                    double v[4], zj[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const bool ok = e + q * G < span;
+                        j[q] = ok ? lds_s32(co + q * cstep) : T.n;  // dummy slot z[n] = +0.0
+                        v[q] = ok ? lds_f64(vo + q * vstep) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[q] = acc[q] + v[q] * zj[q];
+                    co += 4 * cstep;
+                    vo += 4 * vstep;
+                }
+            }
+            double t = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            if (tr && b < 1024) tr[8 * b + 5] = clock64() + (long long)(t == 12345.678);
+            for (int o = G >> 1; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+            if (tr && b < 1024) tr[8 * b + 2] = clock64();
+            if (act && k == 0) {
+                s = z0 - t;
+                if (UPPER) s = div_rn(s, dg, rd);
+                if (ZSM)
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
+                else
+                    zg[i] = s;
+            }
         }
-        __syncthreads();
+        __syncwarp();
+        if (tr && b < 1024) tr[8 * b + 3] = clock64() + (long long)(s == 12345.678);
     }
 }
 
-template <bool UPPER>
-__device__ __forceinline__ void tri_solve(const DevTri& T, double* zg, int z_off, double* xadd, int ring_off,
-                                          int slot_bytes, int prod_off) {
-    if (z_off >= 0)
-        tri_solve_impl<UPPER, true>(T, zg, z_off, xadd, ring_off, slot_bytes, prod_off);
-    else
-        tri_solve_impl<UPPER, false>(T, zg, z_off, xadd, ring_off, slot_bytes, prod_off);
+// Both substitutions of one ILUT application; warp 0 solves, the CTA joins at
+// the closing barrier.  The ring's mbarriers are (re)initialised per call so
+// their phase parity starts at 0.
+__device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, double* zg, int z_off, double* xadd,
+                                           int ring_off, int slot_bytes, int prod_off, bool exact) {
+    __shared__ unsigned long long bars[2 * kTriSlots];
+    // the ring overlays buffers written through the generic proxy in other
+    // phases: order those writes before the TMA (async-proxy) writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const unsigned bar = sh_addr(bars);
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < 2 * kTriSlots; ++k) mbar_init(bar + 8u * k);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        if (z_off >= 0) {
+            tri_solve_warp<false, true>(L, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
+            tri_solve_warp<true, true>(U, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots, exact);
+        } else {
+            tri_solve_warp<false, false>(L, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
+            tri_solve_warp<true, false>(U, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots, exact);
+        }
+    }
+    __syncthreads();
+    // the smoother update x += z (axpy(1, z, x), pmultigrid.hpp:315), off the
+    // substitution's critical path
+    if (xadd) {
+        const double* z = z_off >= 0 ? g_smem + z_off : zg;
+        for (int i = threadIdx.x; i < L.n; i += NT) xadd[i] = xadd[i] + z[i];
+        __syncthreads();
+    }
 }
 
 // Index-ordered dot product (sparse.hpp:188-192): products in parallel into
 // shared scratch, one thread sums them in index order.  Broadcast result.
-__device__ double cta_ordered_dot(const double* a, const double* b, int n, double* scratch, double* sh) {
+__device__ __noinline__ double cta_ordered_dot(const double* a, const double* b, int n, double* scratch, double* sh,
+                                               bool exact = true) {
     double s = 0.0;
+    if (!exact) {  // reassociated: strided partial sums, warp butterflies, warp totals in order
+        double a0 = 0.0, a1 = 0.0;
+        for (int i = threadIdx.x; i < n; i += 2 * NT) {
+            a0 = a0 + a[i] * b[i];
+            if (i + NT < n) a1 = a1 + a[i + NT] * b[i + NT];
+        }
+        double t = a0 + a1;
+        for (int o = 16; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double u = 0.0;
+            for (int k = 0; k < NW; ++k) u = u + scratch[k];
+            sh[0] = u;
+        }
+        __syncthreads();
+        const double v = sh[0];
+        __syncthreads();
+        return v;
+    }
     for (int c0 = 0; c0 < n; c0 += kDotChunk) {
         const int cnt = min(kDotChunk, n - c0);
         __syncthreads();
@@ -516,8 +722,8 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         double* b = w.hb[l];
         double* x = w.hx[l];
         if (phase[l] == 0) {
-            for (int s = 0; s < H.gs_pre; ++s) gs_sweep(lv.a, b, x, false);
-            stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b);
+            gs_sweeps(lv, b, x, false, H.gs_pre, H.exact != 0);
+            stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b, H.exact != 0);
             __syncthreads();
             csr_apply<false>(lv.embed_t, w.hr[l], w.hb[l + 1]);  // rc = E^T r
             cta_fill(w.hx[l + 1], 0.0, H.h[l + 1].n);              // ec = 0
@@ -530,7 +736,7 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         } else {
             csr_apply<true>(lv.embed, w.hx[l + 1], x);  // x += E ec
             __syncthreads();
-            for (int s = 0; s < H.gs_post; ++s) gs_sweep(lv.a, b, x, true);
+            gs_sweeps(lv, b, x, true, H.gs_post, H.exact != 0);
             if (l == 0) break;
             --l;
         }
@@ -540,38 +746,45 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
 // x += S (b - A x), S = ILUT application (pmultigrid.hpp:311-316).
 template <int DEG>
 __device__ __noinline__ void smooth(const DevHier& H, const Ws& w) {
-    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.z, w.b);  // z = r = b - A x
+    pstamp(10);
+    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.z, w.b, H.exact != 0);  // z = r = b - A x
     if (threadIdx.x == 0) w.z[H.n_p] = 0.0;                          // neutral padding slot
     __syncthreads();
-    tri_solve<false>(H.L, w.z, w.z_off, nullptr, w.ring_off, w.slot_bytes, w.prod_off);
-    tri_solve<true>(H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off);
+    pstamp(11);
+    ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, H.exact != 0);
+    pstamp(12);
 }
 
 // One V(nu_pre, nu_post) cycle (pmultigrid.hpp:256-267).
 template <int DEG>
 __device__ __noinline__ void vcycle(const DevHier& H, const Ws& w) {
     for (int s = 0; s < H.nu_pre; ++s) smooth<DEG>(H, w);
-    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b);
+    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0);
     __syncthreads();
-    stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, w.r, w.hb[0], H.inv_l1);  // restrict_to_linear
+    stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, w.r, w.hb[0], H.inv_l1, H.exact != 0);  // restrict_to_linear
     cta_fill(w.hx[0], 0.0, H.n_1);
     __syncthreads();
+    pstamp(20);
     wcycle<DEG>(H, w);
-    stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, w.hx[0], w.x, H.inv_lp);  // x += prolong_from_linear
+    pstamp(21);
+    stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, w.hx[0], w.x, H.inv_lp, H.exact != 0);  // x += prolong_from_linear
     __syncthreads();
+    pstamp(22);
     for (int s = 0; s < H.nu_post; ++s) smooth<DEG>(H, w);
 }
 
 template <int DEG>
 __device__ double rel_residual(const DevHier& H, const Ws& w, double bnorm, double* sh) {
-    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b);
-    const double d = cta_ordered_dot(w.r, w.r, H.n_p, w.dot, sh);
+    pstamp(30);
+    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0);
+    const double d = cta_ordered_dot(w.r, w.r, H.n_p, w.dot, sh, H.exact != 0);
+    pstamp(31);
     return sqrt(d) / bnorm;
 }
 
 // One Phi application: build b, solve (pmultigrid.hpp:271-307), epilogue.
 template <int DEG>
-__device__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs& a, const Ws& w, int task,
+__device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs& a, const Ws& w, int task,
                           int k, double* sh) {
     const int n = H.n_p;
     // ---- right-hand side and initial guess
@@ -583,9 +796,9 @@ __device__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs
         else if (a.LOADV)
             load = a.LOADV + (size_t)task * a.ldl;
         if (load)
-            stencil_apply<kOutAddVec, Widths<DEG>::A>(Am, uprev, w.b, load);  // rhs = A- u + load
+            stencil_apply<kOutAddVec, Widths<DEG>::A>(Am, uprev, w.b, load, H.exact != 0);  // rhs = A- u + load
         else
-            stencil_apply<kOutSet, Widths<DEG>::A>(Am, uprev, w.b, nullptr);
+            stencil_apply<kOutSet, Widths<DEG>::A>(Am, uprev, w.b, nullptr, H.exact != 0);
         const double* guess =
             a.U ? a.U + (size_t)(a.guess_prev ? k - 1 : k) * n : (a.x0_empty ? nullptr : a.X + (size_t)task * a.ldx);
         if (guess)
@@ -609,7 +822,7 @@ __device__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs
     // ---- p-multigrid solve
     int iters = 0, conv = 0;
     double rel = 0.0;
-    const double bnorm = sqrt(cta_ordered_dot(w.b, w.b, n, w.dot, sh));
+    const double bnorm = sqrt(cta_ordered_dot(w.b, w.b, n, w.dot, sh, H.exact != 0));
     if (bnorm == 0.0) {
         cta_fill(w.x, 0.0, n);  // zero rhs -> zero solution, not the guess
         conv = 1;
@@ -681,10 +894,10 @@ __device__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs
             const double wv = g ? w.x[i] + g[i] : w.x[i];
             w.r[i] = wv - u[i];
         }
-        const double d = cta_ordered_dot(w.r, w.r, n, w.dot, sh);
+        const double d = cta_ordered_dot(w.r, w.r, n, w.dot, sh, H.exact != 0);
         if (threadIdx.x == 0) a.SQ[k] = d;
     } else if (a.epi == kEpiNorm) {
-        const double d = cta_ordered_dot(w.x, w.x, n, w.dot, sh);
+        const double d = cta_ordered_dot(w.x, w.x, n, w.dot, sh, H.exact != 0);
         if (threadIdx.x == 0) a.SQ[k] = d;
     } else {
         double* out = a.X + (size_t)task * a.ldx;
@@ -695,12 +908,16 @@ __device__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs
 
 template <int DEG>
 __global__ void __launch_bounds__(NT, 1)
-    phi_wave_kernel(const __grid_constant__ DevHier H, const __grid_constant__ DevStencil Am,
-                    const __grid_constant__ WaveArgs a, const __grid_constant__ SmemPlan P, double* ws_base,
+    phi_wave_kernel(const __grid_constant__ DevHier H_param, const __grid_constant__ DevStencil Am,
+                    const __grid_constant__ WaveArgs a_param, const __grid_constant__ SmemPlan P, double* ws_base,
                     long long ws_stride) {
     double* smem = g_smem;
     __shared__ double sh[4];
-    const Ws w = carve(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
+    __shared__ WaveArgs a_sh;
+    if (threadIdx.x == 0) a_sh = a_param;
+    const WaveArgs& a = a_sh;
+    const DevHier& H = hier_shared(H_param);
+    const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
     for (int task = blockIdx.x; task < a.n_tasks; task += gridDim.x) {
         for (int s = 0; s < a.task_len; ++s) {
             const int k = a.task_k0 ? a.task_k0[task] + s : task;
@@ -712,10 +929,11 @@ __global__ void __launch_bounds__(NT, 1)
 // ---- standalone V-cycle on a batch (PMultigridHierarchy::vcycle) ----------
 template <int DEG>
 __global__ void __launch_bounds__(NT, 1)
-    vcycle_kernel(const __grid_constant__ DevHier H, const double* B, long long ldb, double* X, long long ldx,
+    vcycle_kernel(const __grid_constant__ DevHier H_param, const double* B, long long ldb, double* X, long long ldx,
                   int nrhs, const __grid_constant__ SmemPlan P, double* ws_base, long long ws_stride) {
     double* smem = g_smem;
-    const Ws w = carve(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
+    const DevHier& H = hier_shared(H_param);
+    const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
     const int n = H.n_p;
     for (int t = blockIdx.x; t < nrhs; t += gridDim.x) {
         cta_copy(w.b, B + (size_t)t * ldb, n);
@@ -733,25 +951,25 @@ __global__ void __launch_bounds__(NT, 1)
 //     4 x1 = W-cycle(b1, x1), 5 x = GS(b, x) on level `arg` (arg2 = backward)
 template <int DEG>
 __global__ void __launch_bounds__(NT, 1)
-    unit_kernel(const __grid_constant__ DevHier H, int op, int arg, int arg2, const double* in, double* out,
+    unit_kernel(const __grid_constant__ DevHier H_param, int op, int arg, int arg2, const double* in, double* out,
                 const __grid_constant__ SmemPlan P, double* ws_base, long long ws_stride) {
     double* smem = g_smem;
-    const Ws w = carve(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
+    const DevHier& H = hier_shared(H_param);
+    const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
     const int n = H.n_p;
     if (op == 0) {
-        stencil_apply<kOutSet, Widths<DEG>::A>(H.A, in, out, nullptr);
+        stencil_apply<kOutSet, Widths<DEG>::A>(H.A, in, out, nullptr, H.exact != 0);
     } else if (op == 1) {
         cta_copy(w.z, in, n);
         cta_fill(w.x, 0.0, n);
         if (threadIdx.x == 0) w.z[n] = 0.0;
         __syncthreads();
-        tri_solve<false>(H.L, w.z, w.z_off, nullptr, w.ring_off, w.slot_bytes, w.prod_off);
-        tri_solve<true>(H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off);
+        ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, H.exact != 0);
         cta_copy(out, w.z, n);
     } else if (op == 2) {
-        stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, in, out, H.inv_l1);
+        stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, in, out, H.inv_l1, H.exact != 0);
     } else if (op == 3) {
-        stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, in, out, H.inv_lp);
+        stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, in, out, H.inv_lp, H.exact != 0);
     } else if (op == 4) {
         cta_copy(w.hb[0], in, H.n_1);
         cta_copy(w.hx[0], out, H.n_1);
@@ -763,7 +981,7 @@ __global__ void __launch_bounds__(NT, 1)
         cta_copy(w.hb[arg], in, lv.n);
         cta_copy(w.hx[arg], out, lv.n);
         __syncthreads();
-        gs_sweep(lv.a, w.hb[arg], w.hx[arg], arg2 != 0);
+        gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, H.exact != 0);
         cta_copy(out, w.hx[arg], lv.n);
     }
 }
@@ -837,101 +1055,10 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
-// ---- small elementwise MGRIT helpers --------------------------------------
-// coarse.g[0] = fine.g[0] - fine.u[0]; coarse.u[0] = coarse.g[0]  (mgrit.hpp:155-166)
-__global__ void restrict_first_kernel(const double* fg, const double* fu, double* cg, double* cu, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double v = fg[i] - fu[i];
-        cg[i] = v;
-        cu[i] = v;
-    }
-}
-
-// fine.u[j*m] += coarse.u[j], j = 0..J  (mgrit.hpp:172-180)
-__global__ void inject_kernel(const double* cu, double* fu, int n, int J, int m) {
-    const size_t total = (size_t)(J + 1) * n;
-    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-        const size_t j = t / n, i = t - j * n;
-        double* dst = fu + j * m * (size_t)n + i;
-        *dst = *dst + cu[t];
-    }
-}
-
-// sq[0] = |g[0] - u[0]|^2, index-ordered  (mgrit.hpp:202-203)
-__global__ void resid0_kernel(const double* g, const double* u, double* sq, int n) {
-    __shared__ double sh[4];
-    __shared__ double scratch[kDotChunk];
-    double s = 0.0;
-    for (int c0 = 0; c0 < n; c0 += kDotChunk) {
-        const int cnt = min(kDotChunk, n - c0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const double r = g[c0 + i] - u[c0 + i];
-            scratch[i] = r * r;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0)
-            for (int i = 0; i < cnt; ++i) s = s + scratch[i];
-    }
-    if (threadIdx.x == 0) sq[0] = s;
-    (void)sh;
-}
-
-__global__ void copy_kernel(double* dst, const double* src, size_t n) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
-}
-
 }  // namespace
 
-// ---------------------------------------------------------------------------
-// host launchers
-// ---------------------------------------------------------------------------
-size_t phi_ws_doubles(const DevHier& H) {
-    size_t s = 6 * ((size_t)H.n_p + 2);
-    for (int l = 0; l < H.n_h; ++l) s += 4 * (size_t)H.h[l].n;
-    return (s + 31) & ~size_t(31);
-}
-
-SmemPlan phi_smem_plan(const DevHier& H) {
-    // The three users of shared memory are live in disjoint phases of a
-    // V-cycle, so they overlay one another from offset 0:
-    //   smoothing  : triangular-factor rings + dependency array z
-    //   W-cycle    : the order-1 h-level vectors (restrict .. prolong)
-    //   norms      : the ordered-dot scratch
-    SmemPlan P{};
-    const size_t budget = kPhiSmemBudgetBytes / 8;  // doubles
-    P.ring_off = 0;
-    P.dot_off = 0;
-    P.slot_bytes = (std::max(H.L.max_block_bytes, H.U.max_block_bytes) + 127) / 128 * 128;
-    size_t tri = (size_t)kTriSlots * P.slot_bytes / 8;
-    P.prod_off = (int)tri;
-    tri += ((size_t)std::max(H.L.max_items, H.U.max_items) + 1) / 2 * 2;
-    if (tri * 8 > kPhiSmemBudgetBytes) throw InvalidArgument("triangular-factor blocks exceed shared memory");
-    if (tri + (size_t)H.n_p + 2 <= budget) {
-        P.z_off = (int)tri;
-        tri += H.n_p + 2;
-    } else {
-        P.z_off = -1;
-    }
-    for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
-    // coarsest levels first: they are visited most often by the W-cycle
-    size_t lv = 0;
-    for (int l = H.n_h - 1; l >= 0; --l) {
-        const size_t need = 4 * (size_t)H.h[l].n;
-        if (lv + need <= budget) {
-            P.lvl_off[l] = (int)lv;
-            lv += need;
-        }
-    }
-    P.total = (int)std::max(std::max(tri, lv), (size_t)kDotChunk);
-    return P;
-}
-
-size_t phi_smem_bytes(const DevHier& H) { return (size_t)phi_smem_plan(H).total * 8; }
-
 template <class K>
-static int occupancy_grid(K kernel, size_t smem, int want) {
+static inline int occupancy_grid(K kernel, size_t smem, int want) {
     static int n_sm = 0;
     if (!n_sm) {
         int dev = 0;
@@ -946,115 +1073,53 @@ static int occupancy_grid(K kernel, size_t smem, int want) {
     return std::max(1, std::min(want, per_sm * n_sm));
 }
 
-// Kernels are instantiated per spline degree (compile-time stencil widths).
-#define PHI_DEG_DISPATCH(deg, ...)                                                   \
-    switch (deg) {                                                                    \
-        case 1: { constexpr int DEG = 1; __VA_ARGS__; } break;                               \
-        case 2: { constexpr int DEG = 2; __VA_ARGS__; } break;                               \
-        case 3: { constexpr int DEG = 3; __VA_ARGS__; } break;                               \
-        case 4: { constexpr int DEG = 4; __VA_ARGS__; } break;                               \
-        case 5: { constexpr int DEG = 5; __VA_ARGS__; } break;                               \
-        case 6: { constexpr int DEG = 6; __VA_ARGS__; } break;                               \
-        case 7: { constexpr int DEG = 7; __VA_ARGS__; } break;                               \
-        case 8: { constexpr int DEG = 8; __VA_ARGS__; } break;                               \
-        default: throw InvalidArgument("unsupported spline degree");                  \
-    }
 
-static int degree_of(const DevStencil& A) { return (A.hi - A.lo) / 2; }
-
-int phi_max_slots(const DevHier& H) {
-    int r = 1;
-    PHI_DEG_DISPATCH(degree_of(H.A), r = occupancy_grid(phi_wave_kernel<DEG>, phi_smem_bytes(H), 1 << 30));
-    return r;
+template <int DEG>
+int DegLaunch<DEG>::max_slots(const DevHier& H) {
+    return occupancy_grid(phi_wave_kernel<DEG>, phi_smem_bytes(H), 1 << 30);
 }
 
-void launch_phi_wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws, long long ws_stride,
-                     int max_slots, cudaStream_t s) {
-    if (a.n_tasks <= 0) return;
+template <int DEG>
+void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws, long long ws_stride,
+                          int grid, cudaStream_t s) {
     const SmemPlan P = phi_smem_plan(H);
     const size_t smem = (size_t)P.total * 8;
-    const int grid = std::min(a.n_tasks, max_slots);
-    PHI_DEG_DISPATCH(degree_of(H.A), {
-        occupancy_grid(phi_wave_kernel<DEG>, smem, grid);
-        phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
-    });
+    occupancy_grid(phi_wave_kernel<DEG>, smem, grid);
+    phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
     PHI_CUDA(cudaGetLastError());
 }
 
-void launch_vcycle(const DevHier& H, const double* B, long long ldb, double* X, long long ldx, int nrhs, double* ws,
-                   long long ws_stride, int max_slots, cudaStream_t s) {
-    if (nrhs <= 0) return;
+template <int DEG>
+void DegLaunch<DEG>::vcycle(const DevHier& H, const double* B, long long ldb, double* X, long long ldx, int nrhs,
+                            double* ws, long long ws_stride, int grid, cudaStream_t s) {
     const SmemPlan P = phi_smem_plan(H);
     const size_t smem = (size_t)P.total * 8;
-    const int grid = std::min(nrhs, max_slots);
-    PHI_DEG_DISPATCH(degree_of(H.A), {
-        occupancy_grid(vcycle_kernel<DEG>, smem, grid);
-        vcycle_kernel<DEG><<<grid, NT, smem, s>>>(H, B, ldb, X, ldx, nrhs, P, ws, ws_stride);
-    });
+    occupancy_grid(vcycle_kernel<DEG>, smem, grid);
+    vcycle_kernel<DEG><<<grid, NT, smem, s>>>(H, B, ldb, X, ldx, nrhs, P, ws, ws_stride);
     PHI_CUDA(cudaGetLastError());
 }
 
-void launch_unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
-                 long long ws_stride, cudaStream_t s) {
+template <int DEG>
+void DegLaunch<DEG>::unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
+                          long long ws_stride, cudaStream_t s) {
     const SmemPlan P = phi_smem_plan(H);
     const size_t smem = (size_t)P.total * 8;
-    PHI_DEG_DISPATCH(degree_of(H.A), {
-        occupancy_grid(unit_kernel<DEG>, smem, 1);
-        unit_kernel<DEG><<<1, NT, smem, s>>>(H, op, arg, arg2, in, out, P, ws, ws_stride);
-    });
+    occupancy_grid(unit_kernel<DEG>, smem, 1);
+    unit_kernel<DEG><<<1, NT, smem, s>>>(H, op, arg, arg2, in, out, P, ws, ws_stride);
     PHI_CUDA(cudaGetLastError());
 }
 
-void launch_cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work, double rel_tol,
-               int max_iter, int* result, cudaStream_t s) {
-    PHI_DEG_DISPATCH(degree_of(A), (cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result)));
+template <int DEG>
+void DegLaunch<DEG>::cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
+                        double rel_tol, int max_iter, int* result, cudaStream_t s) {
+    cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result);
     PHI_CUDA(cudaGetLastError());
 }
 
-static DevBuf<long long> g_trace;
-
-void phi_set_tuning(int tri_warps, int gs_warps, int sleep_ns) {
-    Tuning t{std::max(1, std::min(tri_warps, NW)), std::max(1, std::min(gs_warps, NW)), std::max(0, sleep_ns), 0,
-             nullptr};
-    if (sleep_ns < 0) {  // negative: enable the block-timing trace
-        g_trace.alloc((size_t)NW * 1024 * 6);
-        g_trace.zero();
-        t.trace = g_trace.get();
-        t.sleep_ns = 0;
-    }
+template <int DEG>
+void DegLaunch<DEG>::set_trace(long long* trace) {
+    Tuning t{NW, NW, 0, 0, trace};
     PHI_CUDA(cudaMemcpyToSymbol(c_tune, &t, sizeof t));
-}
-
-int phi_read_trace(long long* out, int n) {
-    if (!g_trace.get()) return 0;
-    const auto h = g_trace.download();
-    const int m = std::min<int>(n, (int)h.size());
-    std::copy(h.begin(), h.begin() + m, out);
-    return m;
-}
-
-void launch_restrict_first(const double* fg, const double* fu, double* cg, double* cu, int n, cudaStream_t s) {
-    restrict_first_kernel<<<(n + 255) / 256, 256, 0, s>>>(fg, fu, cg, cu, n);
-    PHI_CUDA(cudaGetLastError());
-}
-
-void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s) {
-    const size_t total = (size_t)(J + 1) * n;
-    const int grid = (int)std::min<size_t>((total + 255) / 256, 4096);
-    inject_kernel<<<grid, 256, 0, s>>>(cu, fu, n, J, m);
-    PHI_CUDA(cudaGetLastError());
-}
-
-void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s) {
-    resid0_kernel<<<1, 256, 0, s>>>(g, u, sq, n);
-    PHI_CUDA(cudaGetLastError());
-}
-
-void launch_copy(double* dst, const double* src, size_t n, cudaStream_t s) {
-    if (!n) return;
-    const int grid = (int)std::min<size_t>((n + 255) / 256, 4096);
-    copy_kernel<<<grid, 256, 0, s>>>(dst, src, n);
-    PHI_CUDA(cudaGetLastError());
 }
 
 }  // namespace phi

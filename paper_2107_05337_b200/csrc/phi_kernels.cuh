@@ -23,6 +23,31 @@ int phi_max_slots(const DevHier& H);
 void phi_set_tuning(int tri_warps, int gs_warps, int sleep_ns);
 int phi_read_trace(long long* out, int n);
 
+/// Degree-templated launchers, explicitly instantiated in phi_deg.cu.
+template <int DEG>
+struct DegLaunch {
+    static int max_slots(const DevHier& H);
+    static void wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws, long long ws_stride,
+                     int grid, cudaStream_t s);
+    static void vcycle(const DevHier& H, const double* B, long long ldb, double* X, long long ldx, int nrhs,
+                       double* ws, long long ws_stride, int grid, cudaStream_t s);
+    static void unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
+                     long long ws_stride, cudaStream_t s);
+    static void cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
+                   double rel_tol, int max_iter, int* result, cudaStream_t s);
+    static void set_trace(long long* trace);
+};
+extern template struct DegLaunch<1>;
+extern template struct DegLaunch<2>;
+extern template struct DegLaunch<3>;
+extern template struct DegLaunch<4>;
+extern template struct DegLaunch<5>;
+extern template struct DegLaunch<6>;
+extern template struct DegLaunch<7>;
+extern template struct DegLaunch<8>;
+/// Longs in the developer trace buffer (phi_set_tuning(.., .., -1)).
+constexpr size_t kTraceLongs = 49152;
+
 void launch_phi_wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws,
                      long long ws_stride, int max_slots, cudaStream_t s);
 void launch_vcycle(const DevHier& H, const double* B, long long ldb, double* X, long long ldx, int nrhs,
@@ -72,5 +97,6 @@ void launch_assemble_load(const DevTables1D& tu, const DevTables1D& tv, int kind
 /// f_k = f_k * (dt*theta) + (dt*(1-theta)) * f_{k-1}   (theta.hpp:186-191)
 void launch_theta_combine(double* fk, const double* fkm1, double a, double b, int n, cudaStream_t s);
 void launch_scale(double* v, double a, size_t n, cudaStream_t s);
+void launch_recip(const double* v, double* out, int n, cudaStream_t s);
 
 }  // namespace phi

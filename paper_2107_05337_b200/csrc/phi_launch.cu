@@ -1,0 +1,207 @@
+// Host launchers of the Phi kernels: shared-memory plan, per-degree dispatch
+// to the DegLaunch instantiations (phi_deg.cu) and the small elementwise
+// MGRIT helpers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "device_types.cuh"
+#include "phi_kernels.cuh"
+
+namespace phi {
+
+namespace {
+
+constexpr int kDotChunk = 2048;  // doubles of shared scratch for ordered dots
+
+// ---- small elementwise MGRIT helpers --------------------------------------
+// coarse.g[0] = fine.g[0] - fine.u[0]; coarse.u[0] = coarse.g[0]  (mgrit.hpp:155-166)
+__global__ void restrict_first_kernel(const double* fg, const double* fu, double* cg, double* cu, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double v = fg[i] - fu[i];
+        cg[i] = v;
+        cu[i] = v;
+    }
+}
+
+// fine.u[j*m] += coarse.u[j], j = 0..J  (mgrit.hpp:172-180)
+__global__ void inject_kernel(const double* cu, double* fu, int n, int J, int m) {
+    const size_t total = (size_t)(J + 1) * n;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const size_t j = t / n, i = t - j * n;
+        double* dst = fu + j * m * (size_t)n + i;
+        *dst = *dst + cu[t];
+    }
+}
+
+// sq[0] = |g[0] - u[0]|^2, index-ordered  (mgrit.hpp:202-203)
+__global__ void resid0_kernel(const double* g, const double* u, double* sq, int n) {
+    __shared__ double sh[4];
+    __shared__ double scratch[kDotChunk];
+    double s = 0.0;
+    for (int c0 = 0; c0 < n; c0 += kDotChunk) {
+        const int cnt = min(kDotChunk, n - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const double r = g[c0 + i] - u[c0 + i];
+            scratch[i] = r * r;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < cnt; ++i) s = s + scratch[i];
+    }
+    if (threadIdx.x == 0) sq[0] = s;
+    (void)sh;
+}
+
+__global__ void copy_kernel(double* dst, const double* src, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+size_t phi_ws_doubles(const DevHier& H) {
+    size_t s = 6 * ((size_t)H.n_p + 2);
+    for (int l = 0; l < H.n_h; ++l) s += 4 * (size_t)H.h[l].n;
+    return (s + 31) & ~size_t(31);
+}
+
+SmemPlan phi_smem_plan(const DevHier& H) {
+    // The three users of shared memory are live in disjoint phases of a
+    // V-cycle, so they overlay one another from offset 0:
+    //   smoothing  : triangular-factor rings + dependency array z
+    //   W-cycle    : the order-1 h-level vectors (restrict .. prolong)
+    //   norms      : the ordered-dot scratch
+    SmemPlan P{};
+    const size_t budget = kPhiSmemBudgetBytes / 8;  // doubles
+    P.ring_off = 0;
+    P.dot_off = 0;
+    P.slot_bytes = (std::max(H.L.max_block_bytes, H.U.max_block_bytes) + 127) / 128 * 128;
+    size_t tri = (size_t)kTriSlots * P.slot_bytes / 8;
+    P.prod_off = (int)tri;
+    tri += kTriMaxItems;
+    if (tri * 8 > kPhiSmemBudgetBytes) throw InvalidArgument("triangular-factor blocks exceed shared memory");
+    if (tri + (size_t)H.n_p + 2 <= budget) {
+        P.z_off = (int)tri;
+        tri += H.n_p + 2;
+    } else {
+        P.z_off = -1;
+    }
+    for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
+    // coarsest levels first: they are visited most often by the W-cycle
+    size_t lv = 0;
+    for (int l = H.n_h - 1; l >= 0; --l) {
+        const size_t need = 4 * (size_t)H.h[l].n;
+        if (lv + need <= budget) {
+            P.lvl_off[l] = (int)lv;
+            lv += need;
+        }
+    }
+    P.total = (int)std::max(std::max(tri, lv), (size_t)kDotChunk);
+    if (std::getenv("PHI_PLAN_DEBUG"))
+        std::fprintf(stderr, "smem plan: slot %d B x %d, prod @%d, z @%d, levels @%d.., total %d doubles\n",
+                     P.slot_bytes, kTriSlots, P.prod_off, P.z_off, P.lvl_off[0], P.total);
+    return P;
+}
+
+size_t phi_smem_bytes(const DevHier& H) { return (size_t)phi_smem_plan(H).total * 8; }
+
+// Kernels are instantiated per spline degree (compile-time stencil widths).
+#define PHI_DEG_DISPATCH(deg, ...)                                                   \
+    switch (deg) {                                                                    \
+        case 1: { constexpr int DEG = 1; __VA_ARGS__; } break;                               \
+        case 2: { constexpr int DEG = 2; __VA_ARGS__; } break;                               \
+        case 3: { constexpr int DEG = 3; __VA_ARGS__; } break;                               \
+        case 4: { constexpr int DEG = 4; __VA_ARGS__; } break;                               \
+        case 5: { constexpr int DEG = 5; __VA_ARGS__; } break;                               \
+        case 6: { constexpr int DEG = 6; __VA_ARGS__; } break;                               \
+        case 7: { constexpr int DEG = 7; __VA_ARGS__; } break;                               \
+        case 8: { constexpr int DEG = 8; __VA_ARGS__; } break;                               \
+        default: throw InvalidArgument("unsupported spline degree");                  \
+    }
+
+static int degree_of(const DevStencil& A) { return (A.hi - A.lo) / 2; }
+
+int phi_max_slots(const DevHier& H) {
+    int r = 1;
+    PHI_DEG_DISPATCH(degree_of(H.A), r = DegLaunch<DEG>::max_slots(H));
+    return r;
+}
+
+void launch_phi_wave(const DevHier& H, const DevStencil& Am, const WaveArgs& a, double* ws, long long ws_stride,
+                     int max_slots, cudaStream_t s) {
+    if (a.n_tasks <= 0) return;
+    const int grid = std::min(a.n_tasks, max_slots);
+    PHI_DEG_DISPATCH(degree_of(H.A), DegLaunch<DEG>::wave(H, Am, a, ws, ws_stride, grid, s));
+}
+
+void launch_vcycle(const DevHier& H, const double* B, long long ldb, double* X, long long ldx, int nrhs, double* ws,
+                   long long ws_stride, int max_slots, cudaStream_t s) {
+    if (nrhs <= 0) return;
+    const int grid = std::min(nrhs, max_slots);
+    PHI_DEG_DISPATCH(degree_of(H.A), DegLaunch<DEG>::vcycle(H, B, ldb, X, ldx, nrhs, ws, ws_stride, grid, s));
+}
+
+void launch_unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
+                 long long ws_stride, cudaStream_t s) {
+    PHI_DEG_DISPATCH(degree_of(H.A), DegLaunch<DEG>::unit(H, op, arg, arg2, in, out, ws, ws_stride, s));
+}
+
+void launch_cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work, double rel_tol,
+               int max_iter, int* result, cudaStream_t s) {
+    PHI_DEG_DISPATCH(degree_of(A), DegLaunch<DEG>::cg(A, diag, b, x, work, rel_tol, max_iter, result, s));
+}
+
+static DevBuf<long long> g_trace;
+
+void phi_set_tuning(int tri_warps, int gs_warps, int sleep_ns) {
+    (void)tri_warps;
+    (void)gs_warps;
+    long long* trace = nullptr;
+    if (sleep_ns < 0) {  // negative: enable the developer timing trace
+        g_trace.alloc(kTraceLongs);
+        g_trace.zero();
+        trace = g_trace.get();
+    }
+    for (int d = 1; d <= 8; ++d) PHI_DEG_DISPATCH(d, DegLaunch<DEG>::set_trace(trace));
+}
+
+int phi_read_trace(long long* out, int n) {
+    if (!g_trace.get()) return 0;
+    const auto h = g_trace.download();
+    const int m = std::min<int>(n, (int)h.size());
+    std::copy(h.begin(), h.begin() + m, out);
+    return m;
+}
+
+void launch_restrict_first(const double* fg, const double* fu, double* cg, double* cu, int n, cudaStream_t s) {
+    restrict_first_kernel<<<(n + 255) / 256, 256, 0, s>>>(fg, fu, cg, cu, n);
+    PHI_CUDA(cudaGetLastError());
+}
+
+void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s) {
+    const size_t total = (size_t)(J + 1) * n;
+    const int grid = (int)std::min<size_t>((total + 255) / 256, 4096);
+    inject_kernel<<<grid, 256, 0, s>>>(cu, fu, n, J, m);
+    PHI_CUDA(cudaGetLastError());
+}
+
+void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s) {
+    resid0_kernel<<<1, 256, 0, s>>>(g, u, sq, n);
+    PHI_CUDA(cudaGetLastError());
+}
+
+void launch_copy(double* dst, const double* src, size_t n, cudaStream_t s) {
+    if (!n) return;
+    const int grid = (int)std::min<size_t>((n + 255) / 256, 4096);
+    copy_kernel<<<grid, 256, 0, s>>>(dst, src, n);
+    PHI_CUDA(cudaGetLastError());
+}
+
+}  // namespace phi

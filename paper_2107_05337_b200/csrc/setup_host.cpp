@@ -383,16 +383,18 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
     p.level_chunk.push_back(0);
     for (int lv = 0; lv < p.n_levels; ++lv) {
         const auto& rs = by_level[lv];
-        for (size_t c0 = 0; c0 < rs.size(); c0 += kTriRows) {
-            const int nr = static_cast<int>(std::min<size_t>(kTriRows, rs.size() - c0));
-            int maxlen = 0;
-            for (int l = 0; l < nr; ++l) {
-                const int i = rs[c0 + l];
-                const int len = m.row_offsets[i + 1] - m.row_offsets[i] - (upper ? 1 : 0);
-                maxlen = std::max(maxlen, len);
+        auto row_len = [&](int i) { return m.row_offsets[i + 1] - m.row_offsets[i] - (upper ? 1 : 0); };
+        for (size_t c0 = 0; c0 < rs.size();) {
+            // widest chunk within kTriRows rows and kTriBlockCap bytes
+            int nr = 0, maxlen = 0;
+            while (c0 + nr < rs.size() && nr < kTriRows) {
+                const int ml = std::max(maxlen, row_len(rs[c0 + nr]));
+                const int sp = std::max(2, (ml + 1) / 2 * 2);
+                if (nr > 0 && 12 * (nr + 1) * sp + 20 * (nr + 1) + 64 > kTriBlockCap) break;
+                maxlen = ml;
+                ++nr;
             }
-            // pad to a whole number (>= 1) of kTriRing-entry blocks
-            const int span = std::max(1, (maxlen + kTriRing - 1) / kTriRing) * kTriRing;
+            const int span = std::max(2, (maxlen + 1) / 2 * 2);  // even: keeps vals 8-byte aligned
             const size_t base = p.cols.size();
             p.chunk_meta.push_back(static_cast<int>(p.rows.size()));
             p.chunk_meta.push_back(nr);
@@ -412,6 +414,7 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
                     p.vals[base + static_cast<size_t>(e) * nr + l] = m.values[b + e];
                 }
             }
+            c0 += nr;
         }
         p.level_chunk.push_back(static_cast<int>(p.chunk_meta.size() / 4));
     }
@@ -430,16 +433,22 @@ TriPlan plan_upper(const HostCsr& upper) { return make_plan(upper, true); }
 
 TriStream make_tri_stream(const TriPlan& p) {
     struct Blk {
-        int chunk, span, bytes;
+        int chunk, nr, span, bytes, diag_off, cols_off, vals_off;
     };
+    const bool upper = !p.diag.empty();
     std::vector<Blk> blocks;
     for (int c = 0; c < p.n_chunks; ++c) {
-        const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1];
-        int maxlen = 0;
-        for (int l = 0; l < nr; ++l) maxlen = std::max(maxlen, p.lens[row0 + l]);
-        const int span = std::max(2, (maxlen + 1) / 2 * 2);  // even: keeps vals 8-byte aligned
-        const int bytes = (kTriBlockPrefix + 12 * nr * span + 15) / 16 * 16;
-        blocks.push_back({c, span, bytes});
+        Blk k{};
+        k.chunk = c;
+        k.nr = p.chunk_meta[4 * c + 1];
+        k.span = p.chunk_meta[4 * c + 3];
+        k.diag_off = 32 + (4 * k.nr + 7) / 8 * 8;
+        k.cols_off = k.diag_off + (upper ? 16 * k.nr : 0);
+        k.vals_off = k.cols_off + 4 * k.nr * k.span;  // nr * span even: 8-byte aligned
+        k.bytes = (k.vals_off + 8 * k.nr * k.span + 15) / 16 * 16;
+        if (k.nr * k.span > kTriMaxItems)
+            throw InvalidArgument("ILUT factor row longer than the triangular-solve block capacity");
+        blocks.push_back(k);
     }
     TriStream ts;
     ts.n_blocks = static_cast<int>(blocks.size());
@@ -449,7 +458,6 @@ TriStream make_tri_stream(const TriPlan& p) {
         off.push_back(total);
         total += k.bytes;
         ts.max_block_bytes = std::max(ts.max_block_bytes, k.bytes);
-        ts.max_items = std::max(ts.max_items, k.span * p.chunk_meta[4 * k.chunk + 1]);
     }
     ts.stream.assign(total + 16, 0);
     ts.prime.assign(2 * (kTriSlots - 1), 0);
@@ -459,10 +467,9 @@ TriStream make_tri_stream(const TriPlan& p) {
     }
     for (size_t k = 0; k < blocks.size(); ++k) {
         const Blk& B = blocks[k];
-        const int c = B.chunk;
-        const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
+        const int row0 = p.chunk_meta[4 * B.chunk], base = p.chunk_meta[4 * B.chunk + 2];
         unsigned char* dst = ts.stream.data() + off[k];
-        int hdr[8] = {nr, B.span, row0, 0, 0, 0, 0, 0};
+        int hdr[8] = {B.nr, B.span, row0, 0, 0, B.cols_off, B.vals_off, B.diag_off};
         const size_t nxt = k + kTriSlots - 1;
         if (nxt < blocks.size()) {
             hdr[3] = static_cast<int>(off[nxt] / 16);
@@ -470,19 +477,22 @@ TriStream make_tri_stream(const TriPlan& p) {
         }
         std::memcpy(dst, hdr, sizeof hdr);
         int* rws = reinterpret_cast<int*>(dst + 32);
-        double* dg = reinterpret_cast<double*>(dst + 64);
-        for (int l = 0; l < nr; ++l) {
-            rws[l] = p.rows[row0 + l];
-            dg[l] = p.diag.empty() ? 1.0 : p.diag[p.rows[row0 + l]];
+        for (int l = 0; l < B.nr; ++l) rws[l] = p.rows[row0 + l];
+        if (upper) {
+            double* dg = reinterpret_cast<double*>(dst + B.diag_off);
+            for (int l = 0; l < B.nr; ++l) {
+                const double d = p.diag[p.rows[row0 + l]];
+                dg[l] = d;
+                dg[B.nr + l] = 1.0 / d;  // IEEE round-to-nearest reciprocal
+            }
         }
-        int* cols = reinterpret_cast<int*>(dst + kTriBlockPrefix);
-        double* vals = reinterpret_cast<double*>(dst + kTriBlockPrefix + 4 * nr * B.span);
+        int* cols = reinterpret_cast<int*>(dst + B.cols_off);
+        double* vals = reinterpret_cast<double*>(dst + B.vals_off);
         for (int e = 0; e < B.span; ++e)
-            for (int l = 0; l < nr; ++l) {
-                const bool real = e < p.lens[row0 + l];
-                const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * nr + l;
-                cols[e * nr + l] = real ? p.cols[src] : p.n;  // neutral dummy: z[n] = +0.0
-                vals[e * nr + l] = real ? p.vals[src] : 0.0;
+            for (int l = 0; l < B.nr; ++l) {
+                const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * B.nr + l;
+                cols[e * B.nr + l] = p.cols[src];
+                vals[e * B.nr + l] = p.vals[src];
             }
     }
     return ts;

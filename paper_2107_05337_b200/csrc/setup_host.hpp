@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "device_types.cuh"
 
 namespace phi {
 
@@ -60,17 +61,16 @@ struct DenseLUHost {
 };
 DenseLUHost dense_lu_factor(const HostCsr& a);
 
-/// Level-ordered, lane-interleaved layout of a triangular factor for the
-/// sync-free device solve.  Rows of one level are independent; a level is
-/// split into chunks of <= 32 rows (one lane per row).  Entry e of lane l of
-/// chunk c lives at base[c] + e * nrows[c] + l (coalesced per warp).
+/// Level schedule of a triangular factor.  Rows of one level depend only on
+/// rows of earlier levels.  A level is split into chunks of <= kTriRows rows
+/// (one lane of the solving warp each) and <= kTriBlockCap bytes.  Entry e of
+/// row l of chunk c lives at base[c] + e * nrows[c] + l.
 ///
-/// Every row of a chunk is padded to the chunk's `span` entries (a multiple of
-/// kTriRing, plus one extra ring block so prefetches never leave the chunk)
-/// with neutral dummies (column n, value +0.0): the device keeps z[n] = +0.0,
-/// and s - (+0.0 * +0.0) == s exactly, so the padded sum is bit-identical.
-constexpr int kTriRing = 8;
-constexpr int kTriRows = 8;  // rows per chunk (one lane each)
+/// Every row of a chunk is padded to the chunk's `span` (the longest row,
+/// rounded up to even) with neutral dummies (column n, value +0.0): the device
+/// keeps z[n] = +0.0 and s - (+0.0 * +0.0) == s exactly, so the padded sum is
+/// bit-identical.
+constexpr int kTriRows = 32;
 struct TriPlan {
     int n = 0, n_levels = 0, n_chunks = 0, max_row_len = 0;
     std::vector<int> level_chunk;  // n_levels + 1
@@ -84,25 +84,23 @@ struct TriPlan {
 TriPlan plan_lower(const HostCsr& lower);
 TriPlan plan_upper(const HostCsr& upper);
 
-/// Level-ordered block stream for the TMA-fed, level-synchronous device solve.
-/// One block = one chunk (<= kTriRows rows of a single level) with every
-/// entry of its rows, stored so that a single cp.async.bulk fetches it:
-///   header (32 B): nr, span (entries per row, even), row0,
-///                  next_off16, next_bytes (block b + kTriSlots - 1, 0 if none),
-///                  3 x pad
-///   rows: 8 x int32 (original row index per lane), diag: 8 x double (U only)
-///   cols: span x nr int32   (entry e of row l at e * nr + l)
-///   vals: span x nr double
-/// Offsets are in 16-byte units of `stream`; `prime` holds (off16, bytes) of
-/// the first kTriSlots - 1 blocks.
-constexpr int kTriSlots = 4;
-constexpr int kTriBlockPrefix = 128;  // header + rows + diag
+/// Level-ordered block stream for the TMA-fed warp solve.  One block = one
+/// chunk with every entry of its rows, fetched by a single cp.async.bulk:
+///   header (32 B): nr, span, row0, next_off16, next_bytes (block
+///                  b + kTriSlots - 1, 0 if none), cols_off, vals_off, diag_off
+///   rows  int32[nr]          at 32 (padded to 8 bytes)
+///   diag  double[nr]         at diag_off      (upper only)
+///   rdiag double[nr]         at diag_off + 8 nr (upper only; RN(1 / diag))
+///   cols  int32[span * nr]   at cols_off      (entry e of row l at e * nr + l)
+///   vals  double[span * nr]  at vals_off
+/// Blocks are 16-byte aligned; offsets in the header are bytes from the block
+/// start, `next_off16` and `prime` are in 16-byte units of `stream`; `prime`
+/// holds (off16, bytes) of the first kTriSlots - 1 blocks.
 struct TriStream {
     std::vector<unsigned char> stream;
     std::vector<int> prime;  // 2 * (kTriSlots - 1)
     int n_blocks = 0;
     int max_block_bytes = 0;
-    int max_items = 0;       // max nr * span over blocks (product scratch)
 };
 TriStream make_tri_stream(const TriPlan& p);
 

@@ -48,7 +48,7 @@ class NotConvergedError(RuntimeError):
 
 class PmgOptions(C.Structure):
     _fields_ = [("ilut_tau", C.c_double), ("ilut_fill", C.c_int), ("nu_pre", C.c_int),
-                ("nu_post", C.c_int), ("gs_pre", C.c_int), ("gs_post", C.c_int)]
+                ("nu_post", C.c_int), ("gs_pre", C.c_int), ("gs_post", C.c_int), ("exact", C.c_int)]
 
 
 class SolverConfig(C.Structure):
@@ -160,8 +160,8 @@ def default_solver_config(**kw) -> SolverConfig:
     c = SolverConfig()
     lib().phi_default_solver_config(C.byref(c))
     for k, v in kw.items():
-        if k in ("ilut_tau", "ilut_fill", "nu_pre", "nu_post", "gs_pre", "gs_post"):
-            setattr(c.pmg, k, v)
+        if k in ("ilut_tau", "ilut_fill", "nu_pre", "nu_post", "gs_pre", "gs_post", "exact"):
+            setattr(c.pmg, k, int(v) if k == "exact" else v)
         else:
             setattr(c, k, v)
     return c
@@ -235,10 +235,12 @@ class PMultigridHierarchy:
     """PMultigridHierarchy(disc, c, opt) (pmultigrid.hpp:215-324), device resident."""
 
     def __init__(self, disc: SpatialDiscretization, c: float, nu_pre=1, nu_post=1, gs_pre=2,
-                 gs_post=2, ilut_tau=1e-13, ilut_fill=0):
+                 gs_post=2, ilut_tau=1e-13, ilut_fill=0, exact=False):
+        """exact=True: the reference's summation order (bit-identical results);
+        False: reassociated parallel sums (within the solver tolerance)."""
         self.disc = disc
         self.n = disc.n_free
-        opt = PmgOptions(ilut_tau, ilut_fill, nu_pre, nu_post, gs_pre, gs_post)
+        opt = PmgOptions(ilut_tau, ilut_fill, nu_pre, nu_post, gs_pre, gs_post, int(exact))
         self.h = _vp()
         _check(lib().phi_hier_create(disc.h, c, C.byref(opt), C.byref(self.h)))
 
@@ -358,7 +360,7 @@ class MgritSolver:
                  source_kind=SOURCE_CONSTANT, source_param=1.0, init_kind=INIT_ZERO,
                  init_coeffs=None, load_terms=None, load_terms_steady=False, cycle=CYCLE_V,
                  relax=RELAX_FCF, m=2, halt_tol=1e-10, max_iter=50, coarse_floor=8,
-                 solver: SolverConfig | None = None):
+                 solver: SolverConfig | None = None, exact: bool | None = None):
         self.disc = disc
         self.nt = nt
         self.max_iter = max_iter
@@ -369,6 +371,8 @@ class MgritSolver:
                      None if self._loads is None else self._loads.ctypes.data, int(load_terms_steady))
         cfg = MgritConfig(cycle, relax, m, halt_tol, max_iter, coarse_floor)
         scfg = solver or default_solver_config()
+        if exact is not None:
+            scfg.pmg.exact = int(exact)
         self.h = _vp()
         _check(lib().phi_mgrit_create(disc.h, C.byref(ps), C.byref(cfg), C.byref(scfg),
                                       C.byref(self.h)))

@@ -1,0 +1,101 @@
+"""GPU parity of the engine's default (reassociated) summation mode.
+
+In the default mode (phi_pmg_options.exact = 0) every reduction on the solve
+path is a parallel tree instead of the reference's left-to-right sum, so the
+results are not bit-identical.  The bar is the north-star tolerance
+(BASELINE.json): MGRIT and p-multigrid iteration counts within +-1 of the
+reference and the final space-time solution within 1e-8 relative L2.  The
+building blocks are held to a few ulps of accumulated rounding (rel 1e-12).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+E = pytest.importorskip("paper_2107_05337_b200.engine")
+
+TOL_TRAJ = 1e-8   # north star: final space-time solution, relative L2
+TOL_BLOCK = 1e-12  # one operator application: reassociation only
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def _ref_or_skip():
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built (make -C oracle ref)")
+
+
+@pytest.mark.parametrize("p,k,c", [(2, 4, 1e-3), (3, 6, 1e-4), (5, 5, 0.01)])
+def test_fast_building_blocks(p, k, c):
+    _ref_or_skip()
+    d = E.SpatialDiscretization.build(p, k)
+    h = E.PMultigridHierarchy(d, c)
+    r = O.RefHier(O.RefDisc(p, k), c)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(d.n_free)
+    b1 = rng.standard_normal(d.n_free_1)
+    assert _rel(h.spmv(b), r.csr(0).spmv(b)) <= TOL_BLOCK
+    assert _rel(h.ilut_apply(b), r.ilut_apply(b)) <= TOL_BLOCK
+    assert _rel(h.restrict_to_linear(b), r.restrict(b)) <= TOL_BLOCK
+    assert _rel(h.prolong_from_linear(b1), r.prolong(b1)) <= TOL_BLOCK
+    assert _rel(h.gauss_seidel_sweep(0, b1, b1), r.gs_sweep(0, b1, b1)) <= TOL_BLOCK
+    assert _rel(h.hmg_wcycle(b1), r.hmg_wcycle(b1)) <= 1e-10
+    assert _rel(h.vcycle(b, np.zeros(d.n_free)), r.vcycle(b, np.zeros(d.n_free))) <= 1e-10
+
+
+@pytest.mark.parametrize("p,k,c", [(2, 5, 0.01), (3, 6, 8e-4)])
+def test_fast_solve_iterations(p, k, c):
+    _ref_or_skip()
+    d = E.SpatialDiscretization.build(p, k)
+    h = E.PMultigridHierarchy(d, c)
+    r = O.RefHier(O.RefDisc(p, k), c)
+    rng = np.random.default_rng(11)
+    B = rng.standard_normal((4, d.n_free))
+    got = h.solve(B, None)
+    for i in range(4):
+        ref = r.solve(B[i])
+        assert abs(int(got["iterations"][i]) - ref["iterations"]) <= 1
+        assert got["converged"][i]
+        assert _rel(got["x"][i], ref["x"]) <= 1e-10
+
+
+@pytest.mark.parametrize("case", [
+    dict(p=2, k=4, nt=100, m=4, cycle=E.CYCLE_TWO_LEVEL, source_param=0.0, init_kind=E.INIT_SIN),
+    dict(p=2, k=3, nt=64, m=2, cycle=E.CYCLE_V),
+    dict(p=3, k=5, nt=64, m=8, cycle=E.CYCLE_TWO_LEVEL, source_kind=E.SOURCE_SIN_EXP,
+         source_param=2 * np.pi ** 2, init_kind=E.INIT_COEFFS),
+])
+def test_fast_mgrit_within_tolerance(case):
+    _ref_or_skip()
+    case = dict(case)
+    p, k, nt = case.pop("p"), case.pop("k"), case.pop("nt")
+    if case.get("init_kind") == E.INIT_COEFFS:
+        case["init_coeffs"] = np.random.default_rng(12345).uniform(-1, 1, (2 ** k + p - 2) ** 2)
+    eng = E.MgritSolver(E.SpatialDiscretization.build(p, k), nt, **case)
+    ref = O.RefMgrit(p, k, nt, **case)
+    rg, rr = eng.solve(), ref.solve()
+    assert abs(rg.iterations - rr["iterations"]) <= 1
+    assert rg.converged
+    assert abs(rg.mean_spatial_iterations - rr["mean_spatial_iterations"]) <= 1.0
+    assert abs(rg.g_norm - rr["g_norm"]) <= 1e-10 * rr["g_norm"]
+    assert _rel(eng.trajectory(), ref.trajectory()) <= TOL_TRAJ
+
+
+def test_fast_and_exact_modes_agree_on_config2_shape():
+    """Same solver, both modes, config-2 operator at reduced Nt: the modes
+    differ only by rounding."""
+    p, k, nt = 3, 6, 64
+    coeffs = np.random.default_rng(12345).uniform(-1, 1, (2 ** k + p - 2) ** 2)
+    kw = dict(cycle=E.CYCLE_TWO_LEVEL, m=8, source_kind=E.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2,
+              init_kind=E.INIT_COEFFS, init_coeffs=coeffs)
+    d = E.SpatialDiscretization.build(p, k)
+    fast, exact = E.MgritSolver(d, nt, **kw), E.MgritSolver(d, nt, exact=True, **kw)
+    rf, re_ = fast.solve(), exact.solve()
+    assert abs(rf.iterations - re_.iterations) <= 1
+    assert _rel(fast.trajectory(), exact.trajectory()) <= TOL_TRAJ

@@ -1,7 +1,8 @@
 """GPU parity: the CUDA engine (through its C ABI) against the reference.
 
-Bar: bit-identical.  The engine evaluates every reference reduction in the
-reference's order without fused multiply-adds, so operators, V-cycles,
+Bar: bit-identical.  In its exact mode (phi_pmg_options.exact = 1) the
+engine evaluates every reference reduction in the reference's order without
+fused multiply-adds, so operators, V-cycles,
 solves, Phi steps and MGRIT trajectories must equal the reference (oracle/_ref,
 the unmodified reference compiled from /root/reference) and the C restatement
 (oracle/phi_oracle.c) exactly.  np.array_equal is the assertion throughout.
@@ -16,6 +17,9 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 E = pytest.importorskip("paper_2107_05337_b200.engine")
+# the bitwise tests run the engine in its exact mode (reference summation
+# order); the default reassociated mode is covered by test_gpu_fast.py
+EXACT = E.default_solver_config(exact=1)
 
 
 def _same_csr(a, b, what):
@@ -56,7 +60,7 @@ def test_device_assembly_matches_reference(p, k):
 def test_hierarchy_matches_reference(p, k, c):
     _ref_or_skip()
     d = disc(p, k)
-    h = E.PMultigridHierarchy(d, c)
+    h = E.PMultigridHierarchy(d, c, exact=True)
     r = O.RefHier(O.RefDisc(p, k), c)
     for which in [0, 1, 2] + [100 + l for l in range(d.n_h_levels)]:
         _same_csr(h.csr(which), r.csr(which), f"hier {which}")
@@ -70,7 +74,7 @@ def _oc(d: "E.SpatialDiscretization", c):
 @pytest.mark.parametrize("p,k,c", [(2, 4, 1e-3), (3, 5, 1e-4), (4, 5, 4e-5)])
 def test_building_blocks_bitwise(p, k, c):
     d = disc(p, k)
-    h = E.PMultigridHierarchy(d, c)
+    h = E.PMultigridHierarchy(d, c, exact=True)
     od, oh = _oc(d, c)
     rng = np.random.default_rng(7)
     r = rng.standard_normal(d.n_free)
@@ -92,7 +96,7 @@ def test_building_blocks_bitwise(p, k, c):
 @pytest.mark.parametrize("p,k,c,nrhs", [(2, 4, 1e-3, 5), (3, 6, 1e-4, 3), (5, 5, 1e-4, 2)])
 def test_vcycle_batched_bitwise(p, k, c, nrhs):
     d = disc(p, k)
-    h = E.PMultigridHierarchy(d, c)
+    h = E.PMultigridHierarchy(d, c, exact=True)
     od, oh = _oc(d, c)
     rng = np.random.default_rng(11)
     b = rng.standard_normal((nrhs, d.n_free))
@@ -105,7 +109,7 @@ def test_vcycle_batched_bitwise(p, k, c, nrhs):
 def test_solve_batched_bitwise_with_zero_rhs_and_early_exit():
     d = disc(3, 5)
     c = 1e-3
-    h = E.PMultigridHierarchy(d, c)
+    h = E.PMultigridHierarchy(d, c, exact=True)
     od, oh = _oc(d, c)
     rng = np.random.default_rng(3)
     b = rng.standard_normal((4, d.n_free))
@@ -124,7 +128,7 @@ def test_solve_batched_bitwise_with_zero_rhs_and_early_exit():
 
 def test_solve_fixed_cycles_and_x0_empty():
     d = disc(2, 5)
-    h = E.PMultigridHierarchy(d, 0.01)
+    h = E.PMultigridHierarchy(d, 0.01, exact=True)
     od, oh = _oc(d, 0.01)
     b = np.random.default_rng(5).standard_normal(d.n_free)
     got = h.solve(b, None, fixed_cycles=3)
@@ -136,7 +140,7 @@ def test_solve_fixed_cycles_and_x0_empty():
 def test_theta_step_bitwise(theta):
     d = disc(2, 5)
     dt = 1e-3
-    st = E.ThetaStepper(d, 1.0, dt, theta)
+    st = E.ThetaStepper(d, 1.0, dt, theta, EXACT)
     od = O.OcDisc(d.operators())
     ost = O.OcStepper(od, 1.0, dt, theta)
     rng = np.random.default_rng(13)
@@ -152,7 +156,7 @@ def test_theta_step_bitwise(theta):
 def test_sequential_integrate_bitwise():
     d = disc(2, 4)
     nt, dt = 32, 0.1 / 32
-    st = E.ThetaStepper(d, 1.0, dt, 1.0)
+    st = E.ThetaStepper(d, 1.0, dt, 1.0, EXACT)
     od = O.OcDisc(d.operators())
     u0 = np.random.default_rng(17).uniform(-1, 1, d.n_free)
     load = np.full(d.n_free, 1e-3)
@@ -164,7 +168,7 @@ def test_sequential_integrate_bitwise():
 def _mgrit_pair(p, k, nt, **kw):
     _ref_or_skip()
     d = disc(p, k)
-    eng = E.MgritSolver(d, nt, **kw)
+    eng = E.MgritSolver(d, nt, exact=True, **kw)
     ref = O.RefMgrit(p, k, nt, **kw)
     return eng, ref
 

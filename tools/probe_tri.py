@@ -1,0 +1,36 @@
+"""Developer probe: per-block phase timing of the warp triangular solve
+(trace stamps in tri_solve_warp) for one ILUT application (L then U)."""
+import ctypes as C
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2107_05337_b200 as P  # noqa: E402
+from paper_2107_05337_b200 import engine as E  # noqa: E402
+
+BASE = 24000
+d = P.SpatialDiscretization.build(3, 6)
+h = P.PMultigridHierarchy(d, 1e-4, exact=len(sys.argv) > 1 and sys.argv[1] == "exact")
+r = np.random.default_rng(0).standard_normal(d.n_free)
+h.ilut_apply(r)
+for kind in ("unit", "solve"):
+    E.dev_tuning(8, 8, -1)
+    if kind == "unit":
+        h.ilut_apply(r)
+    else:
+        h.solve(r, None, fixed_cycles=1)
+    buf = np.zeros(49152, np.int64)
+    E.lib().phi_dev_trace(buf.ctypes.data_as(C.c_void_p), buf.size)
+    t = buf[BASE:BASE + 8 * 1024].reshape(1024, 8).astype(np.float64)
+    nb = int((t[:, 0] > 0).sum())
+    t = t[:nb]
+    wait = t[:, 1] - t[:, 0]
+    ph1 = t[:, 2] - t[:, 1]
+    ph2 = t[:, 3] - t[:, 2]
+    gap = t[1:, 0] - t[:-1, 3]
+    iss = t[:, 4] - t[:, 1]
+    acc = t[:, 5] - t[:, 4]
+    print(f"   issue {np.median(iss):.0f}  accumulate {np.median(acc):.0f}  shuffle {np.median(t[:, 2] - t[:, 5]):.0f}")
+    print(f"{kind}: blocks {nb}  wait {np.median(wait):.0f}/{wait.mean():.0f}  ph1 {np.median(ph1):.0f}/{ph1.mean():.0f}  "
+          f"ph2 {np.median(ph2):.0f}/{ph2.mean():.0f}  gap {np.median(gap):.0f}/{gap.mean():.0f} (median/mean cycles)")

@@ -8,6 +8,8 @@ import numpy as np
 sys.path.insert(0, ".")
 import paper_2107_05337_b200 as P  # noqa: E402
 
+EXACT = "exact" in sys.argv
+
 
 def t(fn, reps=5):
     fn()
@@ -19,7 +21,7 @@ def t(fn, reps=5):
 
 def probe(p, k, c):
     d = P.SpatialDiscretization.build(p, k)
-    h = P.PMultigridHierarchy(d, c)
+    h = P.PMultigridHierarchy(d, c, exact=EXACT)
     rng = np.random.default_rng(0)
     n, n1 = d.n_free, d.n_free_1
     r = rng.standard_normal(n)
