@@ -26,6 +26,8 @@ CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+if os.environ.get("PHI_TRACE") == "1":  # developer timing stamps (tools/probe_*.py)
+    NVCC_FLAGS += ["-DPHI_TRACE_ON=1"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-unused-function",
              f"-I{CUDA_INC}"]
 
@@ -53,6 +55,15 @@ def _run(cmd: list[str], log: list[str]) -> None:
 def build(verbose: bool = False) -> str:
     os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "phi_engine.h")]
+    # a change of compiler flags (e.g. PHI_TRACE) invalidates every object
+    stamp = os.path.join(OUT_DIR, "obj", "flags.txt")
+    flags = " ".join(NVCC_FLAGS + CXX_FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        for f in os.listdir(os.path.join(OUT_DIR, "obj")):
+            if f.endswith(".o"):
+                os.remove(os.path.join(OUT_DIR, "obj", f))
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     jobs, objs = [], []  # compile commands still to run; every object of the library
     for src in CU:
         s = os.path.join(CSRC, src)

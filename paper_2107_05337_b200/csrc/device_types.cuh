@@ -29,23 +29,23 @@ struct DevCsr {
 };
 
 /// Depth of the shared-memory ring that stages triangular-factor blocks.
-constexpr int kTriSlots = 8;
+constexpr int kTriSlots = 4;
 /// Bytes per triangular-factor block (TriPlan chunking) and the product
 /// scratch that bound implies (12 bytes per entry: int32 column + fp64 value).
-constexpr int kTriBlockCap = 12 * 1024;
+constexpr int kTriBlockCap = 5 * 1024;
 constexpr int kTriMaxItems = kTriBlockCap / 12;
 
 /// Level-scheduled triangular factor as a TMA block stream (TriStream).
 struct DevTri {
-    int n, n_levels, n_blocks;
-    int max_block_bytes;
+    int n, n_levels, n_units;
+    int max_unit_bytes;
     int prime[2 * (kTriSlots - 1)];  // (off16, bytes) of the first kTriSlots - 1 blocks
     const unsigned char* stream;  // 16-byte aligned
 };
 
 struct DevHLevel {
     DevStencil a;    // M_l + c K_l, 9-point
-    const double* rdiag;  // RN(1 / a_ii) (Gauss-Seidel division, div_rn)
+    DevTri gs_fwd, gs_bwd;  // Gauss-Seidel sweeps as level-scheduled streams (empty on the coarsest)
     DevCsr embed;    // level l+1 -> level l (empty on the coarsest)
     DevCsr embed_t;  // its transpose (restriction rows, ascending fine index)
     int n;
@@ -82,7 +82,7 @@ struct SmemPlan {
     int prod_off;          // triangular-solve product scratch (kTriMaxItems)
     int dot_off;           // ordered-dot scratch
     int z_off;             // in-place triangular-solve vector (n_p + 1)
-    int lvl_off[kMaxH];    // per h-level: b, x, x2, r (4 n_l)
+    int lvl_off[kMaxH];    // per h-level: b, x, r (3 n_l)
     int total;             // doubles
 };
 

@@ -162,19 +162,19 @@ void Disc::assemble_load(int kind, double c0, double c1, const double* coeffs_de
 // Hier
 // ---------------------------------------------------------------------------
 namespace {
-void upload_tri(const TriPlan& p, Hier::TriDev& d, cudaStream_t s) {
-    const TriStream ts = make_tri_stream(p);
+void upload_tri(const TriPlan& p, bool fast, Hier::TriDev& d, cudaStream_t s) {
+    const TriStream ts = make_tri_stream(p, fast);
     d.stream = dev(ts.stream, s);  // cudaMalloc: 256-byte aligned
-    d.n_blocks = ts.n_blocks;
-    d.max_block_bytes = ts.max_block_bytes;
+    d.n_units = ts.n_units;
+    d.max_unit_bytes = ts.max_unit_bytes;
     for (int k = 0; k < 2 * (kTriSlots - 1); ++k) d.prime[k] = ts.prime[k];
 }
 DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
     DevTri t{};
     t.n = p.n;
     t.n_levels = p.n_levels;
-    t.n_blocks = d.n_blocks;
-    t.max_block_bytes = d.max_block_bytes;
+    t.n_units = d.n_units;
+    t.max_unit_bytes = d.max_unit_bytes;
     for (int k = 0; k < 2 * (kTriSlots - 1); ++k) t.prime[k] = d.prime[k];
     t.stream = d.stream.get();
     return t;
@@ -193,8 +193,8 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     ilut_factor(ah, opt.ilut_tau, opt.ilut_fill, L_host, U_host);
     Lp = plan_lower(L_host);
     Up = plan_upper(U_host);
-    upload_tri(Lp, Ld, s);
-    upload_tri(Up, Ud, s);
+    upload_tri(Lp, opt.exact == 0, Ld, s);
+    upload_tri(Up, opt.exact == 0, Ud, s);
     for (const auto& hl : d.h) {
         StencilBuf a;
         a.ru = a.rv = a.cu = a.cv = hl.nf;
@@ -202,10 +202,17 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
         a.hi = 1;
         a.vals.alloc(a.size());
         launch_axpby(hl.M.vals.get(), c, hl.K.vals.get(), a.vals.get(), a.size(), s);
-        DevBuf<double> rd(hl.n);
-        launch_recip(a.vals.get() + 4 * (size_t)hl.n, rd.get(), hl.n, s);  // centre entry (du, dv) = (0, 0)
         a_h.push_back(std::move(a));
-        a_h_rdiag.push_back(std::move(rd));
+    }
+    // Gauss-Seidel sweeps of the h-levels as level-scheduled streams
+    // (wavefronts), in the hierarchy's summation mode
+    for (size_t l = 0; l + 1 < a_h.size(); ++l) {
+        const HostCsr al = stencil_to_csr(a_h[l]);
+        for (int dir = 0; dir < 2; ++dir) {
+            gs_plans.push_back(plan_gauss_seidel(al, dir == 1));
+            gs_dev.emplace_back();
+            upload_tri(gs_plans.back(), opt.exact == 0, gs_dev.back(), s);
+        }
     }
     coarse = dense_lu_factor(stencil_to_csr(a_h.back()));
     coarse_lu = dev(coarse.lu, s);
@@ -232,7 +239,10 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     for (int l = 0; l < H.n_h; ++l) {
         const auto& hl = d.h[l];
         H.h[l].a = a_h[l].view();
-        H.h[l].rdiag = a_h_rdiag[l].get();
+        if (l + 1 < H.n_h) {
+            H.h[l].gs_fwd = tri_view(gs_plans[2 * l], gs_dev[2 * l]);
+            H.h[l].gs_bwd = tri_view(gs_plans[2 * l + 1], gs_dev[2 * l + 1]);
+        }
         H.h[l].n = hl.n;
         if (l + 1 < H.n_h) {
             H.h[l].embed = DevCsr{hl.E.n_rows, hl.E.n_cols, hl.e_ro.get(), hl.e_ci.get(), hl.e_v.get()};

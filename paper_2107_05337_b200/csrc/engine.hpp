@@ -95,14 +95,15 @@ public:
     HierOptions opt;
     StencilBuf A;                       // M + c K
     std::vector<StencilBuf> a_h;        // per h-level
-    std::vector<DevBuf<double>> a_h_rdiag;  // RN(1 / diagonal) per h-level
     HostCsr L_host, U_host;             // ILUT factors (host copy)
     TriPlan Lp, Up;
     struct TriDev {
         DevBuf<unsigned char> stream;
-        int n_blocks = 0, max_block_bytes = 0;
+        int n_units = 0, max_unit_bytes = 0;
         int prime[2 * (kTriSlots - 1)] = {};
     } Ld, Ud;
+    std::vector<TriPlan> gs_plans;  // per h-level (but the coarsest): forward, backward
+    std::vector<TriDev> gs_dev;
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;
     DevBuf<int> coarse_piv;

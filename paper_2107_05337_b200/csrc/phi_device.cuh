@@ -91,10 +91,14 @@ __device__ __forceinline__ int lds_s32(unsigned a) {
 }
 // Developer phase stamps (trace enabled, CTA 0, thread 0): (id, clock64) pairs
 // after a counter at trace[kStampBase].
+#ifndef PHI_TRACE_ON
+#define PHI_TRACE_ON 0  // developer timing stamps (build with PHI_TRACE=1)
+#endif
+constexpr bool kTrace = PHI_TRACE_ON != 0;
 constexpr int kStampBase = 40000, kStampMax = 4000;
 constexpr int kTriTraceBase = 24000;  // 4 x 2048 stamps (< kStampBase)
 __device__ __forceinline__ void pstamp(int id) {
-    if (c_tune.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (kTrace && c_tune.trace && blockIdx.x == 0 && threadIdx.x == 0) {
         const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(c_tune.trace + kStampBase), 1ULL);
         if (k < kStampMax) {
             c_tune.trace[kStampBase + 1 + 2 * k] = id;
@@ -125,9 +129,9 @@ struct Ws {
     double* z;               // in-place triangular-solve vector (n_p + 1 slots)
     double* dot;             // shared scratch for ordered dots
     int z_off, ring_off, slot_bytes, prod_off;  // g_smem offsets (-1: global)
+    int lvl_off[kMaxH];  // g_smem offset of level l's vectors (b, x, r), -1: global
     double* hb[kMaxH];
     double* hx[kMaxH];
-    double* hx2[kMaxH];
     double* hr[kMaxH];
 };
 
@@ -147,12 +151,12 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     double* g = base + 6 * np;
     for (int l = 0; l < H.n_h; ++l) {
         const int nl = H.h[l].n;
+        w.lvl_off[l] = P.lvl_off[l];
         double* s = P.lvl_off[l] >= 0 ? smem + P.lvl_off[l] : g;
         w.hb[l] = s;
         w.hx[l] = s + nl;
-        w.hx2[l] = s + 2 * (size_t)nl;
-        w.hr[l] = s + 3 * (size_t)nl;
-        g += 4 * (size_t)nl;
+        w.hr[l] = s + 2 * (size_t)nl + 1;  // x has a zero slot x[n] (padded sweep entries)
+        g += 3 * (size_t)nl + 1;
     }
     return w;
 }
@@ -279,124 +283,11 @@ __device__ __forceinline__ void csr_apply(const DevCsr& A, const double* __restr
     }
 }
 
-// Lexicographic Gauss-Seidel sweeps (solvers.hpp:80-99) for the 9-point
-// order-1 operator, in place, by anti-diagonal wavefronts u + 2v = t
-// (forward; mirrored for backward): a row of wavefront t reads updated values
-// only from wavefronts < t and old values only from wavefronts > t, so
-// updating a whole wavefront between two barriers gives exactly the
-// sequential sweep.  ONE warp runs the sweeps (lane q owns rows q, q + 32, ..
-// of each wavefront; __syncwarp() between wavefronts).  The nine matrix
-// entries and the reciprocal diagonal of a lane's first row of the next
-// wavefront are prefetched while the current one is solved.  Entries outside
-// the grid carry a = +0.0 and x = +0.0, and s - (+0 * +0) == s, so the
-// branch-free row sum is bit-identical.
-template <bool SM>
-__device__ __noinline__ void gs_sweeps_warp(const DevStencil& A, const double* __restrict__ rdiag,
-                                            const double* __restrict__ b, double* x, bool backward, int count,
-                                            bool exact) {
-    const unsigned b_s = SM ? sh_addr(b) : 0u, x_s = SM ? sh_addr(x) : 0u;
-    const int nu = A.ru, nv = A.rv, n = nu * nv;
-    const double* __restrict__ av = A.vals;  // cached: A lives in the param space
-    const int T = (nu - 1) + 2 * (nv - 1);
-    const int lane = threadIdx.x & 31;
-    auto row_of = [&](int t, int q, int& iu, int& iv) {
-        const int vlo = max(0, (t - (nu - 1) + 1) / 2);
-        const int vhi = min(nv - 1, t / 2);
-        const int v = vlo + q;
-        if (v > vhi) return -1;
-        const int u = t - 2 * v;
-        iu = backward ? nu - 1 - u : u;
-        iv = backward ? nv - 1 - v : v;
-        return iu + nu * iv;
-    };
-    // Unconditional loads: the stencil-major array stores +0.0 for entries
-    // outside the grid, so no select (which would wait on the fresh load) is
-    // needed, and +0 * +0 leaves the row sum bit-identical.
-    auto fetch = [&](int t, double* a) {
-        int iu = 0, iv = 0;
-        int i = t <= T ? row_of(t, lane, iu, iv) : -1;
-        if (i < 0) i = 0;
-#pragma unroll
-        for (int e = 0; e < 9; ++e) a[e] = __ldg(av + (size_t)e * n + i);
-        a[9] = __ldg(rdiag + i);
-    };
-    auto process = [&](int t, double (&a)[10]) {
-        long long* tr = (c_tune.trace && lane == 0 && t < 1024) ? c_tune.trace + (size_t)NW * 1024 * 2 + (size_t)t * 4
-                                                                : nullptr;
-        if (tr) tr[0] = clock64();
-        int iu = 0, iv = 0;
-        for (int q = lane;; q += 32) {
-            const int i = row_of(t, q, iu, iv);
-            if (i < 0) break;
-            if (q != lane) {  // rows beyond the first 32 of a wavefront: no prefetch
-#pragma unroll
-                for (int e = 0; e < 9; ++e) a[e] = __ldg(av + (size_t)e * n + i);
-                a[9] = __ldg(rdiag + i);
-            }
-            double xv[9];
-#pragma unroll
-            for (int e = 0; e < 9; ++e) {
-                const int dv = e / 3 - 1, du = e % 3 - 1;
-                const bool ok = e != 4 && iu + du >= 0 && iu + du < nu && iv + dv >= 0 && iv + dv < nv;
-                const int j = i + du + nu * dv;
-                xv[e] = ok ? (SM ? lds_f64(x_s + 8u * j) : x[j]) : 0.0;
-            }
-            double s = SM ? lds_f64(b_s + 8u * i) : b[i];
-            double p[9];
-#pragma unroll
-            for (int e = 0; e < 9; ++e) p[e] = a[e] * xv[e];
-            if (exact) {  // the reference's order: (dv, du) ascending
-#pragma unroll
-                for (int e = 0; e < 9; ++e)
-                    if (e != 4) s = s - p[e];
-            } else {  // reassociated: a depth-3 tree
-                s = s - (((p[0] + p[1]) + (p[2] + p[3])) + ((p[5] + p[6]) + (p[7] + p[8])));
-            }
-            if (tr && q == lane) tr[1] = clock64() + (long long)(s == 12345.678);  // s is ready
-            const double xi = div_rn(s, a[4], a[9]);
-            if (SM)
-                asm volatile("st.shared.f64 [%0], %1;" ::"r"(x_s + 8u * i), "d"(xi) : "memory");
-            else
-                x[i] = xi;
-            if (tr && q == lane) tr[2] = clock64() + (long long)(xi == 12345.678);
-        }
-        __syncwarp();
-        if (tr) tr[3] = clock64();
-    };
-    // two register buffers alternated by a 2x-unrolled wavefront loop: a
-    // prefetched row is consumed in place, never copied (a copy would wait on
-    // the load that was just issued)
-    double abuf0[10], abuf1[10];
-    for (int c = 0; c < count; ++c) {
-        fetch(0, abuf0);
-        for (int t = 0; t <= T; t += 2) {
-            fetch(t + 1, abuf1);
-            process(t, abuf0);
-            if (t + 1 > T) break;
-            fetch(t + 2, abuf0);
-            process(t + 1, abuf1);
-        }
-    }
-}
-
-// `count` sweeps by warp 0; the CTA joins at the closing barrier.
-__device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, double* x, bool backward,
-                                          int count, bool exact) {
-    if (threadIdx.x < 32) {
-        if (__isShared(x))
-            gs_sweeps_warp<true>(lv.a, lv.rdiag, b, x, backward, count, exact);
-        else
-            gs_sweeps_warp<false>(lv.a, lv.rdiag, b, x, backward, count, exact);
-    }
-    __syncthreads();
-}
-
 // ---- triangular solves: one warp, TMA-fed ------------------------
-// The factor is one level-ordered stream of blocks (TriStream), each holding a
-// chunk of <= kTriRows rows of one level with all their entries.  A ring of
-// kTriSlots shared-memory slots is filled by TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx), kTriSlots-1 blocks ahead; the next
-// block's address travels in the header of the block being consumed.
+// The factor is one level-ordered stream of blocks (TriStream), packed into
+// fetch units.  A ring of kTriSlots shared-memory slots is filled by TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx), kTriSlots-1 units ahead; the
+// next unit's address travels in the header of the unit being consumed.
 __device__ __forceinline__ void mbar_init(unsigned bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
 }
@@ -419,172 +310,193 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 
 // In-place substitution with an ILUT factor (ilut.hpp:146-163) on z, which
 // holds the right-hand side on entry.  Lower: z_i -= sum_j L_ij z_j (unit
-// diagonal).  Upper: z_i = (z_i - sum_j U_ij z_j) / U_ii.  Executed by ONE warp, block by
-// block (a block is one level, or a slice of a wide level):
-//   1. all 32 lanes form the block's products L_ij * z_j (every z_j belongs
-//      to an earlier level) into shared scratch -- wide, independent loads;
-//   2. lane l subtracts row l's products in CSR order -- the reference's
-//      exact sequence of roundings, a pure load + add chain -- and publishes
-//      z_i.
-// __syncwarp() (a memory barrier among the lanes) separates the phases and
-// closes the block.  Blocks stream through a kTriSlots ring filled by TMA
-// kTriSlots-1 blocks ahead.  Padded entries (column n, value +0.0;
-// z[n] = +0.0) are exactly neutral.
-template <bool UPPER, bool ZSM>
-__device__ __noinline__ void tri_solve_warp(const DevTri& T, double* zg, int z_off, int ring_off, int slot_bytes,
-                                            int prod_off, unsigned bar, bool exact) {
+// diagonal).  Upper: z_i = (z_i - sum_j U_ij z_j) / U_ii.  Executed by ONE
+// warp, block by block (a block holds the rows of one level, or a slice of a
+// wide level; every z_j it reads belongs to an earlier block):
+//  exact: 1. all 32 lanes form the block's products into shared scratch;
+//         2. lane l subtracts row l's products in CSR order -- the
+//            reference's exact sequence of roundings -- and publishes z_i;
+//  fast:  G = 2^lg lanes per row (chosen per block on the host); each lane
+//         sums its contiguous slice of the row with two accumulators, a
+//         butterfly over the G lanes completes the sum, and the row's first
+//         lane publishes z_i (division by the stored reciprocal).
+// __syncwarp() (a memory barrier among the lanes) closes each block.  Padded
+// entries (column n, value +0.0; z[n] = +0.0) are exactly neutral.
+template <bool UPPER, bool ZSM, bool EXACT>
+__device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
+                                              int ring_off, int slot_bytes, int prod_off, unsigned bar) {
     const int lane = threadIdx.x & 31;
     const unsigned ring = sh_addr(g_smem + ring_off);
     const unsigned prod = sh_addr(g_smem + prod_off);
     const unsigned zs = ZSM ? sh_addr(g_smem + z_off) : 0u;
+    // right-hand side of row i: z_i itself (in-place ILUT substitution) or a
+    // separate vector (Gauss-Seidel: b_i), shared (ZSM) or global
+    const unsigned rs = ZSM ? sh_addr(g_smem + r_off) : 0u;
     // cached: T lives in the kernel parameter space (generic loads otherwise)
-    const int n_blocks = T.n_blocks;
+    const int n_units = T.n_units;
     const unsigned char* __restrict__ stream = T.stream;
     if (lane == 0)
-        for (int k = 0; k < kTriSlots - 1 && k < n_blocks; ++k)
+        for (int k = 0; k < kTriSlots - 1 && k < n_units; ++k)
             bulk_fetch(ring + k * slot_bytes, stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
                        bar + 8u * k);
     // developer trace (CTA 0, lane 0, first 1024 blocks): block start, data
-    // ready, products done, block done, prefetch issued, row sums -- at
-    // trace[kTriTraceBase + 8 b]
-    long long* tr = (c_tune.trace && blockIdx.x == 0 && lane == 0) ? c_tune.trace + kTriTraceBase : nullptr;
-    for (int b = 0; b < n_blocks; ++b) {
-        const int slot = b % kTriSlots;
+    // ready, row sums done, block done, -, products / accumulation done --
+    // at trace[kTriTraceBase + 8 b]
+    long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0) ? c_tune.trace + kTriTraceBase : nullptr;
+    int b = 0;
+    for (int u = 0; u < n_units; ++u) {
+        const int slot = u % kTriSlots;
         if (tr && b < 1024) tr[8 * b] = clock64();
-        mbar_wait(bar + 8u * slot, (unsigned)(b / kTriSlots) & 1u);
-        if (tr && b < 1024) tr[8 * b + 1] = clock64();
-        const unsigned blk = ring + slot * slot_bytes;
-        int nr, span, row0, next_off, next_bytes, cols_off, vals_off, diag_off;
+        mbar_wait(bar + 8u * slot, (unsigned)(u / kTriSlots) & 1u);
+        const unsigned unit = ring + slot * slot_bytes;
+        int nblk, next_off, next_bytes, upad;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(nr), "=r"(span), "=r"(row0), "=r"(next_off)
-                     : "r"(blk));
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(next_bytes), "=r"(cols_off), "=r"(vals_off), "=r"(diag_off)
-                     : "r"(blk + 16));
-        (void)row0;
-        // block b + kTriSlots - 1 refills the slot the warp left after block b - 1
+                     : "=r"(nblk), "=r"(next_off), "=r"(next_bytes), "=r"(upad)
+                     : "r"(unit));
+        (void)upad;
+        // unit u + kTriSlots - 1 refills the slot the warp left after unit u - 1
         if (lane == 0 && next_bytes > 0) {
-            const int ns = (b + kTriSlots - 1) % kTriSlots;
+            const int ns = (u + kTriSlots - 1) % kTriSlots;
             bulk_fetch(ring + ns * slot_bytes, stream + (size_t)next_off * 16, next_bytes, bar + 8u * ns);
         }
-        if (tr && b < 1024) tr[8 * b + 4] = clock64();
-        const unsigned cols = blk + cols_off, vals = blk + vals_off;
-        double s = 0.0;
-        if (exact) {
-            // ---- exact: the reference's rounding sequence
-            int i = 0;
-            double dg = 1.0, rd = 1.0;
-            if (lane < nr) {  // row data first: its latency overlaps phase 1
-                i = lds_s32(blk + 32u + 4u * lane);
-                s = ZSM ? lds_f64(zs + 8u * i) : zg[i];
-                if (UPPER) {
-                    const unsigned dp = blk + diag_off + 8u * lane;
-                    dg = lds_f64(dp);
-                    rd = lds_f64(dp + 8u * nr);
-                }
+        unsigned blk = unit + 16u;
+        for (int kb = 0; kb < nblk; ++kb, ++b) {
+            if (tr && b < 1024) {
+                if (kb) tr[8 * b] = clock64();
+                tr[8 * b + 1] = clock64();
             }
-            // phase 1: all lanes form the block's products into shared scratch
-            const int items = nr * span;
-            for (int t0 = 0; t0 < items; t0 += 128) {
-                int j[4];
-                double v[4], zj[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int t = min(t0 + q * 32 + lane, items - 1);
-                    j[q] = lds_s32(cols + 4u * t);
-                    v[q] = lds_f64(vals + 8u * t);
+            int nr, per, lg, bytes, cols_off, vals_off, diag_off, bpad;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(nr), "=r"(per), "=r"(lg), "=r"(bytes)
+                         : "r"(blk));
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(cols_off), "=r"(vals_off), "=r"(diag_off), "=r"(bpad)
+                         : "r"(blk + 16));
+            (void)bpad;
+            const unsigned cols = blk + cols_off, vals = blk + vals_off;
+            double s = 0.0;
+            if constexpr (EXACT) {
+                const int span = per;
+                int i = 0;
+                double dg = 1.0, rd = 1.0;
+                if (lane < nr) {  // row data first: its latency overlaps phase 1
+                    i = lds_s32(blk + 32u + 4u * lane);
+                    s = ZSM ? lds_f64(rs + 8u * i) : rg[i];
+                    if (UPPER) {
+                        const unsigned dp = blk + diag_off + 8u * lane;
+                        dg = lds_f64(dp);
+                        rd = lds_f64(dp + 8u * nr);
+                    }
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int t = t0 + q * 32 + lane;
-                    if (t < items)
-                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(prod + 8u * t), "d"(v[q] * zj[q]) : "memory");
-                }
-            }
-            __syncwarp();
-            if (tr && b < 1024) tr[8 * b + 2] = clock64();
-            // phase 2: lane l subtracts row l's products in CSR order
-            if (lane < nr) {
-                const unsigned pp = prod + 8u * lane, st = 8u * nr;
-                int e = 0;
-                for (; e + 8 <= span; e += 8) {
-                    double pq[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) pq[q] = lds_f64(pp + (e + q) * st);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) s = s - pq[q];
-                }
-                for (; e < span; e += 2) {  // span is even
-                    const double p0 = lds_f64(pp + e * st), p1 = lds_f64(pp + (e + 1) * st);
-                    s = s - p0;
-                    s = s - p1;
-                }
-                if (UPPER) s = div_rn(s, dg, rd);
-                if (ZSM)
-                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
-                else
-                    zg[i] = s;
-            }
-        } else {
-            // ---- fast: G = 32 / pow2ceil(nr) lanes per row; lane k of a row
-            // sums entries k, k + G, .. with four accumulators, then a
-            // butterfly over the G lanes completes the row sum (reassociated:
-            // within the solver tolerance, not bit-identical)
-            const int lg = nr > 16 ? 0 : nr > 8 ? 1 : nr > 4 ? 2 : nr > 2 ? 3 : nr > 1 ? 4 : 5;
-            const int G = 1 << lg;
-            const int r = lane >> lg, k = lane & (G - 1);
-            const bool act = r < nr;
-            int i = 0;
-            double dg = 1.0, rd = 1.0, z0 = 0.0;
-            if (act && k == 0) {
-                i = lds_s32(blk + 32u + 4u * r);
-                z0 = ZSM ? lds_f64(zs + 8u * i) : zg[i];
-                if (UPPER) {
-                    const unsigned dp = blk + diag_off + 8u * r;
-                    dg = lds_f64(dp);
-                    rd = lds_f64(dp + 8u * nr);
-                }
-            }
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            if (act) {
-                const unsigned ce = cols + 4u * r, ve = vals + 8u * r;
-                const unsigned cstep = 4u * nr * G, vstep = 8u * nr * G;
-                unsigned co = ce + 4u * nr * k, vo = ve + 8u * nr * k;
-                for (int e = k; e < span; e += 4 * G) {
+                // phase 1: all lanes form the block's products into shared scratch
+                const int items = nr * span;
+                for (int t0 = 0; t0 < items; t0 += 128) {
                     int j[4];
                     double v[4], zj[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const bool ok = e + q * G < span;
-                        j[q] = ok ? lds_s32(co + q * cstep) : T.n;  // dummy slot z[n] = +0.0
-                        v[q] = ok ? lds_f64(vo + q * vstep) : 0.0;
+                        const int t = min(t0 + q * 32 + lane, items - 1);
+                        j[q] = lds_s32(cols + 4u * t);
+                        v[q] = lds_f64(vals + 8u * t);
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[q] = acc[q] + v[q] * zj[q];
-                    co += 4 * cstep;
-                    vo += 4 * vstep;
+                    for (int q = 0; q < 4; ++q) {
+                        const int t = t0 + q * 32 + lane;
+                        if (t < items)
+                            asm volatile("st.shared.f64 [%0], %1;" ::"r"(prod + 8u * t), "d"(v[q] * zj[q]) : "memory");
+                    }
+                }
+                __syncwarp();
+                if (tr && b < 1024) tr[8 * b + 5] = clock64();
+                // phase 2: lane l subtracts row l's products in CSR order
+                if (lane < nr) {
+                    const unsigned pp = prod + 8u * lane, st = 8u * nr;
+                    int e = 0;
+                    for (; e + 8 <= span; e += 8) {
+                        double pq[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) pq[q] = lds_f64(pp + (e + q) * st);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) s = s - pq[q];
+                    }
+                    for (; e < span; e += 2) {  // span is even
+                        const double p0 = lds_f64(pp + e * st), p1 = lds_f64(pp + (e + 1) * st);
+                        s = s - p0;
+                        s = s - p1;
+                    }
+                    if (UPPER) s = div_rn(s, dg, rd);
+                    if (ZSM)
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
+                    else
+                        zg[i] = s;
+                }
+                if (tr && b < 1024) tr[8 * b + 2] = clock64();
+            } else {
+                const int m = per, G = 1 << lg;
+                // per-lane tables: the row index on a row's first lane (-1
+                // elsewhere) and its reciprocal diagonal
+                const int i = lds_s32(blk + 32u + 4u * lane);
+                const bool head = i >= 0;
+                double rd = 1.0, z0 = 0.0;
+                if (head) {
+                    z0 = ZSM ? lds_f64(rs + 8u * i) : rg[i];
+                    if (UPPER) rd = lds_f64(blk + diag_off + 8u * lane);
+                }
+                // slice sums: slot q of every lane is one conflict-free load
+                // (entry-major layout), in batches of 8 slots
+                double t = 0.0;
+                {
+                    const unsigned cp = cols + 4u * lane, vp = vals + 8u * lane;
+                    double a0 = 0.0, a1 = 0.0;
+                    for (int q0 = 0; q0 < m; q0 += 8) {
+                        int j[8];
+                        double v[8], zj[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const bool ok = q0 + q < m;
+                            j[q] = ok ? lds_s32(cp + 128u * (q0 + q)) : T.n;
+                            v[q] = ok ? lds_f64(vp + 256u * (q0 + q)) : 0.0;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
+                        double pr[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
+                        a0 = a0 + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+                        a1 = a1 + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+                    }
+                    t = a0 + a1;  // idle lanes hold zero slots
+                }
+                if (tr && b < 1024) tr[8 * b + 5] = clock64() + (long long)(t == 12345.678);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)  // uniform predicate: straight-line butterfly
+                    if (o < G) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+                if (tr && b < 1024) tr[8 * b + 2] = clock64();
+                if (head) {
+                    s = z0 - t;
+                    if (UPPER) s = s * rd;  // reassociated mode: within one ulp of the quotient
+                    if (ZSM)
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
+                    else
+                        zg[i] = s;
                 }
             }
-            double t = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-            if (tr && b < 1024) tr[8 * b + 5] = clock64() + (long long)(t == 12345.678);
-            for (int o = G >> 1; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
-            if (tr && b < 1024) tr[8 * b + 2] = clock64();
-            if (act && k == 0) {
-                s = z0 - t;
-                if (UPPER) s = div_rn(s, dg, rd);
-                if (ZSM)
-                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
-                else
-                    zg[i] = s;
-            }
+            __syncwarp();
+            if (tr && b < 1024) tr[8 * b + 3] = clock64() + (long long)(s == 12345.678);
+            blk += bytes;
         }
-        __syncwarp();
-        if (tr && b < 1024) tr[8 * b + 3] = clock64() + (long long)(s == 12345.678);
     }
+}
+
+template <bool UPPER, bool ZSM>
+__device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
+                                               int ring_off, int slot_bytes, int prod_off, unsigned bar, bool exact) {
+    if (exact)
+        tri_solve_warp_t<UPPER, ZSM, true>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
+    else
+        tri_solve_warp_t<UPPER, ZSM, false>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
 }
 
 // Both substitutions of one ILUT application; warp 0 solves, the CTA joins at
@@ -605,11 +517,13 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
         }
         __syncwarp();
         if (z_off >= 0) {
-            tri_solve_warp<false, true>(L, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
-            tri_solve_warp<true, true>(U, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots, exact);
+            tri_solve_warp<false, true>(L, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
+            tri_solve_warp<true, true>(U, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots,
+                                       exact);
         } else {
-            tri_solve_warp<false, false>(L, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
-            tri_solve_warp<true, false>(U, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots, exact);
+            tri_solve_warp<false, false>(L, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
+            tri_solve_warp<true, false>(U, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots,
+                                        exact);
         }
     }
     __syncthreads();
@@ -620,6 +534,39 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
         for (int i = threadIdx.x; i < L.n; i += NT) xadd[i] = xadd[i] + z[i];
         __syncthreads();
     }
+}
+
+// Lexicographic Gauss-Seidel sweeps (solvers.hpp:80-99) of an order-1
+// h-level, in place on x: the sweep is a level-scheduled "triangular" solve
+// (TriStream built by plan_gauss_seidel): the levels are the anti-diagonal
+// wavefronts u + 2v = t (mirrored backward), every row sums its eight
+// off-diagonal entries against the current x -- updated values from earlier
+// wavefronts, old ones from later wavefronts, exactly as the sequential sweep
+// sees them -- and divides by its diagonal.  Warp 0 runs `count` sweeps; the
+// CTA joins at the closing barrier.
+__device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, double* x, bool backward, int count,
+                                          bool exact, int x_off, int b_off, int ring_off, int slot_bytes,
+                                          int prod_off) {
+    __shared__ unsigned long long gbar[kTriSlots];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const unsigned bar = sh_addr(gbar);
+        const DevTri& T = backward ? lv.gs_bwd : lv.gs_fwd;
+        for (int c = 0; c < count; ++c) {
+            if (threadIdx.x == 0) {
+                for (int k = 0; k < kTriSlots; ++k) mbar_init(bar + 8u * k);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncwarp();
+            if (x_off >= 0 && b_off >= 0)
+                tri_solve_warp<true, true>(T, x, x_off, b, b_off, ring_off, slot_bytes, prod_off, bar, exact);
+            else
+                tri_solve_warp<true, false>(T, x, -1, b, -1, ring_off, slot_bytes, prod_off, bar, exact);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
 }
 
 // Index-ordered dot product (sparse.hpp:188-192): products in parallel into
@@ -711,6 +658,11 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
     int phase[kMaxH];
     int l = 0;
     phase[0] = 0;
+    // neutral slots x[n] of the padded sweep entries (the vectors overlay the
+    // smoother's shared memory)
+    if (threadIdx.x == 0)
+        for (int k = 0; k < H.n_h; ++k) w.hx[k][H.h[k].n] = 0.0;
+    __syncthreads();
     for (;;) {
         if (l + 1 == H.n_h) {
             coarse_solve(H, w.hb[l], w.hx[l]);
@@ -721,8 +673,9 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         const DevHLevel& lv = H.h[l];
         double* b = w.hb[l];
         double* x = w.hx[l];
+        const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + lv.n : -1;
         if (phase[l] == 0) {
-            gs_sweeps(lv, b, x, false, H.gs_pre, H.exact != 0);
+            gs_sweeps(lv, b, x, false, H.gs_pre, H.exact != 0, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
             stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b, H.exact != 0);
             __syncthreads();
             csr_apply<false>(lv.embed_t, w.hr[l], w.hb[l + 1]);  // rc = E^T r
@@ -736,7 +689,7 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         } else {
             csr_apply<true>(lv.embed, w.hx[l + 1], x);  // x += E ec
             __syncthreads();
-            gs_sweeps(lv, b, x, true, H.gs_post, H.exact != 0);
+            gs_sweeps(lv, b, x, true, H.gs_post, H.exact != 0, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
             if (l == 0) break;
             --l;
         }
@@ -981,7 +934,10 @@ __global__ void __launch_bounds__(NT, 1)
         cta_copy(w.hb[arg], in, lv.n);
         cta_copy(w.hx[arg], out, lv.n);
         __syncthreads();
-        gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, H.exact != 0);
+        if (threadIdx.x == 0) w.hx[arg][lv.n] = 0.0;  // neutral slot of padded sweep entries
+        __syncthreads();
+        const int bo = w.lvl_off[arg], xo = bo >= 0 ? bo + lv.n : -1;
+        gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, H.exact != 0, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
         cta_copy(out, w.hx[arg], lv.n);
     }
 }

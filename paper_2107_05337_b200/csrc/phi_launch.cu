@@ -68,42 +68,48 @@ __global__ void copy_kernel(double* dst, const double* src, size_t n) {
 // ---------------------------------------------------------------------------
 size_t phi_ws_doubles(const DevHier& H) {
     size_t s = 6 * ((size_t)H.n_p + 2);
-    for (int l = 0; l < H.n_h; ++l) s += 4 * (size_t)H.h[l].n;
+    for (int l = 0; l < H.n_h; ++l) s += 3 * (size_t)H.h[l].n + 1;
     return (s + 31) & ~size_t(31);
 }
 
 SmemPlan phi_smem_plan(const DevHier& H) {
-    // The three users of shared memory are live in disjoint phases of a
-    // V-cycle, so they overlay one another from offset 0:
-    //   smoothing  : triangular-factor rings + dependency array z
-    //   W-cycle    : the order-1 h-level vectors (restrict .. prolong)
-    //   norms      : the ordered-dot scratch
+    // Shared memory of one Phi CTA, by V-cycle phase:
+    //   [0, tri)        TMA ring of the level-scheduled sweeps (ILUT factors
+    //                   and Gauss-Seidel) + the exact mode's product scratch;
+    //                   the ordered-dot scratch overlays it (norm phases)
+    //   [tri, total)    the ILUT dependency vector z (smoothing) overlaid by
+    //                   the order-1 h-level vectors b, x, r (W-cycle)
     SmemPlan P{};
     const size_t budget = kPhiSmemBudgetBytes / 8;  // doubles
     P.ring_off = 0;
     P.dot_off = 0;
-    P.slot_bytes = (std::max(H.L.max_block_bytes, H.U.max_block_bytes) + 127) / 128 * 128;
+    int slot = std::max(H.L.max_unit_bytes, H.U.max_unit_bytes);
+    for (int l = 0; l + 1 < H.n_h; ++l)
+        slot = std::max(slot, std::max(H.h[l].gs_fwd.max_unit_bytes, H.h[l].gs_bwd.max_unit_bytes));
+    P.slot_bytes = (slot + 127) / 128 * 128;
     size_t tri = (size_t)kTriSlots * P.slot_bytes / 8;
     P.prod_off = (int)tri;
     tri += kTriMaxItems;
     if (tri * 8 > kPhiSmemBudgetBytes) throw InvalidArgument("triangular-factor blocks exceed shared memory");
+    size_t top = tri;
     if (tri + (size_t)H.n_p + 2 <= budget) {
         P.z_off = (int)tri;
-        tri += H.n_p + 2;
+        top = std::max(top, tri + H.n_p + 2);
     } else {
         P.z_off = -1;
     }
     for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
     // coarsest levels first: they are visited most often by the W-cycle
-    size_t lv = 0;
+    size_t lv = tri;
     for (int l = H.n_h - 1; l >= 0; --l) {
-        const size_t need = 4 * (size_t)H.h[l].n;
+        const size_t need = 3 * (size_t)H.h[l].n + 1;
         if (lv + need <= budget) {
             P.lvl_off[l] = (int)lv;
             lv += need;
         }
     }
-    P.total = (int)std::max(std::max(tri, lv), (size_t)kDotChunk);
+    top = std::max(top, lv);
+    P.total = (int)std::max(top, (size_t)kDotChunk);
     if (std::getenv("PHI_PLAN_DEBUG"))
         std::fprintf(stderr, "smem plan: slot %d B x %d, prod @%d, z @%d, levels @%d.., total %d doubles\n",
                      P.slot_bytes, kTriSlots, P.prod_off, P.z_off, P.lvl_off[0], P.total);

@@ -356,39 +356,49 @@ DenseLUHost dense_lu_factor(const HostCsr& a) {
 
 namespace {
 
-TriPlan make_plan(const HostCsr& m, bool upper) {
+// Row view of a level-scheduled sweep: row i's dependency columns, its
+// summed entries (columns ascending = the reference's order) and, for a
+// dividing sweep, its diagonal.
+struct SweepRows {
+    std::function<void(int, std::vector<int>&)> deps;
+    std::function<void(int, std::vector<int>&, std::vector<double>&)> entries;
+    std::function<double(int)> diag;  // empty: unit diagonal
+};
+
+TriPlan make_plan(int n, bool descending, const SweepRows& rv) {
     TriPlan p;
-    const int n = m.n_rows;
     p.n = n;
-    std::vector<int> level(n, 0);
+    std::vector<int> level(n, 0), dep;
     int max_level = -1;
     auto row_level = [&](int i) {
         int lv = 0;
-        const int b = m.row_offsets[i] + (upper ? 1 : 0);
-        for (int e = b; e < m.row_offsets[i + 1]; ++e) lv = std::max(lv, level[m.col_indices[e]] + 1);
+        rv.deps(i, dep);
+        for (int j : dep) lv = std::max(lv, level[j] + 1);
         level[i] = lv;
         max_level = std::max(max_level, lv);
     };
-    if (upper)
+    if (descending)
         for (int i = n - 1; i >= 0; --i) row_level(i);
     else
         for (int i = 0; i < n; ++i) row_level(i);
     p.n_levels = max_level + 1;
     // bucket rows by level; within a level keep solve order
     std::vector<std::vector<int>> by_level(p.n_levels);
-    if (upper)
+    if (descending)
         for (int i = n - 1; i >= 0; --i) by_level[level[i]].push_back(i);
     else
         for (int i = 0; i < n; ++i) by_level[level[i]].push_back(i);
+    std::vector<std::vector<int>> rc(n);
+    std::vector<std::vector<double>> rvv(n);
+    for (int i = 0; i < n; ++i) rv.entries(i, rc[i], rvv[i]);
     p.level_chunk.push_back(0);
     for (int lv = 0; lv < p.n_levels; ++lv) {
         const auto& rs = by_level[lv];
-        auto row_len = [&](int i) { return m.row_offsets[i + 1] - m.row_offsets[i] - (upper ? 1 : 0); };
         for (size_t c0 = 0; c0 < rs.size();) {
             // widest chunk within kTriRows rows and kTriBlockCap bytes
             int nr = 0, maxlen = 0;
             while (c0 + nr < rs.size() && nr < kTriRows) {
-                const int ml = std::max(maxlen, row_len(rs[c0 + nr]));
+                const int ml = std::max(maxlen, static_cast<int>(rc[rs[c0 + nr]].size()));
                 const int sp = std::max(2, (ml + 1) / 2 * 2);
                 if (nr > 0 && 12 * (nr + 1) * sp + 20 * (nr + 1) + 64 > kTriBlockCap) break;
                 maxlen = ml;
@@ -404,14 +414,13 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
             p.vals.resize(base + static_cast<size_t>(span) * nr, 0.0);
             for (int l = 0; l < nr; ++l) {
                 const int i = rs[c0 + l];
-                const int b = m.row_offsets[i] + (upper ? 1 : 0);
-                const int len = m.row_offsets[i + 1] - b;
+                const int len = static_cast<int>(rc[i].size());
                 p.rows.push_back(i);
                 p.lens.push_back(len);
                 p.max_row_len = std::max(p.max_row_len, len);
                 for (int e = 0; e < len; ++e) {
-                    p.cols[base + static_cast<size_t>(e) * nr + l] = m.col_indices[b + e];
-                    p.vals[base + static_cast<size_t>(e) * nr + l] = m.values[b + e];
+                    p.cols[base + static_cast<size_t>(e) * nr + l] = rc[i][e];
+                    p.vals[base + static_cast<size_t>(e) * nr + l] = rvv[i][e];
                 }
             }
             c0 += nr;
@@ -419,81 +428,198 @@ TriPlan make_plan(const HostCsr& m, bool upper) {
         p.level_chunk.push_back(static_cast<int>(p.chunk_meta.size() / 4));
     }
     p.n_chunks = static_cast<int>(p.chunk_meta.size() / 4);
-    if (upper) {
+    if (rv.diag) {
         p.diag.resize(n);
-        for (int i = 0; i < n; ++i) p.diag[i] = m.values[m.row_offsets[i]];
+        for (int i = 0; i < n; ++i) p.diag[i] = rv.diag(i);
     }
     return p;
 }
 
+// triangular factor rows: every stored entry is summed and is a dependency;
+// the upper factor's diagonal (first entry of each row) divides
+SweepRows factor_rows(const HostCsr& m, bool upper) {
+    SweepRows rv;
+    const int skip = upper ? 1 : 0;
+    rv.deps = [&m, skip](int i, std::vector<int>& d) {
+        d.assign(m.col_indices.begin() + m.row_offsets[i] + skip, m.col_indices.begin() + m.row_offsets[i + 1]);
+    };
+    rv.entries = [&m, skip](int i, std::vector<int>& c, std::vector<double>& v) {
+        c.assign(m.col_indices.begin() + m.row_offsets[i] + skip, m.col_indices.begin() + m.row_offsets[i + 1]);
+        v.assign(m.values.begin() + m.row_offsets[i] + skip, m.values.begin() + m.row_offsets[i + 1]);
+    };
+    if (upper) rv.diag = [&m](int i) { return m.values[m.row_offsets[i]]; };
+    return rv;
+}
+
 }  // namespace
 
-TriPlan plan_lower(const HostCsr& lower) { return make_plan(lower, false); }
-TriPlan plan_upper(const HostCsr& upper) { return make_plan(upper, true); }
+TriPlan plan_lower(const HostCsr& lower) { return make_plan(lower.n_rows, false, factor_rows(lower, false)); }
+TriPlan plan_upper(const HostCsr& upper) { return make_plan(upper.n_rows, true, factor_rows(upper, true)); }
 
-TriStream make_tri_stream(const TriPlan& p) {
-    struct Blk {
-        int chunk, nr, span, bytes, diag_off, cols_off, vals_off;
+TriPlan plan_gauss_seidel(const HostCsr& a, bool backward) {
+    // gauss_seidel_sweep (solvers.hpp:80-99): row i sums every off-diagonal
+    // entry in CSR order and divides by its diagonal; it must follow the rows
+    // it reads updated (j < i forward, j > i backward).  For a symmetric
+    // pattern these levels are the anti-diagonal wavefronts, and every row
+    // that row i reads in its old state lies on a later level.
+    SweepRows rv;
+    rv.deps = [&a, backward](int i, std::vector<int>& d) {
+        d.clear();
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) {
+            const int j = a.col_indices[e];
+            if (backward ? j > i : j < i) d.push_back(j);
+        }
     };
+    rv.entries = [&a](int i, std::vector<int>& c, std::vector<double>& v) {
+        c.clear();
+        v.clear();
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e)
+            if (a.col_indices[e] != i) {
+                c.push_back(a.col_indices[e]);
+                v.push_back(a.values[e]);
+            }
+    };
+    rv.diag = [&a](int i) {
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e)
+            if (a.col_indices[e] == i) return a.values[e];
+        throw std::runtime_error("gauss_seidel_sweep: zero diagonal entry");
+    };
+    return make_plan(a.n_rows, backward, rv);
+}
+
+TriStream make_tri_stream(const TriPlan& p, bool fast) {
     const bool upper = !p.diag.empty();
-    std::vector<Blk> blocks;
+    // ---- block images
+    std::vector<std::vector<unsigned char>> blocks;
     for (int c = 0; c < p.n_chunks; ++c) {
-        Blk k{};
-        k.chunk = c;
-        k.nr = p.chunk_meta[4 * c + 1];
-        k.span = p.chunk_meta[4 * c + 3];
-        k.diag_off = 32 + (4 * k.nr + 7) / 8 * 8;
-        k.cols_off = k.diag_off + (upper ? 16 * k.nr : 0);
-        k.vals_off = k.cols_off + 4 * k.nr * k.span;  // nr * span even: 8-byte aligned
-        k.bytes = (k.vals_off + 8 * k.nr * k.span + 15) / 16 * 16;
-        if (k.nr * k.span > kTriMaxItems)
-            throw InvalidArgument("ILUT factor row longer than the triangular-solve block capacity");
-        blocks.push_back(k);
+        const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
+        const int span = p.chunk_meta[4 * c + 3];
+        int lg = 0, m = span;
+        if (fast) {
+            // lanes per row: minimise the batches of 8 entries per lane plus the
+            // pairwise reduction of the G slice sums
+            int maxlen = 0;
+            for (int l = 0; l < nr; ++l) maxlen = std::max(maxlen, p.lens[row0 + l]);
+            double best = 1e30;
+            for (int g = 0; (nr << g) <= 32; ++g) {
+                const int mm = std::max(1, (maxlen + (1 << g) - 1) >> g);
+                // measured (tools/block_probe.cu): ~100 cycles per batch of 8
+                // slots, ~45 per butterfly round
+                const double cost = 100.0 * ((mm + 7) / 8) + 45.0 * g;
+                if (cost < best) {
+                    best = cost;
+                    lg = g;
+                    m = mm;
+                }
+            }
+        }
+        // fast: entry-major over a full warp (slot q of lane L at q * 32 + L),
+        // so that one load instruction reads one slot of every lane
+        // conflict-free; exact: entry e of row l at e * nr + l
+        const int lanes = fast ? 32 : nr;
+        const int per = fast ? m : span;  // entries per lane (fast) / per row (exact)
+        // exact: rows int32[nr] at 32, diag + rdiag double[nr] each at diag_off;
+        // fast: per-lane tables at 32: row index of the row's first lane
+        // (-1 elsewhere) int32[32], and at diag_off its reciprocal diagonal
+        // double[32]
+        const int rows_n = fast ? 32 : nr;
+        const int diag_off = 32 + (4 * rows_n + 7) / 8 * 8;
+        const int cols_off = diag_off + (upper ? (fast ? 8 * 32 : 16 * nr) : 0);
+        const int vals_off = (cols_off + 4 * lanes * per + 15) / 16 * 16;
+        const int bytes = (vals_off + 8 * lanes * per + 15) / 16 * 16;
+        if (bytes + 16 > kTriUnitCap || (!fast && nr * span > kTriMaxItems))
+            throw InvalidArgument("ILUT factor level slice exceeds the triangular-solve block capacity");
+        std::vector<unsigned char> img(bytes, 0);
+        const int hdr[8] = {nr, per, lg, bytes, cols_off, vals_off, diag_off, 0};
+        std::memcpy(img.data(), hdr, sizeof hdr);
+        int* rws = reinterpret_cast<int*>(img.data() + 32);
+        double* dg = reinterpret_cast<double*>(img.data() + diag_off);
+        if (fast) {
+            for (int L = 0; L < 32; ++L) rws[L] = -1;
+            for (int l = 0; l < nr; ++l) {
+                const int i = p.rows[row0 + l];
+                rws[l << lg] = i;
+                if (upper) dg[l << lg] = 1.0 / p.diag[i];  // IEEE round-to-nearest reciprocal
+            }
+        } else {
+            for (int l = 0; l < nr; ++l) rws[l] = p.rows[row0 + l];
+            if (upper)
+                for (int l = 0; l < nr; ++l) {
+                    const double d = p.diag[p.rows[row0 + l]];
+                    dg[l] = d;
+                    dg[nr + l] = 1.0 / d;  // IEEE round-to-nearest reciprocal
+                }
+        }
+        int* cols = reinterpret_cast<int*>(img.data() + cols_off);
+        double* vals = reinterpret_cast<double*>(img.data() + vals_off);
+        for (int l = 0; l < nr; ++l) {
+            for (int e = 0; e < span; ++e) {  // plan entry e of row l (dummies past its length)
+                const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * nr + l;
+                size_t dst;
+                if (fast) {
+                    const int k = e / m, q = e % m;
+                    if (k >= (1 << lg)) continue;  // beyond the lanes: only dummies live there
+                    dst = static_cast<size_t>(q) * 32 + (l << lg) + k;
+                } else {
+                    dst = static_cast<size_t>(e) * nr + l;
+                }
+                cols[dst] = p.cols[src];
+                vals[dst] = p.vals[src];
+            }
+            if (fast)  // slots past the row's padded span
+                for (int e = span; e < (m << lg); ++e) {
+                    const size_t dst = static_cast<size_t>(e % m) * 32 + (l << lg) + e / m;
+                    cols[dst] = p.n;
+                    vals[dst] = 0.0;
+                }
+        }
+        blocks.push_back(std::move(img));
     }
+    // ---- units
     TriStream ts;
     ts.n_blocks = static_cast<int>(blocks.size());
-    std::vector<size_t> off;
+    std::vector<std::pair<size_t, size_t>> units;  // [first block, end block)
+    {
+        size_t b = 0;
+        while (b < blocks.size()) {
+            size_t e = b, bytes = 16;
+            while (e < blocks.size() && bytes + blocks[e].size() <= static_cast<size_t>(kTriUnitCap))
+                bytes += blocks[e++].size();
+            units.emplace_back(b, e);
+            b = e;
+        }
+    }
+    ts.n_units = static_cast<int>(units.size());
+    std::vector<size_t> uoff, ubytes;
     size_t total = 0;
-    for (const Blk& k : blocks) {
-        off.push_back(total);
-        total += k.bytes;
-        ts.max_block_bytes = std::max(ts.max_block_bytes, k.bytes);
+    for (const auto& u : units) {
+        size_t bytes = 16;
+        for (size_t k = u.first; k < u.second; ++k) bytes += blocks[k].size();
+        uoff.push_back(total);
+        ubytes.push_back(bytes);
+        total += bytes;
+        ts.max_unit_bytes = std::max(ts.max_unit_bytes, static_cast<int>(bytes));
     }
     ts.stream.assign(total + 16, 0);
     ts.prime.assign(2 * (kTriSlots - 1), 0);
-    for (int k = 0; k < kTriSlots - 1 && k < ts.n_blocks; ++k) {
-        ts.prime[2 * k] = static_cast<int>(off[k] / 16);
-        ts.prime[2 * k + 1] = blocks[k].bytes;
+    for (int k = 0; k < kTriSlots - 1 && k < ts.n_units; ++k) {
+        ts.prime[2 * k] = static_cast<int>(uoff[k] / 16);
+        ts.prime[2 * k + 1] = static_cast<int>(ubytes[k]);
     }
-    for (size_t k = 0; k < blocks.size(); ++k) {
-        const Blk& B = blocks[k];
-        const int row0 = p.chunk_meta[4 * B.chunk], base = p.chunk_meta[4 * B.chunk + 2];
-        unsigned char* dst = ts.stream.data() + off[k];
-        int hdr[8] = {B.nr, B.span, row0, 0, 0, B.cols_off, B.vals_off, B.diag_off};
-        const size_t nxt = k + kTriSlots - 1;
-        if (nxt < blocks.size()) {
-            hdr[3] = static_cast<int>(off[nxt] / 16);
-            hdr[4] = blocks[nxt].bytes;
+    for (size_t u = 0; u < units.size(); ++u) {
+        unsigned char* dst = ts.stream.data() + uoff[u];
+        int hdr[4] = {static_cast<int>(units[u].second - units[u].first), 0, 0, 0};
+        const size_t nxt = u + kTriSlots - 1;
+        if (nxt < units.size()) {
+            hdr[1] = static_cast<int>(uoff[nxt] / 16);
+            hdr[2] = static_cast<int>(ubytes[nxt]);
         }
         std::memcpy(dst, hdr, sizeof hdr);
-        int* rws = reinterpret_cast<int*>(dst + 32);
-        for (int l = 0; l < B.nr; ++l) rws[l] = p.rows[row0 + l];
-        if (upper) {
-            double* dg = reinterpret_cast<double*>(dst + B.diag_off);
-            for (int l = 0; l < B.nr; ++l) {
-                const double d = p.diag[p.rows[row0 + l]];
-                dg[l] = d;
-                dg[B.nr + l] = 1.0 / d;  // IEEE round-to-nearest reciprocal
-            }
+        size_t o = 16;
+        for (size_t k = units[u].first; k < units[u].second; ++k) {
+            std::memcpy(dst + o, blocks[k].data(), blocks[k].size());
+            o += blocks[k].size();
         }
-        int* cols = reinterpret_cast<int*>(dst + B.cols_off);
-        double* vals = reinterpret_cast<double*>(dst + B.vals_off);
-        for (int e = 0; e < B.span; ++e)
-            for (int l = 0; l < B.nr; ++l) {
-                const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * B.nr + l;
-                cols[e * B.nr + l] = p.cols[src];
-                vals[e * B.nr + l] = p.vals[src];
-            }
     }
     return ts;
 }

@@ -83,25 +83,39 @@ struct TriPlan {
 };
 TriPlan plan_lower(const HostCsr& lower);
 TriPlan plan_upper(const HostCsr& upper);
+/// Level schedule of a lexicographic Gauss-Seidel sweep (rows: off-diagonal
+/// entries in CSR order, diag = the diagonal; levels = wavefronts).
+TriPlan plan_gauss_seidel(const HostCsr& a, bool backward);
 
-/// Level-ordered block stream for the TMA-fed warp solve.  One block = one
-/// chunk with every entry of its rows, fetched by a single cp.async.bulk:
-///   header (32 B): nr, span, row0, next_off16, next_bytes (block
-///                  b + kTriSlots - 1, 0 if none), cols_off, vals_off, diag_off
-///   rows  int32[nr]          at 32 (padded to 8 bytes)
-///   diag  double[nr]         at diag_off      (upper only)
-///   rdiag double[nr]         at diag_off + 8 nr (upper only; RN(1 / diag))
-///   cols  int32[span * nr]   at cols_off      (entry e of row l at e * nr + l)
-///   vals  double[span * nr]  at vals_off
-/// Blocks are 16-byte aligned; offsets in the header are bytes from the block
-/// start, `next_off16` and `prime` are in 16-byte units of `stream`; `prime`
-/// holds (off16, bytes) of the first kTriSlots - 1 blocks.
+/// Level-ordered stream for the TMA-fed warp solve.  The factor is a sequence
+/// of blocks (one per plan chunk: rows of one level), packed into fetch units
+/// of <= kTriUnitCap bytes; one cp.async.bulk moves one unit into a slot of the
+/// shared-memory ring.
+///   unit header (16 B): n_blocks, next_off16, next_bytes (unit
+///                       u + kTriSlots - 1, 0 if none), pad
+///   block header (32 B): nr, span | m, lg, block_bytes, cols_off, vals_off,
+///                        diag_off, pad
+///   rows  int32[nr]   at 32 (padded to 8 bytes)
+///   diag  double[nr]  at diag_off (upper only), rdiag = RN(1 / diag) after it
+/// Exact layout (the reference's summation order): cols int32[span][nr],
+/// vals double[span][nr], entry e of row l at e * nr + l, rows padded to
+/// `span` (even) with neutral dummies.
+/// Fast layout (reassociated sums): G = 2^lg lanes per row; lane L = r G + k
+/// owns entries [k m, (k + 1) m) of row r, stored entry-major over a full
+/// warp: cols int32[m][32], vals double[m][32] (slot q of lane L at
+/// q * 32 + L), padded with dummies.
+/// Dummies are column n with value +0.0 (the device keeps z[n] = +0.0), so
+/// they are exactly neutral.  Offsets in headers are bytes from the block /
+/// unit start; `next_off16` and `prime` are 16-byte units of `stream`;
+/// `prime` holds (off16, bytes) of the first kTriSlots - 1 units.
+constexpr int kTriUnitCap = 12 * 1024;
 struct TriStream {
     std::vector<unsigned char> stream;
     std::vector<int> prime;  // 2 * (kTriSlots - 1)
-    int n_blocks = 0;
-    int max_block_bytes = 0;
+    int n_blocks = 0;        // blocks (levels / level slices)
+    int n_units = 0;
+    int max_unit_bytes = 0;
 };
-TriStream make_tri_stream(const TriPlan& p);
+TriStream make_tri_stream(const TriPlan& p, bool fast);
 
 }  // namespace phi

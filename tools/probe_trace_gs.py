@@ -22,6 +22,7 @@ g = buf[8 * 1024 * 2:8 * 1024 * 2 + 4096].reshape(1024, 4)
 nz = g[:, 0] > 0
 g = g[nz]
 print("wavefronts", len(g))
-print("start->sum ready", np.median(g[:, 1] - g[:, 0]), " sum->stored", np.median(g[:, 2] - g[:, 1]),
-      " stored->after barrier", np.median(g[:, 3] - g[:, 2]), " barrier->next start", np.median(g[1:, 0] - g[:-1, 3]))
+print("first row", np.median(g[:, 1] - g[:, 0]), " extra rows", np.median(g[:, 2] - g[:, 1]),
+      " syncwarp", np.median(g[:, 3] - g[:, 2]), " -> next start", np.median(g[1:, 0] - g[:-1, 3]),
+      " per wavefront", np.median(g[1:, 0] - g[:-1, 0]))
 print("first rows:", (g[:6] - g[0, 0]).tolist())

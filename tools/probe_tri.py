@@ -26,11 +26,11 @@ for kind in ("unit", "solve"):
     nb = int((t[:, 0] > 0).sum())
     t = t[:nb]
     wait = t[:, 1] - t[:, 0]
-    ph1 = t[:, 2] - t[:, 1]
-    ph2 = t[:, 3] - t[:, 2]
+    acc = t[:, 5] - t[:, 1]
+    red = t[:, 2] - t[:, 5]
+    fin = t[:, 3] - t[:, 2]
     gap = t[1:, 0] - t[:-1, 3]
-    iss = t[:, 4] - t[:, 1]
-    acc = t[:, 5] - t[:, 4]
-    print(f"   issue {np.median(iss):.0f}  accumulate {np.median(acc):.0f}  shuffle {np.median(t[:, 2] - t[:, 5]):.0f}")
-    print(f"{kind}: blocks {nb}  wait {np.median(wait):.0f}/{wait.mean():.0f}  ph1 {np.median(ph1):.0f}/{ph1.mean():.0f}  "
-          f"ph2 {np.median(ph2):.0f}/{ph2.mean():.0f}  gap {np.median(gap):.0f}/{gap.mean():.0f} (median/mean cycles)")
+    tot = t[1:, 0] - t[:-1, 0]
+    med = lambda v: float(np.median(v))
+    print(f"{kind}: blocks {nb}  wait {med(wait):.0f}  accumulate {med(acc):.0f}  reduce {med(red):.0f}  "
+          f"finish {med(fin):.0f}  gap {med(gap):.0f}  per block {med(tot):.0f} / mean {tot.mean():.0f} cycles")
