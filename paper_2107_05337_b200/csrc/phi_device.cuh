@@ -450,14 +450,13 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
                 {
                     const unsigned cp = cols + 4u * lane, vp = vals + 8u * lane;
                     double a0 = 0.0, a1 = 0.0;
-                    for (int q0 = 0; q0 < m; q0 += 8) {
+                    for (int q0 = 0; q0 < m; q0 += 8) {  // m: whole batches of 8 (host-padded)
                         int j[8];
                         double v[8], zj[8];
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            const bool ok = q0 + q < m;
-                            j[q] = ok ? lds_s32(cp + 128u * (q0 + q)) : T.n;
-                            v[q] = ok ? lds_f64(vp + 256u * (q0 + q)) : 0.0;
+                            j[q] = lds_s32(cp + 128u * (q0 + q));
+                            v[q] = lds_f64(vp + 256u * (q0 + q));
                         }
 #pragma unroll
                         for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];

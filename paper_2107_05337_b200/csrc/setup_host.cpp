@@ -502,10 +502,11 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
             for (int l = 0; l < nr; ++l) maxlen = std::max(maxlen, p.lens[row0 + l]);
             double best = 1e30;
             for (int g = 0; (nr << g) <= 32; ++g) {
-                const int mm = std::max(1, (maxlen + (1 << g) - 1) >> g);
-                // measured (tools/block_probe.cu): ~100 cycles per batch of 8
-                // slots, ~45 per butterfly round
-                const double cost = 100.0 * ((mm + 7) / 8) + 45.0 * g;
+                // slots per lane padded to whole batches of 8 (unpredicated
+                // loads); measured (tools/block_probe.cu): ~180 cycles per
+                // batch, ~45 per butterfly round
+                const int mm = (std::max(1, (maxlen + (1 << g) - 1) >> g) + 7) / 8 * 8;
+                const double cost = 180.0 * (mm / 8) + 45.0 * g;
                 if (cost < best) {
                     best = cost;
                     lg = g;

@@ -19,22 +19,20 @@ __device__ __forceinline__ int lds_s32(unsigned a) {
 template <int MODE>
 __global__ void blocks(long long* cyc, int nr, int lg, int m, int nblk, int n) {
     extern __shared__ __align__(16) unsigned char sm[];
-    double* z = reinterpret_cast<double*>(sm + 16384);
+    double* z = reinterpret_cast<double*>(sm + 32768);
     int* rows = reinterpret_cast<int*>(sm);
     int* cols = reinterpret_cast<int*>(sm + 256);
-    double* vals = reinterpret_cast<double*>(sm + 4096);
+    double* vals = reinterpret_cast<double*>(sm + 8192);
     const int G = 1 << lg;
     for (int i = threadIdx.x; i < n + 1; i += blockDim.x) z[i] = 1e-3 * (i % 13);
-    for (int i = threadIdx.x; i < nr * G * m; i += blockDim.x) {
-        cols[i] = (i * 37) % n;
-        vals[i] = 1e-2 * (i % 7);
-    }
+    for (int i = threadIdx.x; i < 32 * 60; i += blockDim.x) cols[i] = (i * 37) % n;
+    for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) vals[i] = 1e-2 * (i % 7);
     for (int i = threadIdx.x; i < nr; i += blockDim.x) rows[i] = (i * 101) % n;
     __syncthreads();
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     const unsigned base = (unsigned)__cvta_generic_to_shared(sm);
-    const unsigned zs = base + 16384, cb = base + 256, vb = base + 4096;
+    const unsigned zs = base + 32768, cb = base + 256, vb = base + 8192;
     long long t0 = clock64();
     for (int b = 0; b < nblk; ++b) {
         const int r = lane >> lg;
@@ -120,12 +118,38 @@ __global__ void blocks(long long* cyc, int nr, int lg, int m, int nblk, int n) {
                 for (int q = 0; q < 8; ++q) p[q] = v[q] * zj[q];
                 t = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
             }
+        } else if (MODE == 5 || MODE == 6) {  // entry-major, runtime m in batches of 8 (engine fast path)
+            double a0 = 0.0, a1 = 0.0;
+            for (int q0 = 0; q0 < m; q0 += 8) {
+                int j[8];
+                double v[8], zj[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const bool ok = q0 + q < m;
+                    j[q] = ok ? lds_s32(cb + 128u * (q0 + q) + 4u * lane) : n;
+                    v[q] = ok ? lds_f64(vb + 256u * ((q0 + q) & 7) + 8u * lane) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) zj[q] = lds_f64(zs + 8u * j[q]);
+                double pr[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
+                a0 = a0 + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+                a1 = a1 + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+            }
+            t = a0 + a1;
         } else {  // pure latency reference: one dependent LDS + DADD
             if (act) t = lds_f64(zs + 8u * lane);
         }
         // reduce over G lanes: butterfly (MODE 3) or shared scratch
         if (MODE == 3 || MODE == 4) {
             for (int o = G >> 1; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+        } else if (MODE == 5) {
+            for (int o = G >> 1; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+        } else if (MODE == 6) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                if (o < G) t = t + __shfl_xor_sync(0xffffffffu, t, o);
         } else if (G > 1) {
             double* scr = reinterpret_cast<double*>(sm + 14336);
             scr[lane] = t;
@@ -152,16 +176,20 @@ int main() {
     cudaFuncSetAttribute(blocks<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(blocks<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(blocks<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    int cfg[][3] = {{4, 3, 6}, {4, 0, 48}, {4, 2, 12}, {32, 0, 8}};
+    cudaFuncSetAttribute(blocks<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(blocks<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    int cfg[][3] = {{4, 3, 6}, {4, 0, 48}, {4, 2, 12}, {4, 1, 24}, {32, 0, 8}, {1, 5, 2}};
     for (auto& c : cfg) {
         blocks<0><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], c[2], 2000, n);
         blocks<1><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], 8, 2000, n);
         blocks<2><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], c[2], 2000, n);
         blocks<3><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], 8, 2000, n);
         blocks<4><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], 8, 2000, n);
+        blocks<5><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], c[2], 2000, n);
+        blocks<6><<<1, 256, 64 * 1024>>>(cyc, c[0], c[1], c[2], 2000, n);
         cudaDeviceSynchronize();
-        printf("nr=%d lg=%d m=%d: engine-shape %lld  fixed8 %lld  fixed8+shfl %lld  entry-major8+shfl %lld  latency-floor %lld (%s)\n",
-               c[0], c[1], c[2], cyc[0], cyc[1], cyc[3], cyc[4], cyc[2], cudaGetErrorString(cudaGetLastError()));
+        printf("nr=%d lg=%d m=%d: engine-shape %lld  fixed8 %lld  fixed8+shfl %lld  entry-major8+shfl %lld  em-runtime-m %lld / unrolled-bfly %lld  floor %lld (%s)\n",
+               c[0], c[1], c[2], cyc[0], cyc[1], cyc[3], cyc[4], cyc[5], cyc[6], cyc[2], cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
 }
