@@ -168,6 +168,27 @@ int phi_mgrit_initial(const phi_mgrit* g, double* out);
 int phi_mgrit_initialize(phi_mgrit* g, double* g_norm);
 int phi_mgrit_cycle(phi_mgrit* g, int level);
 int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out);
+/* ---- time-sharded multi-GPU support (paper_2107_05337_b200/timeshard.py,
+ * DESIGN.md section 6): one rank per GPU owns the coarse intervals
+ * [j_lo, j_hi) of level 0; coarser levels are replicated.  Per-point
+ * reduction terms come back with zeros for points other ranks own, so an
+ * elementwise sum over ranks plus the ordered host sum reproduces the
+ * single-GPU reduction exactly. */
+int phi_mgrit_set_range(phi_mgrit* g, int j_lo, int j_hi); /* j_hi = -1: all */
+int phi_mgrit_initialize_state(phi_mgrit* g);               /* initialize() minus the g-norm */
+/* steps_0 + 1 terms: [0] = |g_0|^2, [k] = squared norms of the load solves (mgrit.hpp:292-310) */
+int phi_mgrit_gnorm_terms(phi_mgrit* g, double* terms);
+/* steps_level + 1 per-point squared residuals (mgrit.hpp:200-214) */
+int phi_mgrit_residual_terms(phi_mgrit* g, int level, double* terms);
+/* op 0 F-relaxation, 1 F+C relaxation, 2 restrict residual to level+1,
+ * 3 inject the coarse correction into the C-points, 4 full cycle from level */
+int phi_mgrit_phase(phi_mgrit* g, int level, int op);
+/* copy `count` consecutive point vectors k0.. of level's u (which 0) or g (1)
+ * to (set 0) or from (set 1) ptr, a host or device pointer */
+int phi_mgrit_points(phi_mgrit* g, int level, int which, int k0, int count, double* ptr, int device_ptr,
+                     int set);
+/* [level-0 solves, level-0 p-MG cycles, coarser solves, coarser cycles] */
+int phi_mgrit_stats(const phi_mgrit* g, long long* out4);
 /* kernel launches issued by the last solve() (bench evidence) */
 long long phi_mgrit_launches(const phi_mgrit* g);
 /* replace the spline coefficients of a PHI_INIT_COEFFS problem (host array,

@@ -552,6 +552,34 @@ int phi_mgrit_residual_norm(phi_mgrit* g, int level, double* out) {
 
 long long phi_mgrit_launches(const phi_mgrit* g) { return g->g->launches; }
 
+int phi_mgrit_set_range(phi_mgrit* g, int j_lo, int j_hi) {
+    return guarded([&] { g->g->set_range(j_lo, j_hi); });
+}
+
+int phi_mgrit_initialize_state(phi_mgrit* g) {
+    return guarded([&] { g->g->initialize_state(); });
+}
+
+int phi_mgrit_gnorm_terms(phi_mgrit* g, double* terms) {
+    return guarded([&] { g->g->gnorm_terms(terms); });
+}
+
+int phi_mgrit_residual_terms(phi_mgrit* g, int level, double* terms) {
+    return guarded([&] { g->g->residual_terms(level, terms); });
+}
+
+int phi_mgrit_phase(phi_mgrit* g, int level, int op) {
+    return guarded([&] { g->g->phase(level, op); });
+}
+
+int phi_mgrit_points(phi_mgrit* g, int level, int which, int k0, int count, double* ptr, int device_ptr, int set) {
+    return guarded([&] { g->g->points(level, which, k0, count, ptr, device_ptr != 0, set != 0); });
+}
+
+int phi_mgrit_stats(const phi_mgrit* g, long long* out4) {
+    return guarded([&] { g->g->stats(out4); });
+}
+
 int phi_mgrit_set_init_coeffs(phi_mgrit* g, const double* coeffs) {
     return guarded([&] { g->g->set_init_coeffs(coeffs); });
 }

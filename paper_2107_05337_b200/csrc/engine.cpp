@@ -308,6 +308,7 @@ Mgrit::Mgrit(std::shared_ptr<const Disc> disc_, const ProblemOptions& ps_, const
     build_loads();
     sq.alloc(levels[0].steps + 1);
     stat.alloc(2);
+    stat_c.alloc(2);
     err.alloc(3);
     err_rel.alloc(1);
     u0.alloc(disc->n_p);
@@ -441,7 +442,7 @@ void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, 
     a.CU = CU;
     a.m = cfg.m;
     a.SQ = sq.get();
-    a.stat = stat.get();
+    a.stat = l == 0 ? stat.get() : stat_c.get();
     a.err = err.get();
     a.err_rel = err_rel.get();
     a.level = l;
@@ -472,25 +473,37 @@ void Mgrit::check_errors() {
 
 // mgrit.hpp:122-141; with FCF the first F sweep also covers the C-point of its
 // interval (same operations in the same order per point).
+int Mgrit::range_hi(int l) const {
+    const int J = levels[l].steps / cfg.m;
+    return (l == 0 && j_hi >= 0) ? std::min(j_hi, J) : J;
+}
+
+// F-relaxation of every interval (mgrit.hpp:122-132); with_c adds the
+// C-relaxation (135-141) as a second wave.  The two must not be fused per
+// interval: interval j + 1 has to start from the C-point u[(j+1) m] as it was
+// BEFORE interval j's C-relaxation updates it, which a fused task only sees
+// while all intervals happen to be resident at once.
 void Mgrit::f_relax(int l, bool with_c) {
     Level& lv = levels[l];
-    const int J = lv.steps / cfg.m;
-    wave(l, kModeStep, kEpiStore, J, lv.kF.get(), with_c ? cfg.m : cfg.m - 1);
+    const int lo = range_lo(l), hi = range_hi(l);
+    wave(l, kModeStep, kEpiStore, hi - lo, lv.kF.get() + lo, cfg.m - 1);
+    if (with_c) c_relax(l);
 }
 
 void Mgrit::c_relax(int l) {
     Level& lv = levels[l];
-    wave(l, kModeStep, kEpiStore, lv.steps / cfg.m, lv.kR.get(), 1);
+    const int lo = range_lo(l), hi = range_hi(l);
+    wave(l, kModeStep, kEpiStore, hi - lo, lv.kR.get() + lo, 1);
 }
 
 void Mgrit::restrict_residual(int l) {
     Level& f = levels[l];
     Level& c = levels[l + 1];
     const int n = disc->n_p;
-    const int J = f.steps / cfg.m;
+    const int lo = range_lo(l), hi = range_hi(l);
     launch_restrict_first(f.g.get(), f.u.get(), c.g.get(), c.u.get(), n, stream);
     ++launches;
-    wave(l, kModeStep, kEpiRestrict, J, f.kR.get(), 1, c.g.get(), c.u.get());
+    wave(l, kModeStep, kEpiRestrict, hi - lo, f.kR.get() + lo, 1, c.g.get(), c.u.get());
 }
 
 void Mgrit::interpolate_and_correct(int l) {
@@ -528,51 +541,86 @@ void Mgrit::cycle_impl(int l, bool f_schedule) {
 void Mgrit::mgrit_cycle(int l) { cycle_impl(l, cfg.cycle == 1); }
 
 double Mgrit::residual_norm(int l) {
-    Level& lv = levels[l];
-    const int n = disc->n_p;
-    launch_resid0(lv.g.get(), lv.u.get(), sq.get(), n, stream);
-    ++launches;
-    wave(l, kModeStep, kEpiResid, lv.steps, lv.kAll.get(), 1);
-    std::vector<double> h(lv.steps + 1);
-    PHI_CUDA(cudaMemcpyAsync(h.data(), sq.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, stream));
-    PHI_CUDA(cudaStreamSynchronize(stream));
-    check_errors();
+    std::vector<double> h(levels[l].steps + 1);
+    residual_terms(l, h.data());
     double total = 0.0;
     for (double s : h) total += s;  // fixed order (mgrit.hpp:211-212)
     return std::sqrt(total);
 }
 
-double Mgrit::compute_g_norm() {
-    Level& lv0 = levels[0];
+void Mgrit::residual_terms(int l, double* host) {
+    Level& lv = levels[l];
     const int n = disc->n_p;
-    std::vector<double> g0(n);
-    PHI_CUDA(cudaMemcpyAsync(g0.data(), lv0.g.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
-    PHI_CUDA(cudaStreamSynchronize(stream));
-    double total = 0.0;
-    for (int i = 0; i < n; ++i) total += g0[i] * g0[i];
-    if (has_loads) {
-        PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (lv0.steps + 1), stream));
-        if (loads_steady) {
-            wave(0, kModeSolve, kEpiNorm, 1, lv0.kAll.get(), 1);
-            double v = 0.0;
-            PHI_CUDA(cudaMemcpyAsync(&v, sq.get() + 1, sizeof(double), cudaMemcpyDeviceToHost, stream));
-            PHI_CUDA(cudaStreamSynchronize(stream));
-            check_errors();
-            total += lv0.steps * v;
-        } else {
-            wave(0, kModeSolve, kEpiNorm, lv0.steps, lv0.kAll.get(), 1);
-            std::vector<double> h(lv0.steps + 1);
-            PHI_CUDA(cudaMemcpyAsync(h.data(), sq.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
-                                     stream));
-            PHI_CUDA(cudaStreamSynchronize(stream));
-            check_errors();
-            for (double s : h) total += s;
-        }
+    const int lo = range_lo(l), hi = range_hi(l);
+    PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (lv.steps + 1), stream));
+    if (lo == 0) {  // point 0 belongs to the first rank
+        launch_resid0(lv.g.get(), lv.u.get(), sq.get(), n, stream);
+        ++launches;
     }
+    const int k_begin = lo * cfg.m + 1;
+    const int k_end = (hi == lv.steps / cfg.m) ? lv.steps : hi * cfg.m;  // the last rank takes any tail
+    if (k_end >= k_begin) wave(l, kModeStep, kEpiResid, k_end - k_begin + 1, lv.kAll.get() + (k_begin - 1), 1);
+    PHI_CUDA(cudaMemcpyAsync(host, sq.get(), sizeof(double) * (lv.steps + 1), cudaMemcpyDeviceToHost, stream));
+    PHI_CUDA(cudaStreamSynchronize(stream));
+    check_errors();
+}
+
+double Mgrit::compute_g_norm() {
+    std::vector<double> h(levels[0].steps + 1);
+    gnorm_terms(h.data());
+    double total = 0.0;
+    for (double s : h) total += s;  // [0] = |g_0|^2 summed in index order, then the points
     return std::sqrt(total);
 }
 
+// g-norm terms (mgrit.hpp:292-310): [0] = |g_0|^2 (index-ordered), [k] =
+// |Phi-solve of load_k|^2 for the transient loads of the owned points (a
+// steady load contributes steps copies of one term, folded into [1]).
+void Mgrit::gnorm_terms(double* host) {
+    Level& lv0 = levels[0];
+    const int n = disc->n_p;
+    const int lo = range_lo(0), hi = range_hi(0);
+    std::vector<double> h(lv0.steps + 1, 0.0);
+    if (lo == 0) {
+        std::vector<double> g0(n);
+        PHI_CUDA(cudaMemcpyAsync(g0.data(), lv0.g.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+        PHI_CUDA(cudaStreamSynchronize(stream));
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += g0[i] * g0[i];
+        h[0] = t;
+    }
+    if (has_loads) {
+        PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (lv0.steps + 1), stream));
+        if (loads_steady) {
+            if (lo == 0) {
+                wave(0, kModeSolve, kEpiNorm, 1, lv0.kAll.get(), 1);
+                double v = 0.0;
+                PHI_CUDA(cudaMemcpyAsync(&v, sq.get() + 1, sizeof(double), cudaMemcpyDeviceToHost, stream));
+                PHI_CUDA(cudaStreamSynchronize(stream));
+                check_errors();
+                h[1] = lv0.steps * v;
+            }
+        } else {
+            const int k_begin = lo * cfg.m + 1;
+            const int k_end = (hi == lv0.steps / cfg.m) ? lv0.steps : hi * cfg.m;
+            if (k_end >= k_begin)
+                wave(0, kModeSolve, kEpiNorm, k_end - k_begin + 1, lv0.kAll.get() + (k_begin - 1), 1);
+            std::vector<double> s(lv0.steps + 1);
+            PHI_CUDA(cudaMemcpyAsync(s.data(), sq.get(), sizeof(double) * s.size(), cudaMemcpyDeviceToHost, stream));
+            PHI_CUDA(cudaStreamSynchronize(stream));
+            check_errors();
+            for (int k = 1; k <= lv0.steps; ++k) h[k] = s[k];
+        }
+    }
+    std::copy(h.begin(), h.end(), host);
+}
+
 void Mgrit::initialize() {
+    initialize_state();
+    g_norm = compute_g_norm();
+}
+
+void Mgrit::initialize_state() {
     const int n = disc->n_p;
     for (auto& lv : levels) {
         lv.u.zero(stream);
@@ -583,9 +631,63 @@ void Mgrit::initialize() {
     launch_copy(levels[0].u.get(), u0.get(), n, stream);
     launches += 2;
     stat.zero(stream);
+    stat_c.zero(stream);
     const std::vector<int> e0{0, INT_MAX, -1};
     err.upload(e0, stream);
-    g_norm = compute_g_norm();
+}
+
+void Mgrit::set_range(int lo, int hi) {
+    const int J = levels[0].steps / cfg.m;
+    if (lo < 0 || (hi >= 0 && (hi < lo || hi > J))) throw InvalidArgument("MGRIT interval range out of bounds");
+    j_lo = lo;
+    j_hi = hi;
+}
+
+void Mgrit::phase(int l, int op) {
+    if (l < 0 || l >= n_levels()) throw InvalidArgument("MGRIT level out of range");
+    switch (op) {
+        case 0: f_relax(l, false); break;
+        case 1: f_relax(l, true); break;
+        case 2:
+            if (l + 1 >= n_levels()) throw InvalidArgument("restriction from the coarsest level");
+            restrict_residual(l);
+            break;
+        case 3: {  // fine.u[j m] += coarse.u[j] for every C-point (mgrit.hpp:172-180)
+            if (l + 1 >= n_levels()) throw InvalidArgument("interpolation to the coarsest level");
+            Level& f = levels[l];
+            Level& c = levels[l + 1];
+            launch_inject(c.u.get(), f.u.get(), disc->n_p, f.steps / cfg.m, cfg.m, stream);
+            ++launches;
+            break;
+        }
+        case 4: cycle_impl(l, cfg.cycle == 1); break;
+        default: throw InvalidArgument("unknown MGRIT phase");
+    }
+    PHI_CUDA(cudaStreamSynchronize(stream));
+    check_errors();
+}
+
+void Mgrit::points(int l, int which, int k0, int count, double* ptr, bool device, bool set) {
+    if (l < 0 || l >= n_levels()) throw InvalidArgument("MGRIT level out of range");
+    Level& lv = levels[l];
+    if (k0 < 0 || count < 0 || k0 + count > lv.steps + 1) throw InvalidArgument("MGRIT point range out of bounds");
+    const size_t n = disc->n_p;
+    double* arr = (which == 0 ? lv.u.get() : lv.g.get()) + (size_t)k0 * n;
+    const size_t bytes = sizeof(double) * n * count;
+    if (set)
+        PHI_CUDA(cudaMemcpyAsync(arr, ptr, bytes, device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
+    else
+        PHI_CUDA(cudaMemcpyAsync(ptr, arr, bytes, device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+    PHI_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Mgrit::stats(long long* out4) const {
+    const auto s0 = stat.download(stream);
+    const auto sc = stat_c.download(stream);
+    out4[0] = (long long)s0[0];
+    out4[1] = (long long)s0[1];
+    out4[2] = (long long)sc[0];
+    out4[3] = (long long)sc[1];
 }
 
 void Mgrit::set_init_coeffs(const double* host) {
@@ -676,9 +778,11 @@ MgritResultHost Mgrit::solve() {
         }
     }
     res.final_relative_residual = res.residual_history.back();
-    const auto st = stat.download(stream);
-    res.total_spatial_solves = (long long)st[0];
-    res.mean_spatial_iterations = st[0] > 0 ? (double)st[1] / (double)st[0] : 0.0;
+    long long st[4];
+    stats(st);
+    const long long solves = st[0] + st[2], iters = st[1] + st[3];
+    res.total_spatial_solves = solves;
+    res.mean_spatial_iterations = solves > 0 ? (double)iters / (double)solves : 0.0;
     return res;
 }
 

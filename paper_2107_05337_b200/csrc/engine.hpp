@@ -164,6 +164,20 @@ public:
     void initialize();
     void mgrit_cycle(int l);
     double residual_norm(int l);
+
+    // ---- time-sharded driver support (one rank per GPU, see timeshard.py):
+    // level 0 works on coarse intervals [j_lo, j_hi) only; coarser levels are
+    // replicated.  Per-point reduction terms are returned with zeros for the
+    // points other ranks own, so an elementwise sum over ranks followed by the
+    // ordered host sum reproduces the single-GPU reduction exactly.
+    int j_lo = 0, j_hi = -1;  // -1: all intervals
+    void set_range(int lo, int hi);
+    void initialize_state();                     // initialize() without the g-norm
+    void gnorm_terms(double* host);              // steps_0 + 1 terms: [0] = |g_0|^2
+    void residual_terms(int l, double* host);    // steps_l + 1 terms
+    void phase(int l, int op);                   // see phi_mgrit_phase
+    void points(int l, int which, int k0, int count, double* ptr, bool device, bool set);
+    void stats(long long* out4) const;           // level-0 solves, iters; coarser solves, iters
     int n_levels() const { return (int)levels.size(); }
 
     struct Level {
@@ -183,7 +197,8 @@ public:
     DevBuf<double> loads;  // level-0 terms: steady (n) or transient (steps x n)
     bool has_loads = false, loads_steady = false;
     DevBuf<double> sq;
-    DevBuf<unsigned long long> stat;
+    DevBuf<unsigned long long> stat;    // level-0 Phi solves, p-MG cycles
+    DevBuf<unsigned long long> stat_c;  // coarser levels
     DevBuf<int> err;
     DevBuf<double> err_rel;
     DevBuf<double> u0;
@@ -212,6 +227,8 @@ private:
     void wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, double* CG = nullptr,
               double* CU = nullptr);
     void check_errors();
+    int range_lo(int l) const { return l == 0 ? j_lo : 0; }
+    int range_hi(int l) const;
     void f_relax(int l, bool with_c);
     void c_relax(int l);
     void restrict_residual(int l);

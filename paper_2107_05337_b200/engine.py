@@ -34,7 +34,9 @@ EXPORTED = [
     "phi_mgrit_free", "phi_mgrit_levels", "phi_mgrit_solve", "phi_mgrit_trajectory",
     "phi_mgrit_initial", "phi_mgrit_initialize", "phi_mgrit_cycle", "phi_mgrit_residual_norm",
     "phi_mgrit_launches", "phi_mgrit_set_init_coeffs", "phi_mgrit_profile", "phi_mgrit_wave_report",
-    "phi_dev_tuning", "phi_dev_trace",
+    "phi_dev_tuning", "phi_dev_trace", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
+    "phi_mgrit_gnorm_terms", "phi_mgrit_residual_terms", "phi_mgrit_phase", "phi_mgrit_points",
+    "phi_mgrit_stats",
 ]
 
 
@@ -125,6 +127,13 @@ def lib():
         L.phi_mgrit_launches.restype = _ll
         L.phi_dev_tuning.argtypes = [_i, _i, _i]
         L.phi_dev_trace.argtypes = [_vp, _i]
+        L.phi_mgrit_set_range.argtypes = [_vp, _i, _i]
+        L.phi_mgrit_initialize_state.argtypes = [_vp]
+        L.phi_mgrit_gnorm_terms.argtypes = [_vp, _vp]
+        L.phi_mgrit_residual_terms.argtypes = [_vp, _i, _vp]
+        L.phi_mgrit_phase.argtypes = [_vp, _i, _i]
+        L.phi_mgrit_points.argtypes = [_vp, _i, _i, _i, _i, _vp, _i, _i]
+        L.phi_mgrit_stats.argtypes = [_vp, _vp]
         L.phi_mgrit_set_init_coeffs.argtypes = [_vp, _vp]
         L.phi_mgrit_profile.argtypes = [_vp, _i]
         L.phi_mgrit_wave_report.argtypes = [_vp, _vp, _vp]
@@ -364,6 +373,7 @@ class MgritSolver:
         self.disc = disc
         self.nt = nt
         self.max_iter = max_iter
+        self.m, self.cycle, self.relax, self.halt_tol = m, cycle, relax, halt_tol
         self._coeffs = None if init_coeffs is None else _f64(init_coeffs)
         self._loads = None if load_terms is None else _f64(load_terms)
         ps = Problem(kappa, t_final, theta, nt, source_kind, source_param, init_kind,
@@ -421,6 +431,34 @@ class MgritSolver:
 
     def launches(self) -> int:
         return int(lib().phi_mgrit_launches(self.h))
+
+    # ---- phase-level access for the time-sharded driver (timeshard.py) ----
+    def set_range(self, j_lo: int, j_hi: int) -> None:
+        _check(lib().phi_mgrit_set_range(self.h, j_lo, j_hi))
+
+    def initialize_state(self) -> None:
+        _check(lib().phi_mgrit_initialize_state(self.h))
+
+    def gnorm_terms(self) -> np.ndarray:
+        out = np.zeros(self.levels()[0][0] + 1)
+        _check(lib().phi_mgrit_gnorm_terms(self.h, _p(out)))
+        return out
+
+    def residual_terms(self, level: int = 0) -> np.ndarray:
+        out = np.zeros(self.levels()[0][level] + 1)
+        _check(lib().phi_mgrit_residual_terms(self.h, level, _p(out)))
+        return out
+
+    def phase(self, level: int, op: int) -> None:
+        _check(lib().phi_mgrit_phase(self.h, level, op))
+
+    def points(self, level: int, which: int, k0: int, count: int, ptr: int, device: bool, set_: bool) -> None:
+        _check(lib().phi_mgrit_points(self.h, level, which, k0, count, ptr, int(device), int(set_)))
+
+    def stats(self) -> tuple[int, int, int, int]:
+        out = np.zeros(4, np.int64)
+        _check(lib().phi_mgrit_stats(self.h, _p(out)))
+        return tuple(int(v) for v in out)
 
     def set_init_coeffs(self, coeffs) -> None:
         self._coeffs = _f64(coeffs)
