@@ -52,13 +52,13 @@ extern __shared__ __align__(16) double g_smem[];
 
 // Runtime tuning of the sync-free sweeps (developer knob, phi_dev_tuning).
 struct Tuning {
-    int tri_warps;  // warps taking part in a triangular solve (<= NW)
+    int xmask;      // developer timing experiments (phi_dev_tuning 1st arg; 0 = normal)
     int gs_warps;   // warps taking part in a Gauss-Seidel sweep (<= NW)
     int sleep_ns;   // back-off between failed readiness polls (0 = spin)
     int pad;
     long long* trace;  // developer timing trace of triangular-solve blocks (null = off)
 };
-__constant__ Tuning c_tune = {NW, NW, 0, 0, nullptr};
+__constant__ Tuning c_tune = {0, NW, 0, 0, nullptr};
 
 // Explicit 32-bit shared-window accesses.  Deriving shared pointers inside hot
 // loops makes the compiler re-read the window base (S2R SR_SWINHI /
@@ -105,6 +105,29 @@ __device__ __forceinline__ void pstamp(int id) {
             c_tune.trace[kStampBase + 2 + 2 * k] = clock64();
         }
     }
+}
+
+// Butterfly sum of an fp64 value over aligned groups of 2^lg lanes (lg in
+// 1..5, uniform across the warp): raw shfl.sync.bfly on the two halves, with
+// no divergence checks; the group count is dispatched once.
+__device__ __forceinline__ double shfl_bfly(double v, int o) {
+    unsigned lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    asm volatile("shfl.sync.bfly.b32 %0, %0, %1, 0x1f, 0xffffffff;" : "+r"(lo) : "r"(o));
+    asm volatile("shfl.sync.bfly.b32 %0, %0, %1, 0x1f, 0xffffffff;" : "+r"(hi) : "r"(o));
+    double r;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+__device__ __forceinline__ double bfly_sum(double t, int lg) {
+    switch (lg) {
+        case 5: t = t + shfl_bfly(t, 16); [[fallthrough]];
+        case 4: t = t + shfl_bfly(t, 8); [[fallthrough]];
+        case 3: t = t + shfl_bfly(t, 4); [[fallthrough]];
+        case 2: t = t + shfl_bfly(t, 2); [[fallthrough]];
+        default: t = t + shfl_bfly(t, 1);
+    }
+    return t;
 }
 
 // Correctly rounded s / d from r = RN(1 / d): q0 = RN(s r) is within two ulps,
@@ -326,6 +349,7 @@ template <bool UPPER, bool ZSM, bool EXACT>
 __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
                                               int ring_off, int slot_bytes, int prod_off, unsigned bar) {
     const int lane = threadIdx.x & 31;
+    const int xm = c_tune.xmask;  // developer experiments, 0 in production
     const unsigned ring = sh_addr(g_smem + ring_off);
     const unsigned prod = sh_addr(g_smem + prod_off);
     const unsigned zs = ZSM ? sh_addr(g_smem + z_off) : 0u;
@@ -434,7 +458,7 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
                 }
                 if (tr && b < 1024) tr[8 * b + 2] = clock64();
             } else {
-                const int m = per, G = 1 << lg;
+                const int m = per;
                 // per-lane tables: the row index on a row's first lane (-1
                 // elsewhere) and its reciprocal diagonal
                 const int i = lds_s32(blk + 32u + 4u * lane);
@@ -459,7 +483,8 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
                             v[q] = lds_f64(vp + 256u * (q0 + q));
                         }
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
+                        for (int q = 0; q < 8; ++q)
+                            zj[q] = (xm & 2) ? 1.0 : (ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]]);
                         double pr[8];
 #pragma unroll
                         for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
@@ -469,9 +494,7 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
                     t = a0 + a1;  // idle lanes hold zero slots
                 }
                 if (tr && b < 1024) tr[8 * b + 5] = clock64() + (long long)(t == 12345.678);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1)  // uniform predicate: straight-line butterfly
-                    if (o < G) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+                if (!(xm & 1) && lg > 0) t = bfly_sum(t, lg);
                 if (tr && b < 1024) tr[8 * b + 2] = clock64();
                 if (head) {
                     s = z0 - t;
@@ -489,13 +512,141 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
     }
 }
 
+__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+
+// Fast (reassociated) sweep on TWO warps in ping-pong: block b is solved by
+// warp b & 1.  While one warp runs block b's dependent chain (z loads ->
+// products -> butterfly -> store), the other prepares block b + 1: its header,
+// per-lane tables, right-hand sides and first batch of columns and values,
+// none of which depend on block b.  Hand-off: the warp that finished block b
+// arrives on named barrier 1 + (b & 1); the warp of block b + 1 syncs on it
+// before its z loads (bar.sync orders the shared-memory stores).  The TMA
+// ring is walked by both warps; the slot of a finished unit is refilled by
+// the warp that opens the next unit, once the unit's last block is done.
+template <bool UPPER, bool ZSM>
+__device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
+                                          int ring_off, int slot_bytes, unsigned bar) {
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 1;
+    const unsigned ring = sh_addr(g_smem + ring_off);
+    const unsigned zs = ZSM ? sh_addr(g_smem + z_off) : 0u;
+    const unsigned rs = ZSM ? sh_addr(g_smem + r_off) : 0u;
+    const int n_units = T.n_units;
+    const unsigned char* __restrict__ stream = T.stream;
+    if (n_units == 0) return;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < kTriSlots - 1 && k < n_units; ++k)
+            bulk_fetch(ring + k * slot_bytes, stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
+                       bar + 8u * k);
+    auto open_unit = [&](int uu, int& nblk, int& noff, int& nbytes) -> unsigned {
+        const int slot = uu % kTriSlots;
+        mbar_wait(bar + 8u * slot, (unsigned)(uu / kTriSlots) & 1u);
+        const unsigned unit = ring + slot * slot_bytes;
+        int pad;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nblk), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(unit));
+        (void)pad;
+        return unit + 16u;
+    };
+    int nblk, noff, nbytes;
+    unsigned blk = open_unit(0, nblk, noff, nbytes);
+    // unit kTriSlots - 1 goes to the one slot the prime left empty
+    if (threadIdx.x == 0 && nbytes > 0)
+        bulk_fetch(ring + (kTriSlots - 1) * slot_bytes, stream + (size_t)noff * 16, nbytes,
+                   bar + 8u * (kTriSlots - 1));
+    int u = 0, left = nblk, b = 0;
+    int refill_block = -1, refill_slot = 0, refill_off = 0, refill_bytes = 0;
+    for (;;) {
+        int nr, m, lg, bytes;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nr), "=r"(m), "=r"(lg), "=r"(bytes) : "r"(blk));
+        (void)nr;
+        const bool last = left == 1 && u + 1 == n_units;
+        if ((b & 1) == w) {
+            // ---- prepare block b (independent of block b - 1)
+            int cols_off, vals_off, diag_off, pad;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(cols_off), "=r"(vals_off), "=r"(diag_off), "=r"(pad)
+                         : "r"(blk + 16));
+            (void)pad;
+            const int i = lds_s32(blk + 32u + 4u * lane);  // row index on a row's first lane, -1 elsewhere
+            double rd = 1.0, z0 = 0.0;
+            if (i >= 0) {
+                z0 = ZSM ? lds_f64(rs + 8u * i) : rg[i];  // a row's right-hand side is final from the start
+                if (UPPER) rd = lds_f64(blk + diag_off + 8u * lane);
+            }
+            const unsigned cp = blk + cols_off + 4u * lane, vp = blk + vals_off + 8u * lane;
+            int j[8];
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                j[q] = lds_s32(cp + 128u * q);
+                v[q] = lds_f64(vp + 256u * q);
+            }
+            // ---- wait for block b - 1, then the dependent chain
+            if (b > 0) nbar_sync(1 + ((b - 1) & 1));
+            if (b == refill_block && lane == 0 && refill_bytes > 0)
+                bulk_fetch(ring + refill_slot * slot_bytes, stream + (size_t)refill_off * 16, refill_bytes,
+                           bar + 8u * refill_slot);
+            double zj[8], pr[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
+            double a0 = (pr[0] + pr[1]) + (pr[2] + pr[3]);
+            double a1 = (pr[4] + pr[5]) + (pr[6] + pr[7]);
+            for (int q0 = 8; q0 < m; q0 += 8) {  // further batches (long rows)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    j[q] = lds_s32(cp + 128u * (q0 + q));
+                    v[q] = lds_f64(vp + 256u * (q0 + q));
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
+                a0 = a0 + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+                a1 = a1 + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+            }
+            double t = a0 + a1;  // idle lanes hold zero slots
+            if (lg > 0) t = bfly_sum(t, lg);
+            if (i >= 0) {
+                double s = z0 - t;
+                if (UPPER) s = s * rd;  // reassociated mode: within one ulp of the quotient
+                if (ZSM)
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
+                else
+                    zg[i] = s;
+            }
+            if (!last) nbar_arrive(1 + (b & 1));  // block b done
+        }
+        if (last) break;
+        // ---- advance (both warps walk every block)
+        if (--left > 0) {
+            blk += bytes;
+        } else {
+            ++u;
+            blk = open_unit(u, nblk, noff, nbytes);
+            left = nblk;
+            // unit u + kTriSlots - 1 refills unit u - 1's slot once its last block (b) is done
+            refill_block = b + 1;
+            refill_slot = (u + kTriSlots - 1) % kTriSlots;
+            refill_off = noff;
+            refill_bytes = nbytes;
+        }
+        ++b;
+    }
+}
+
 template <bool UPPER, bool ZSM>
 __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
                                                int ring_off, int slot_bytes, int prod_off, unsigned bar, bool exact) {
-    if (exact)
-        tri_solve_warp_t<UPPER, ZSM, true>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
-    else
-        tri_solve_warp_t<UPPER, ZSM, false>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
+    // called by warps 0 and 1: the exact sweep runs on warp 0, the fast one on both
+    if (exact) {
+        if (threadIdx.x < 32)
+            tri_solve_warp_t<UPPER, ZSM, true>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
+    } else {
+        tri_solve_pp<UPPER, ZSM>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, bar);
+    }
+    nbar_sync(3);  // both warps done (the next sweep reuses the ring and mbarriers)
 }
 
 // Both substitutions of one ILUT application; warp 0 solves, the CTA joins at
@@ -508,13 +659,13 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
     // phases: order those writes before the TMA (async-proxy) writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (threadIdx.x < 32) {
+    if (threadIdx.x < 64) {
         const unsigned bar = sh_addr(bars);
         if (threadIdx.x == 0) {
             for (int k = 0; k < 2 * kTriSlots; ++k) mbar_init(bar + 8u * k);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        __syncwarp();
+        nbar_sync(3);
         if (z_off >= 0) {
             tri_solve_warp<false, true>(L, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
             tri_solve_warp<true, true>(U, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots,
@@ -549,7 +700,7 @@ __device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, 
     __shared__ unsigned long long gbar[kTriSlots];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (threadIdx.x < 32) {
+    if (threadIdx.x < 64) {
         const unsigned bar = sh_addr(gbar);
         const DevTri& T = backward ? lv.gs_bwd : lv.gs_fwd;
         for (int c = 0; c < count; ++c) {
@@ -557,12 +708,11 @@ __device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, 
                 for (int k = 0; k < kTriSlots; ++k) mbar_init(bar + 8u * k);
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             }
-            __syncwarp();
+            nbar_sync(3);
             if (x_off >= 0 && b_off >= 0)
                 tri_solve_warp<true, true>(T, x, x_off, b, b_off, ring_off, slot_bytes, prod_off, bar, exact);
             else
                 tri_solve_warp<true, false>(T, x, -1, b, -1, ring_off, slot_bytes, prod_off, bar, exact);
-            __syncwarp();
         }
     }
     __syncthreads();
@@ -1072,8 +1222,8 @@ void DegLaunch<DEG>::cg(const DevStencil& A, const double* diag, const double* b
 }
 
 template <int DEG>
-void DegLaunch<DEG>::set_trace(long long* trace) {
-    Tuning t{NW, NW, 0, 0, trace};
+void DegLaunch<DEG>::set_trace(long long* trace, int xmask) {
+    Tuning t{xmask, NW, 0, 0, trace};
     PHI_CUDA(cudaMemcpyToSymbol(c_tune, &t, sizeof t));
 }
 

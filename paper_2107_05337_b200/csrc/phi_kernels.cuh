@@ -35,7 +35,7 @@ struct DegLaunch {
                      long long ws_stride, cudaStream_t s);
     static void cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
                    double rel_tol, int max_iter, int* result, cudaStream_t s);
-    static void set_trace(long long* trace);
+    static void set_trace(long long* trace, int xmask);
 };
 extern template struct DegLaunch<1>;
 extern template struct DegLaunch<2>;

@@ -167,7 +167,7 @@ void launch_cg(const DevStencil& A, const double* diag, const double* b, double*
 static DevBuf<long long> g_trace;
 
 void phi_set_tuning(int tri_warps, int gs_warps, int sleep_ns) {
-    (void)tri_warps;
+
     (void)gs_warps;
     long long* trace = nullptr;
     if (sleep_ns < 0) {  // negative: enable the developer timing trace
@@ -175,7 +175,7 @@ void phi_set_tuning(int tri_warps, int gs_warps, int sleep_ns) {
         g_trace.zero();
         trace = g_trace.get();
     }
-    for (int d = 1; d <= 8; ++d) PHI_DEG_DISPATCH(d, DegLaunch<DEG>::set_trace(trace));
+    for (int d = 1; d <= 8; ++d) PHI_DEG_DISPATCH(d, DegLaunch<DEG>::set_trace(trace, tri_warps < 0 ? -tri_warps : 0));
 }
 
 int phi_read_trace(long long* out, int n) {

@@ -5,6 +5,8 @@
 #include "setup_host.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -487,6 +489,22 @@ TriPlan plan_gauss_seidel(const HostCsr& a, bool backward) {
     return make_plan(a.n_rows, backward, rv);
 }
 
+namespace {
+// Cost model of a fast block (cycles): per batch of 8 slots per lane, per
+// butterfly round.  Developer override: PHI_TRI_COST="batch,round".
+double tri_cost(int which) {
+    static double v[2] = {-1.0, -1.0};
+    if (v[0] < 0.0) {
+        v[0] = 180.0;
+        v[1] = 85.0;
+        if (const char* e = std::getenv("PHI_TRI_COST")) std::sscanf(e, "%lf,%lf", &v[0], &v[1]);
+    }
+    return v[which];
+}
+double tri_cost_batch() { return tri_cost(0); }
+double tri_cost_round() { return tri_cost(1); }
+}  // namespace
+
 TriStream make_tri_stream(const TriPlan& p, bool fast) {
     const bool upper = !p.diag.empty();
     // ---- block images
@@ -506,7 +524,7 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
                 // loads); measured (tools/block_probe.cu): ~180 cycles per
                 // batch, ~45 per butterfly round
                 const int mm = (std::max(1, (maxlen + (1 << g) - 1) >> g) + 7) / 8 * 8;
-                const double cost = 180.0 * (mm / 8) + 45.0 * g;
+                const double cost = tri_cost_batch() * (mm / 8) + tri_cost_round() * g;
                 if (cost < best) {
                     best = cost;
                     lg = g;
