@@ -383,7 +383,7 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
             const int ns = (u + kTriSlots - 1) % kTriSlots;
             bulk_fetch(ring + ns * slot_bytes, stream + (size_t)next_off * 16, next_bytes, bar + 8u * ns);
         }
-        unsigned blk = unit + 16u;
+        unsigned blk = unit + 16u + ((2u * nblk + 15u) & ~15u);  // after the block-offset table
         for (int kb = 0; kb < nblk; ++kb, ++b) {
             if (tr && b < 1024) {
                 if (kb) tr[8 * b] = clock64();
@@ -512,22 +512,29 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
     }
 }
 
+// Warps that take turns on the blocks of a fast sweep (setup_host.hpp
+// kSweepWarps: the host classifies entries as "fresh" against this distance).
+constexpr int kSW = kSweepWarps;
+constexpr int kSweepBar = kSW + 1;  // named barrier of all sweep warps
 __device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void sweep_sync() { asm volatile("bar.sync %0, %1;" ::"r"(kSweepBar), "r"(32 * kSW) : "memory"); }
 
-// Fast (reassociated) sweep on TWO warps in ping-pong: block b is solved by
-// warp b & 1.  While one warp runs block b's dependent chain (z loads ->
-// products -> butterfly -> store), the other prepares block b + 1: its header,
-// per-lane tables, right-hand sides and first batch of columns and values,
-// none of which depend on block b.  Hand-off: the warp that finished block b
-// arrives on named barrier 1 + (b & 1); the warp of block b + 1 syncs on it
-// before its z loads (bar.sync orders the shared-memory stores).  The TMA
-// ring is walked by both warps; the slot of a finished unit is refilled by
-// the warp that opens the next unit, once the unit's last block is done.
+// Fast (reassociated) sweep on kSW warps taking turns: block b is solved by
+// warp b % kSW.  A warp prepares its next block while the others run theirs:
+// header, per-lane tables, right-hand sides, the complete sum of the block's
+// "old" entries (columns solved kSW or more blocks earlier -- final once the
+// warp's own previous block is done) and the columns and values of its
+// "fresh" entries.  Only the fresh entries' z loads, a short tree, the update
+// and the store remain on the critical path.  Hand-off: the warp that
+// finished block b arrives on named barrier 1 + b % kSW; the warp of block
+// b + 1 syncs on it (bar.sync orders the shared-memory stores).  All warps
+// walk the TMA ring; the slot of a finished unit is refilled by the warp that
+// opens the next unit once the unit's last block is done.
 template <bool UPPER, bool ZSM>
 __device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
                                           int ring_off, int slot_bytes, unsigned bar) {
-    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // w < kSW
     const unsigned ring = sh_addr(g_smem + ring_off);
     const unsigned zs = ZSM ? sh_addr(g_smem + z_off) : 0u;
     const unsigned rs = ZSM ? sh_addr(g_smem + r_off) : 0u;
@@ -538,62 +545,62 @@ __device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off
         for (int k = 0; k < kTriSlots - 1 && k < n_units; ++k)
             bulk_fetch(ring + k * slot_bytes, stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
                        bar + 8u * k);
-    auto open_unit = [&](int uu, int& nblk, int& noff, int& nbytes) -> unsigned {
+    // each warp visits only its own blocks: b = w, w + kSW, ..; a unit is
+    // opened (mbarrier wait + header) when a warp's next block lies in it, and
+    // the unit's block-offset table locates the block
+    int u = 0, nblk = 0, noff = 0, nbytes = 0;
+    unsigned unit = 0;
+    auto open_unit = [&](int uu) {
         const int slot = uu % kTriSlots;
         mbar_wait(bar + 8u * slot, (unsigned)(uu / kTriSlots) & 1u);
-        const unsigned unit = ring + slot * slot_bytes;
+        unit = ring + slot * slot_bytes;
         int pad;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nblk), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(unit));
         (void)pad;
-        return unit + 16u;
     };
-    int nblk, noff, nbytes;
-    unsigned blk = open_unit(0, nblk, noff, nbytes);
+    open_unit(0);
     // unit kTriSlots - 1 goes to the one slot the prime left empty
     if (threadIdx.x == 0 && nbytes > 0)
         bulk_fetch(ring + (kTriSlots - 1) * slot_bytes, stream + (size_t)noff * 16, nbytes,
                    bar + 8u * (kTriSlots - 1));
-    int u = 0, left = nblk, b = 0;
-    int refill_block = -1, refill_slot = 0, refill_off = 0, refill_bytes = 0;
-    for (;;) {
+    int k = w;  // this warp's block within unit u
+    for (int b = w;; b += kSW) {
+        while (k >= nblk) {  // the block lies in a later unit
+            if (u + 1 >= n_units) return;  // past the end of the stream
+            k -= nblk;
+            open_unit(++u);
+        }
+        unsigned short boff;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(boff) : "r"(unit + 16u + 2u * k));
+        const unsigned blk = unit + boff;
+        const bool last = u + 1 == n_units && k + 1 == nblk;
         int nr, m, lg, bytes;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nr), "=r"(m), "=r"(lg), "=r"(bytes) : "r"(blk));
         (void)nr;
-        const bool last = left == 1 && u + 1 == n_units;
-        if ((b & 1) == w) {
-            // ---- prepare block b (independent of block b - 1)
-            int cols_off, vals_off, diag_off, pad;
+        (void)bytes;
+        long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && b < 1024)
+                            ? c_tune.trace + kTriTraceBase + 8 * b
+                            : nullptr;
+        if (tr) tr[0] = clock64();
+        {
+            // ---- prepare block b: everything but its fresh entries
+            int cols_off, vals_off, diag_off, fp;
             asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(cols_off), "=r"(vals_off), "=r"(diag_off), "=r"(pad)
+                         : "=r"(cols_off), "=r"(vals_off), "=r"(diag_off), "=r"(fp)
                          : "r"(blk + 16));
-            (void)pad;
             const int i = lds_s32(blk + 32u + 4u * lane);  // row index on a row's first lane, -1 elsewhere
             double rd = 1.0, z0 = 0.0;
             if (i >= 0) {
                 z0 = ZSM ? lds_f64(rs + 8u * i) : rg[i];  // a row's right-hand side is final from the start
                 if (UPPER) rd = lds_f64(blk + diag_off + 8u * lane);
             }
+            // old entries: solved kSW or more blocks ago (this warp's previous
+            // block b - kSW is done, so they are final)
             const unsigned cp = blk + cols_off + 4u * lane, vp = blk + vals_off + 8u * lane;
-            int j[8];
-            double v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                j[q] = lds_s32(cp + 128u * q);
-                v[q] = lds_f64(vp + 256u * q);
-            }
-            // ---- wait for block b - 1, then the dependent chain
-            if (b > 0) nbar_sync(1 + ((b - 1) & 1));
-            if (b == refill_block && lane == 0 && refill_bytes > 0)
-                bulk_fetch(ring + refill_slot * slot_bytes, stream + (size_t)refill_off * 16, refill_bytes,
-                           bar + 8u * refill_slot);
-            double zj[8], pr[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
-            double a0 = (pr[0] + pr[1]) + (pr[2] + pr[3]);
-            double a1 = (pr[4] + pr[5]) + (pr[6] + pr[7]);
-            for (int q0 = 8; q0 < m; q0 += 8) {  // further batches (long rows)
+            double t_old = 0.0;
+            for (int q0 = 0; q0 < m; q0 += 8) {
+                int j[8];
+                double v[8], zj[8], pr[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     j[q] = lds_s32(cp + 128u * (q0 + q));
@@ -603,50 +610,75 @@ __device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off
                 for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
-                a0 = a0 + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
-                a1 = a1 + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+                t_old = t_old + (((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7])));
             }
-            double t = a0 + a1;  // idle lanes hold zero slots
-            if (lg > 0) t = bfly_sum(t, lg);
+            if (lg > 0) t_old = bfly_sum(t_old, lg);  // idle lanes hold zero slots
+            // fresh entries (solved by blocks b - kSW + 1 .. b - 1): columns
+            // and values now, their z after the hand-off
+            const unsigned fc = (vals_off + 256u * m + 15u) & ~15u;
+            const unsigned fv = (fc + 128u * fp + 15u) & ~15u;
+            const unsigned fcp = blk + fc + 4u * lane, fvp = blk + fv + 8u * lane;
+            int fj[8];
+            double fvv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                fj[q] = fp > 0 ? lds_s32(fcp + 128u * q) : T.n;
+                fvv[q] = fp > 0 ? lds_f64(fvp + 256u * q) : 0.0;
+            }
+            // ---- wait for block b - 1, then the critical path
+            if (tr) tr[1] = clock64() + (long long)(t_old == 12345.678) + (long long)(fj[7] == -7) + (long long)(fvv[7] == 1.5);
+            if (b > 0) nbar_sync(1 + (b - 1) % kSW);
+            if (tr) tr[2] = clock64();
+            // the first block of unit u refills unit u - 1's slot (all of its
+            // blocks are done now) with unit u + kTriSlots - 1
+            if (k == 0 && u > 0 && lane == 0 && nbytes > 0)
+                bulk_fetch(ring + ((u + kTriSlots - 1) % kTriSlots) * slot_bytes, stream + (size_t)noff * 16, nbytes,
+                           bar + 8u * ((u + kTriSlots - 1) % kTriSlots));
+            double zj[8], pr[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * fj[q]) : zg[fj[q]];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pr[q] = fvv[q] * zj[q];
+            double t_new = ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+            for (int q0 = 8; q0 < fp; q0 += 8) {  // rare: more than 8 fresh entries
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    fj[q] = lds_s32(fcp + 128u * (q0 + q));
+                    fvv[q] = lds_f64(fvp + 256u * (q0 + q));
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * fj[q]) : zg[fj[q]];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pr[q] = fvv[q] * zj[q];
+                t_new = t_new + (((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7])));
+            }
             if (i >= 0) {
-                double s = z0 - t;
+                double s = z0 - (t_old + t_new);
                 if (UPPER) s = s * rd;  // reassociated mode: within one ulp of the quotient
                 if (ZSM)
                     asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
                 else
                     zg[i] = s;
             }
-            if (!last) nbar_arrive(1 + (b & 1));  // block b done
+            if (tr) tr[3] = clock64();
+            if (!last) nbar_arrive(1 + b % kSW);  // block b done
         }
-        if (last) break;
-        // ---- advance (both warps walk every block)
-        if (--left > 0) {
-            blk += bytes;
-        } else {
-            ++u;
-            blk = open_unit(u, nblk, noff, nbytes);
-            left = nblk;
-            // unit u + kTriSlots - 1 refills unit u - 1's slot once its last block (b) is done
-            refill_block = b + 1;
-            refill_slot = (u + kTriSlots - 1) % kTriSlots;
-            refill_off = noff;
-            refill_bytes = nbytes;
-        }
-        ++b;
+        if (last) return;
+        k += kSW;
     }
 }
 
 template <bool UPPER, bool ZSM>
 __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
                                                int ring_off, int slot_bytes, int prod_off, unsigned bar, bool exact) {
-    // called by warps 0 and 1: the exact sweep runs on warp 0, the fast one on both
+    // called by the kSW sweep warps: the exact sweep runs on warp 0, the fast one on all
     if (exact) {
         if (threadIdx.x < 32)
             tri_solve_warp_t<UPPER, ZSM, true>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
     } else {
         tri_solve_pp<UPPER, ZSM>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, bar);
     }
-    nbar_sync(3);  // both warps done (the next sweep reuses the ring and mbarriers)
+    sweep_sync();  // all sweep warps done (the next sweep reuses the ring and mbarriers)
 }
 
 // Both substitutions of one ILUT application; warp 0 solves, the CTA joins at
@@ -659,13 +691,13 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
     // phases: order those writes before the TMA (async-proxy) writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (threadIdx.x < 64) {
+    if (threadIdx.x < 32 * kSW) {
         const unsigned bar = sh_addr(bars);
         if (threadIdx.x == 0) {
             for (int k = 0; k < 2 * kTriSlots; ++k) mbar_init(bar + 8u * k);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        nbar_sync(3);
+        sweep_sync();
         if (z_off >= 0) {
             tri_solve_warp<false, true>(L, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar, exact);
             tri_solve_warp<true, true>(U, zg, z_off, zg, z_off, ring_off, slot_bytes, prod_off, bar + 8u * kTriSlots,
@@ -700,7 +732,7 @@ __device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, 
     __shared__ unsigned long long gbar[kTriSlots];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (threadIdx.x < 64) {
+    if (threadIdx.x < 32 * kSW) {
         const unsigned bar = sh_addr(gbar);
         const DevTri& T = backward ? lv.gs_bwd : lv.gs_fwd;
         for (int c = 0; c < count; ++c) {
@@ -708,7 +740,7 @@ __device__ __forceinline__ void gs_sweeps(const DevHLevel& lv, const double* b, 
                 for (int k = 0; k < kTriSlots; ++k) mbar_init(bar + 8u * k);
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             }
-            nbar_sync(3);
+            sweep_sync();
             if (x_off >= 0 && b_off >= 0)
                 tri_solve_warp<true, true>(T, x, x_off, b, b_off, ring_off, slot_bytes, prod_off, bar, exact);
             else

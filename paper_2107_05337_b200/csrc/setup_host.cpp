@@ -505,11 +505,93 @@ double tri_cost_batch() { return tri_cost(0); }
 double tri_cost_round() { return tri_cost(1); }
 }  // namespace
 
+// Fast block c: every entry of its rows is either "old" (its column was
+// solved kSweepWarps or more blocks earlier, or is solved later) or "fresh"
+// (solved by one of the kSweepWarps - 1 blocks just before c).  Old
+// entries: G = 2^lg lanes per row, slot q of lane L at q * 32 + L over m
+// slots; they are summed while the previous block is still being solved.
+// Fresh entries sit on the row's first lane (Fp slots, same layout) and are
+// the only loads on the critical path.  Header: nr, m, lg, bytes, cols_off,
+// vals_off, diag_off, Fp; fresh columns at align16(vals_off + 256 m), fresh
+// values at align16(that + 128 Fp).
+static std::vector<unsigned char> fast_block(const TriPlan& p, int c, const std::vector<int>& block_of, bool upper) {
+    const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
+    std::vector<std::vector<std::pair<int, double>>> olde(nr), frsh(nr);
+    int maxold = 0, maxfresh = 0;
+    for (int l = 0; l < nr; ++l) {
+        for (int e = 0; e < p.lens[row0 + l]; ++e) {
+            const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * nr + l;
+            const int col = p.cols[src];
+            // solved by one of the kSweepWarps - 1 blocks before this one
+            const bool fresh = col < p.n && block_of[col] < c && block_of[col] > c - kSweepWarps;
+            (fresh ? frsh : olde)[l].emplace_back(col, p.vals[src]);
+        }
+        maxold = std::max(maxold, static_cast<int>(olde[l].size()));
+        maxfresh = std::max(maxfresh, static_cast<int>(frsh[l].size()));
+    }
+    int lg = 0, m = 0;
+    if (maxold > 0) {
+        double best = 1e30;
+        for (int g = 0; (nr << g) <= 32; ++g) {
+            const int mm = (std::max(1, (maxold + (1 << g) - 1) >> g) + 7) / 8 * 8;
+            const double cost = tri_cost_batch() * (mm / 8) + tri_cost_round() * g;
+            if (cost < best) {
+                best = cost;
+                lg = g;
+                m = mm;
+            }
+        }
+    }
+    const int fp = (maxfresh + 7) / 8 * 8;
+    const int diag_off = 32 + 4 * 32;
+    const int cols_off = diag_off + (upper ? 8 * 32 : 0);
+    const int vals_off = (cols_off + 128 * m + 15) / 16 * 16;
+    const int fcols_off = (vals_off + 256 * m + 15) / 16 * 16;
+    const int fvals_off = (fcols_off + 128 * fp + 15) / 16 * 16;
+    const int bytes = (fvals_off + 256 * fp + 15) / 16 * 16;
+    if (bytes + 16 > kTriUnitCap)
+        throw InvalidArgument("ILUT factor level slice exceeds the triangular-solve block capacity");
+    std::vector<unsigned char> img(bytes, 0);
+    const int hdr[8] = {nr, m, lg, bytes, cols_off, vals_off, diag_off, fp};
+    std::memcpy(img.data(), hdr, sizeof hdr);
+    int* rws = reinterpret_cast<int*>(img.data() + 32);
+    double* rd = reinterpret_cast<double*>(img.data() + diag_off);
+    int* cols = reinterpret_cast<int*>(img.data() + cols_off);
+    double* vals = reinterpret_cast<double*>(img.data() + vals_off);
+    int* fcols = reinterpret_cast<int*>(img.data() + fcols_off);
+    double* fvals = reinterpret_cast<double*>(img.data() + fvals_off);
+    for (int s = 0; s < 32 * m; ++s) cols[s] = p.n;  // neutral dummies (z[n] = +0.0, value +0.0)
+    for (int s = 0; s < 32 * fp; ++s) fcols[s] = p.n;
+    for (int L = 0; L < 32; ++L) rws[L] = -1;
+    for (int l = 0; l < nr; ++l) {
+        const int i = p.rows[row0 + l], lane0 = l << lg;
+        rws[lane0] = i;
+        if (upper) rd[lane0] = 1.0 / p.diag[i];  // IEEE round-to-nearest reciprocal
+        for (size_t e = 0; e < olde[l].size(); ++e) {
+            const size_t dst = (e % m) * 32 + lane0 + e / m;
+            cols[dst] = olde[l][e].first;
+            vals[dst] = olde[l][e].second;
+        }
+        for (size_t e = 0; e < frsh[l].size(); ++e) {
+            fcols[e * 32 + lane0] = frsh[l][e].first;
+            fvals[e * 32 + lane0] = frsh[l][e].second;
+        }
+    }
+    return img;
+}
+
 TriStream make_tri_stream(const TriPlan& p, bool fast) {
     const bool upper = !p.diag.empty();
+    std::vector<int> block_of(p.n, -1);  // plan chunk (stream block) of every row
+    for (int c = 0; c < p.n_chunks; ++c)
+        for (int l = 0; l < p.chunk_meta[4 * c + 1]; ++l) block_of[p.rows[p.chunk_meta[4 * c] + l]] = c;
     // ---- block images
     std::vector<std::vector<unsigned char>> blocks;
     for (int c = 0; c < p.n_chunks; ++c) {
+        if (fast) {
+            blocks.push_back(fast_block(p, c, block_of, upper));
+            continue;
+        }
         const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
         const int span = p.chunk_meta[4 * c + 3];
         int lg = 0, m = span;
@@ -594,16 +676,20 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
         }
         blocks.push_back(std::move(img));
     }
-    // ---- units
+    // ---- units: header (16 B: n_blocks, next_off16, next_bytes, pad) + a
+    // table of uint16 block offsets from the unit start (padded to 16 B),
+    // then the blocks
+    auto hdr_bytes = [](size_t nb) { return 16 + (2 * nb + 15) / 16 * 16; };
     TriStream ts;
     ts.n_blocks = static_cast<int>(blocks.size());
     std::vector<std::pair<size_t, size_t>> units;  // [first block, end block)
     {
         size_t b = 0;
         while (b < blocks.size()) {
-            size_t e = b, bytes = 16;
-            while (e < blocks.size() && bytes + blocks[e].size() <= static_cast<size_t>(kTriUnitCap))
+            size_t e = b, bytes = 0;
+            while (e < blocks.size() && hdr_bytes(e + 1 - b) + bytes + blocks[e].size() <= static_cast<size_t>(kTriUnitCap))
                 bytes += blocks[e++].size();
+            if (e == b) throw InvalidArgument("triangular-solve block exceeds the TMA unit capacity");
             units.emplace_back(b, e);
             b = e;
         }
@@ -612,7 +698,7 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
     std::vector<size_t> uoff, ubytes;
     size_t total = 0;
     for (const auto& u : units) {
-        size_t bytes = 16;
+        size_t bytes = hdr_bytes(u.second - u.first);
         for (size_t k = u.first; k < u.second; ++k) bytes += blocks[k].size();
         uoff.push_back(total);
         ubytes.push_back(bytes);
@@ -627,15 +713,18 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
     }
     for (size_t u = 0; u < units.size(); ++u) {
         unsigned char* dst = ts.stream.data() + uoff[u];
-        int hdr[4] = {static_cast<int>(units[u].second - units[u].first), 0, 0, 0};
+        const size_t nb = units[u].second - units[u].first;
+        int hdr[4] = {static_cast<int>(nb), 0, 0, 0};
         const size_t nxt = u + kTriSlots - 1;
         if (nxt < units.size()) {
             hdr[1] = static_cast<int>(uoff[nxt] / 16);
             hdr[2] = static_cast<int>(ubytes[nxt]);
         }
         std::memcpy(dst, hdr, sizeof hdr);
-        size_t o = 16;
+        auto* tab = reinterpret_cast<unsigned short*>(dst + 16);
+        size_t o = hdr_bytes(nb);
         for (size_t k = units[u].first; k < units[u].second; ++k) {
+            tab[k - units[u].first] = static_cast<unsigned short>(o);
             std::memcpy(dst + o, blocks[k].data(), blocks[k].size());
             o += blocks[k].size();
         }

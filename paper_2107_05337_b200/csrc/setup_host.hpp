@@ -92,7 +92,8 @@ TriPlan plan_gauss_seidel(const HostCsr& a, bool backward);
 /// of <= kTriUnitCap bytes; one cp.async.bulk moves one unit into a slot of the
 /// shared-memory ring.
 ///   unit header (16 B): n_blocks, next_off16, next_bytes (unit
-///                       u + kTriSlots - 1, 0 if none), pad
+///                       u + kTriSlots - 1, 0 if none), pad; then uint16
+///                       byte offsets of the unit's blocks (padded to 16 B)
 ///   block header (32 B): nr, span | m, lg, block_bytes, cols_off, vals_off,
 ///                        diag_off, pad
 ///   rows  int32[nr]   at 32 (padded to 8 bytes)
@@ -108,7 +109,7 @@ TriPlan plan_gauss_seidel(const HostCsr& a, bool backward);
 /// they are exactly neutral.  Offsets in headers are bytes from the block /
 /// unit start; `next_off16` and `prime` are 16-byte units of `stream`;
 /// `prime` holds (off16, bytes) of the first kTriSlots - 1 units.
-constexpr int kTriUnitCap = 12 * 1024;
+constexpr int kTriUnitCap = 8 * 1024;
 struct TriStream {
     std::vector<unsigned char> stream;
     std::vector<int> prime;  // 2 * (kTriSlots - 1)

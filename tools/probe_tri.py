@@ -25,12 +25,16 @@ for kind in ("unit", "solve"):
     t = buf[BASE:BASE + 8 * 1024].reshape(1024, 8).astype(np.float64)
     nb = int((t[:, 0] > 0).sum())
     t = t[:nb]
-    wait = t[:, 1] - t[:, 0]
-    acc = t[:, 5] - t[:, 1]
-    red = t[:, 2] - t[:, 5]
-    fin = t[:, 3] - t[:, 2]
-    gap = t[1:, 0] - t[:-1, 3]
-    tot = t[1:, 0] - t[:-1, 0]
+    prep = t[:, 1] - t[:, 0]
+    wait = t[:, 2] - t[:, 1]
+    chain = t[:, 3] - t[:, 2]
+    period = np.diff(t[:, 2])
+    walk = t[4:, 0] - t[:-4, 3]
+    wk = buf[BASE + 8192:BASE + 8192 + 4096].reshape(4, 1024).astype(np.float64)
+    for w in range(2):
+        d = np.diff(wk[w, :nb])
+        print(f"   warp {w} loop-top deltas (first 16):", d[:16].astype(int).tolist())
+    print("   walk (chain end -> prep of the warp's next block)", float(np.median(walk)))
     med = lambda v: float(np.median(v))
-    print(f"{kind}: blocks {nb}  wait {med(wait):.0f}  accumulate {med(acc):.0f}  reduce {med(red):.0f}  "
-          f"finish {med(fin):.0f}  gap {med(gap):.0f}  per block {med(tot):.0f} / mean {tot.mean():.0f} cycles")
+    print(f"{kind}: blocks {nb}  prep {med(prep):.0f}  wait {med(wait):.0f}  chain {med(chain):.0f}  "
+          f"period {med(period):.0f} / mean {period.mean():.0f} cycles")
