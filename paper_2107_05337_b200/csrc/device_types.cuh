@@ -39,10 +39,11 @@ constexpr int kTriMaxItems = kTriBlockCap / 12;
 
 /// Level-scheduled triangular factor as a TMA block stream (TriStream).
 struct DevTri {
-    int n, n_levels, n_units;
+    int n, n_levels, n_units, n_blocks;
     int max_unit_bytes;
-    int prime[2 * (kTriSlots - 1)];  // (off16, bytes) of the first kTriSlots - 1 blocks
+    int prime[2 * (kTriSlots - 1)];  // (off16, bytes) of the first kTriSlots - 1 units
     const unsigned char* stream;  // 16-byte aligned
+    const int4* blocks;           // per block: unit, byte offset in the unit, first-in-unit flag, 0
 };
 
 struct DevHLevel {

@@ -165,6 +165,8 @@ namespace {
 void upload_tri(const TriPlan& p, bool fast, Hier::TriDev& d, cudaStream_t s) {
     const TriStream ts = make_tri_stream(p, fast);
     d.stream = dev(ts.stream, s);  // cudaMalloc: 256-byte aligned
+    d.block_info = dev(ts.block_info, s);
+    d.n_blocks = ts.n_blocks;
     d.n_units = ts.n_units;
     d.max_unit_bytes = ts.max_unit_bytes;
     for (int k = 0; k < 2 * (kTriSlots - 1); ++k) d.prime[k] = ts.prime[k];
@@ -174,7 +176,9 @@ DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
     t.n = p.n;
     t.n_levels = p.n_levels;
     t.n_units = d.n_units;
+    t.n_blocks = d.n_blocks;
     t.max_unit_bytes = d.max_unit_bytes;
+    t.blocks = reinterpret_cast<const int4*>(d.block_info.get());
     for (int k = 0; k < 2 * (kTriSlots - 1); ++k) t.prime[k] = d.prime[k];
     t.stream = d.stream.get();
     return t;

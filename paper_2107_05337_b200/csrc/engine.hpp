@@ -99,7 +99,8 @@ public:
     TriPlan Lp, Up;
     struct TriDev {
         DevBuf<unsigned char> stream;
-        int n_units = 0, max_unit_bytes = 0;
+        DevBuf<int> block_info;
+        int n_units = 0, n_blocks = 0, max_unit_bytes = 0;
         int prime[2 * (kTriSlots - 1)] = {};
     } Ld, Ud;
     std::vector<TriPlan> gs_plans;  // per h-level (but the coarsest): forward, backward

@@ -545,35 +545,41 @@ __device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off
         for (int k = 0; k < kTriSlots - 1 && k < n_units; ++k)
             bulk_fetch(ring + k * slot_bytes, stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
                        bar + 8u * k);
-    // each warp visits only its own blocks: b = w, w + kSW, ..; a unit is
-    // opened (mbarrier wait + header) when a warp's next block lies in it, and
-    // the unit's block-offset table locates the block
-    int u = 0, nblk = 0, noff = 0, nbytes = 0;
+    // Each warp touches only the units that hold its own blocks b = w,
+    // w + kSW, ..: the block table (global, prefetched one turn ahead) gives
+    // a block's unit and offset, so no warp ever reads a unit whose slot may
+    // already be recycled (a slot is refilled once all of its blocks are done).
+    const int n_blocks = T.n_blocks;
+    const int4* __restrict__ table = T.blocks;
+    int u = -1, noff = 0, nbytes = 0;
     unsigned unit = 0;
-    auto open_unit = [&](int uu) {
-        const int slot = uu % kTriSlots;
-        mbar_wait(bar + 8u * slot, (unsigned)(uu / kTriSlots) & 1u);
-        unit = ring + slot * slot_bytes;
-        int pad;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nblk), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(unit));
+    if (threadIdx.x == 0) {  // unit kTriSlots - 1 goes to the one slot the prime left empty
+        mbar_wait(bar, 0u);
+        int nb, pad;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nb), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(ring));
+        (void)nb;
         (void)pad;
-    };
-    open_unit(0);
-    // unit kTriSlots - 1 goes to the one slot the prime left empty
-    if (threadIdx.x == 0 && nbytes > 0)
-        bulk_fetch(ring + (kTriSlots - 1) * slot_bytes, stream + (size_t)noff * 16, nbytes,
-                   bar + 8u * (kTriSlots - 1));
-    int k = w;  // this warp's block within unit u
-    for (int b = w;; b += kSW) {
-        while (k >= nblk) {  // the block lies in a later unit
-            if (u + 1 >= n_units) return;  // past the end of the stream
-            k -= nblk;
-            open_unit(++u);
+        if (nbytes > 0)
+            bulk_fetch(ring + (kTriSlots - 1) * slot_bytes, stream + (size_t)noff * 16, nbytes,
+                       bar + 8u * (kTriSlots - 1));
+    }
+    int4 nxt = w < n_blocks ? __ldg(table + w) : make_int4(0, 0, 0, 0);
+    for (int b = w; b < n_blocks; b += kSW) {
+        const int4 info = nxt;
+        if (b + kSW < n_blocks) nxt = __ldg(table + b + kSW);
+        if (info.x != u) {  // open the block's unit: wait for its TMA, read its refill fields
+            u = info.x;
+            const int slot = u % kTriSlots;
+            mbar_wait(bar + 8u * slot, (unsigned)(u / kTriSlots) & 1u);
+            unit = ring + slot * slot_bytes;
+            int nb, pad;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nb), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(unit));
+            (void)nb;
+            (void)pad;
         }
-        unsigned short boff;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(boff) : "r"(unit + 16u + 2u * k));
-        const unsigned blk = unit + boff;
-        const bool last = u + 1 == n_units && k + 1 == nblk;
+        const unsigned blk = unit + (unsigned)info.y;
+        const bool last = b + 1 == n_blocks;
+        const int k = info.z ? 0 : 1;  // 0: first block of its unit
         int nr, m, lg, bytes;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nr), "=r"(m), "=r"(lg), "=r"(bytes) : "r"(blk));
         (void)nr;
@@ -664,7 +670,6 @@ __device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off
             if (!last) nbar_arrive(1 + b % kSW);  // block b done
         }
         if (last) return;
-        k += kSW;
     }
 }
 

@@ -726,6 +726,8 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
         for (size_t k = units[u].first; k < units[u].second; ++k) {
             tab[k - units[u].first] = static_cast<unsigned short>(o);
             std::memcpy(dst + o, blocks[k].data(), blocks[k].size());
+            ts.block_info.insert(ts.block_info.end(),
+                                 {static_cast<int>(u), static_cast<int>(o), k == units[u].first ? 1 : 0, 0});
             o += blocks[k].size();
         }
     }

@@ -116,6 +116,7 @@ struct TriStream {
     int n_blocks = 0;        // blocks (levels / level slices)
     int n_units = 0;
     int max_unit_bytes = 0;
+    std::vector<int> block_info;  // 4 per block: unit, byte offset in the unit, first in unit, 0
 };
 TriStream make_tri_stream(const TriPlan& p, bool fast);
 
