@@ -31,7 +31,7 @@ struct DevCsr {
 /// Depth of the shared-memory ring that stages triangular-factor blocks.
 constexpr int kTriSlots = 8;
 /// Warps that take turns on the blocks of a fast (reassociated) sweep.
-constexpr int kSweepWarps = 4;
+constexpr int kSweepWarps = 6;
 /// Bytes per triangular-factor block (TriPlan chunking) and the product
 /// scratch that bound implies (12 bytes per entry: int32 column + fp64 value).
 constexpr int kTriBlockCap = 5 * 1024;

@@ -109,7 +109,7 @@ TriPlan plan_gauss_seidel(const HostCsr& a, bool backward);
 /// they are exactly neutral.  Offsets in headers are bytes from the block /
 /// unit start; `next_off16` and `prime` are 16-byte units of `stream`;
 /// `prime` holds (off16, bytes) of the first kTriSlots - 1 units.
-constexpr int kTriUnitCap = 8 * 1024;
+constexpr int kTriUnitCap = 10 * 1024;
 struct TriStream {
     std::vector<unsigned char> stream;
     std::vector<int> prime;  // 2 * (kTriSlots - 1)
