@@ -549,9 +549,7 @@ static std::vector<unsigned char> fast_block(const TriPlan& p, int c, const std:
     const int fcols_off = (vals_off + 256 * m + 15) / 16 * 16;
     const int fvals_off = (fcols_off + 128 * fp + 15) / 16 * 16;
     const int bytes = (fvals_off + 256 * fp + 15) / 16 * 16;
-    if (bytes + 16 > kTriUnitCap)
-        throw InvalidArgument("ILUT factor level slice exceeds the triangular-solve block capacity");
-    std::vector<unsigned char> img(bytes, 0);
+    std::vector<unsigned char> img(bytes, 0);  // may exceed kTriUnitCap: then it is a unit of its own
     const int hdr[8] = {nr, m, lg, bytes, cols_off, vals_off, diag_off, fp};
     std::memcpy(img.data(), hdr, sizeof hdr);
     int* rws = reinterpret_cast<int*>(img.data() + 32);
@@ -687,9 +685,9 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
         size_t b = 0;
         while (b < blocks.size()) {
             size_t e = b, bytes = 0;
-            while (e < blocks.size() && hdr_bytes(e + 1 - b) + bytes + blocks[e].size() <= static_cast<size_t>(kTriUnitCap))
-                bytes += blocks[e++].size();
-            if (e == b) throw InvalidArgument("triangular-solve block exceeds the TMA unit capacity");
+            while (e < blocks.size() &&
+                   (e == b || hdr_bytes(e + 1 - b) + bytes + blocks[e].size() <= static_cast<size_t>(kTriUnitCap)))
+                bytes += blocks[e++].size();  // a block larger than the cap forms a unit of its own
             units.emplace_back(b, e);
             b = e;
         }
