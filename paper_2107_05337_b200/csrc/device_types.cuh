@@ -30,6 +30,11 @@ struct DevCsr {
 
 /// Depth of the shared-memory ring that stages triangular-factor blocks.
 constexpr int kTriSlots = 8;
+/// Block sweeps: maximum ring depth, maximum fresh distance F and the depth of
+/// the worker -> solver hand-off ring (>= F + 1).
+constexpr int kBlkMaxSlots = 8;
+constexpr int kBlkMaxFresh = 4;
+constexpr int kBlkHand = 8;
 /// Warps that take turns on the blocks of a fast (reassociated) sweep.
 constexpr int kSweepWarps = 6;
 /// Bytes per triangular-factor block (TriPlan chunking) and the product
@@ -46,9 +51,18 @@ struct DevTri {
     const int4* blocks;           // per block: unit, byte offset in the unit, first-in-unit flag, 0
 };
 
+/// Block-recurrence sweep (BlkStream, setup_host.hpp): one fetch unit per
+/// block of 32 rows in solve order; `table` holds (offset / 16, bytes).
+struct DevBlk {
+    int n, n_blocks, fresh, max_unit_bytes;
+    const unsigned char* stream;  // 16-byte aligned
+    const int2* table;
+};
+
 struct DevHLevel {
     DevStencil a;    // M_l + c K_l, 9-point
-    DevTri gs_fwd, gs_bwd;  // Gauss-Seidel sweeps as level-scheduled streams (empty on the coarsest)
+    DevTri gs_fwd, gs_bwd;  // Gauss-Seidel sweeps as level-scheduled streams (exact mode; empty on the coarsest)
+    DevBlk gsb_fwd, gsb_bwd;  // the same sweeps as block recurrences (reassociated mode)
     DevCsr embed;    // level l+1 -> level l (empty on the coarsest)
     DevCsr embed_t;  // its transpose (restriction rows, ascending fine index)
     int n;
@@ -65,7 +79,8 @@ struct DevHier {
     DevStencil Tt;  // its transpose
     const double* inv_lp;
     const double* inv_l1;
-    DevTri L, U;
+    DevTri L, U;    // level-scheduled ILUT factors (exact mode)
+    DevBlk Lb, Ub;  // block-recurrence ILUT factors (reassociated mode)
     DevHLevel h[kMaxH];
     const double* coarse_lu;
     const int* coarse_piv;
@@ -82,6 +97,9 @@ struct DevHier {
 struct SmemPlan {
     int ring_off;          // triangular-factor block ring (TMA staging)
     int slot_bytes;        // bytes per ring slot
+    int n_slots;           // ring depth (block sweeps; level streams use kTriSlots)
+    int gs_slot_bytes;     // ring slot / depth of the W-cycle phase (block sweeps)
+    int gs_n_slots;
     int prod_off;          // triangular-solve product scratch (kTriMaxItems)
     int dot_off;           // ordered-dot scratch
     int z_off;             // in-place triangular-solve vector (n_p + 1)

@@ -183,7 +183,33 @@ DevTri tri_view(const TriPlan& p, const Hier::TriDev& d) {
     t.stream = d.stream.get();
     return t;
 }
+void upload_blk(const BlkStream& b, Hier::BlkDev& d, cudaStream_t s) {
+    d.stream = dev(b.stream, s);
+    d.table = dev(b.table, s);
+    d.n = b.n;
+    d.n_blocks = b.n_blocks;
+    d.fresh = b.fresh;
+    d.max_unit_bytes = b.max_unit_bytes;
+}
+// Fresh distance F of the block sweeps (blocks whose columns are summed on the
+// critical path).  Developer override: PHI_BLK_FRESH="ilut,gs".
+int blk_fresh(int which) {
+    int f[2] = {1, 2};
+    if (const char* e = std::getenv("PHI_BLK_FRESH")) std::sscanf(e, "%d,%d", &f[0], &f[1]);
+    return std::min(std::max(f[which], 1), kBlkMaxFresh);
+}
 }  // namespace
+
+DevBlk Hier::BlkDev::view() const {
+    DevBlk b{};
+    b.n = n;
+    b.n_blocks = n_blocks;
+    b.fresh = fresh;
+    b.max_unit_bytes = max_unit_bytes;
+    b.stream = stream.get();
+    b.table = reinterpret_cast<const int2*>(table.get());
+    return b;
+}
 
 Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_, cudaStream_t s)
     : disc(std::move(disc_)), c(c_), opt(opt_) {
@@ -195,10 +221,17 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     launch_axpby(d.M.vals.get(), c, d.K.vals.get(), A.vals.get(), A.size(), s);
     const HostCsr ah = stencil_to_csr(A);
     ilut_factor(ah, opt.ilut_tau, opt.ilut_fill, L_host, U_host);
-    Lp = plan_lower(L_host);
-    Up = plan_upper(U_host);
-    upload_tri(Lp, opt.exact == 0, Ld, s);
-    upload_tri(Up, opt.exact == 0, Ud, s);
+    // exact mode: level-scheduled streams (the reference's summation order);
+    // reassociated mode: block recurrences
+    if (opt.exact) {
+        Lp = plan_lower(L_host);
+        Up = plan_upper(U_host);
+        upload_tri(Lp, false, Ld, s);
+        upload_tri(Up, false, Ud, s);
+    } else {
+        upload_blk(blk_lower(L_host, blk_fresh(0)), Lbd, s);
+        upload_blk(blk_upper(U_host, blk_fresh(0)), Ubd, s);
+    }
     for (const auto& hl : d.h) {
         StencilBuf a;
         a.ru = a.rv = a.cu = a.cv = hl.nf;
@@ -213,9 +246,14 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     for (size_t l = 0; l + 1 < a_h.size(); ++l) {
         const HostCsr al = stencil_to_csr(a_h[l]);
         for (int dir = 0; dir < 2; ++dir) {
-            gs_plans.push_back(plan_gauss_seidel(al, dir == 1));
-            gs_dev.emplace_back();
-            upload_tri(gs_plans.back(), opt.exact == 0, gs_dev.back(), s);
+            if (opt.exact) {
+                gs_plans.push_back(plan_gauss_seidel(al, dir == 1));
+                gs_dev.emplace_back();
+                upload_tri(gs_plans.back(), false, gs_dev.back(), s);
+            } else {
+                gsb_dev.emplace_back();
+                upload_blk(blk_gauss_seidel(al, dir == 1, blk_fresh(1)), gsb_dev.back(), s);
+            }
         }
     }
     coarse = dense_lu_factor(stencil_to_csr(a_h.back()));
@@ -238,14 +276,22 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     H.Tt = d.Tt.view();
     H.inv_lp = d.inv_lp.get();
     H.inv_l1 = d.inv_l1.get();
-    H.L = tri_view(Lp, Ld);
-    H.U = tri_view(Up, Ud);
+    if (opt.exact) {
+        H.L = tri_view(Lp, Ld);
+        H.U = tri_view(Up, Ud);
+    } else {
+        H.Lb = Lbd.view();
+        H.Ub = Ubd.view();
+    }
     for (int l = 0; l < H.n_h; ++l) {
         const auto& hl = d.h[l];
         H.h[l].a = a_h[l].view();
-        if (l + 1 < H.n_h) {
+        if (l + 1 < H.n_h && opt.exact) {
             H.h[l].gs_fwd = tri_view(gs_plans[2 * l], gs_dev[2 * l]);
             H.h[l].gs_bwd = tri_view(gs_plans[2 * l + 1], gs_dev[2 * l + 1]);
+        } else if (l + 1 < H.n_h) {
+            H.h[l].gsb_fwd = gsb_dev[2 * l].view();
+            H.h[l].gsb_bwd = gsb_dev[2 * l + 1].view();
         }
         H.h[l].n = hl.n;
         if (l + 1 < H.n_h) {

@@ -105,6 +105,13 @@ public:
     } Ld, Ud;
     std::vector<TriPlan> gs_plans;  // per h-level (but the coarsest): forward, backward
     std::vector<TriDev> gs_dev;
+    struct BlkDev {
+        DevBuf<unsigned char> stream;
+        DevBuf<int> table;
+        int n = 0, n_blocks = 0, fresh = 1, max_unit_bytes = 0;
+        DevBlk view() const;
+    } Lbd, Ubd;
+    std::vector<BlkDev> gsb_dev;  // per h-level (but the coarsest): forward, backward
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;
     DevBuf<int> coarse_piv;

@@ -152,6 +152,7 @@ struct Ws {
     double* z;               // in-place triangular-solve vector (n_p + 1 slots)
     double* dot;             // shared scratch for ordered dots
     int z_off, ring_off, slot_bytes, prod_off;  // g_smem offsets (-1: global)
+    int n_slots, gs_slot_bytes, gs_n_slots;     // block-sweep rings (SmemPlan)
     int lvl_off[kMaxH];  // g_smem offset of level l's vectors (b, x, r), -1: global
     double* hb[kMaxH];
     double* hx[kMaxH];
@@ -171,6 +172,9 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     w.ring_off = P.ring_off;
     w.slot_bytes = P.slot_bytes;
     w.prod_off = P.prod_off;
+    w.n_slots = P.n_slots;
+    w.gs_slot_bytes = P.gs_slot_bytes;
+    w.gs_n_slots = P.gs_n_slots;
     double* g = base + 6 * np;
     for (int l = 0; l < H.n_h; ++l) {
         const int nl = H.h[l].n;
@@ -320,9 +324,15 @@ __device__ __forceinline__ void bulk_fetch(unsigned dst, const void* src, int by
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+#ifndef PHI_SPIN_GUARD
+#define PHI_SPIN_GUARD 1  // bounded spins: report and trap instead of hanging
+#endif
+__device__ __noinline__ void spin_fail(int what, int have, int want);
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     unsigned done;
+    const long long t0 = PHI_SPIN_GUARD ? clock64() : 0;
     do {
+        if (PHI_SPIN_GUARD && clock64() - t0 > 4000000000LL) spin_fail(3, (int)(bar & 0xffff), (int)parity);
         asm volatile(
             "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
@@ -686,12 +696,228 @@ __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int 
     sweep_sync();  // all sweep warps done (the next sweep reuses the ring and mbarriers)
 }
 
+// ---- block-recurrence sweeps (reassociated mode) ---------------------------
+// One sweep (ILUT substitution or Gauss-Seidel) over a BlkStream
+// (setup_host.hpp): blocks of 32 consecutive rows in solve order, block k
+// solved as x_{R_k} = B_k^{-1} (rhs - old - fresh).
+//  * warp 0 (the solver) runs the dependent chain: per block it waits for the
+//    block's "old" sums, subtracts the fresh entries (columns of the last F
+//    blocks, loaded from x now), multiplies by the dense inverse (the 32
+//    right-hand sides broadcast through shared memory) and stores the 32 new
+//    values;
+//  * warps 1..7 (the workers) take the blocks in turn: once block k-F-1 is
+//    done they sum the block's old entries and hand c = rhs - old over.
+// The blocks stream through a shared-memory ring of n_slots units filled by
+// TMA bulk copies; the solver refills the slot of block k (with block k +
+// n_slots) once block k is done -- its worker finished earlier.  Hand-offs
+// are release/acquire flags in shared memory: `prog` (last block done) and
+// flag[k % kBlkHand] = k (old sums of block k ready).
+__device__ __forceinline__ void st_release_s32(unsigned a, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_s32(unsigned a) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __noinline__ void spin_fail(int what, int have, int want) {
+    printf("phi spin guard: block %d thread %d wait %d have %d want %d\n", blockIdx.x, threadIdx.x, what, have, want);
+    __trap();
+}
+__device__ __forceinline__ void wait_ge(unsigned a, int v) {
+    const long long t0 = PHI_SPIN_GUARD ? clock64() : 0;
+    int h;
+    while ((h = ld_acquire_s32(a)) < v)
+        if (PHI_SPIN_GUARD && clock64() - t0 > 4000000000LL) spin_fail(1, h, v);
+}
+__device__ __forceinline__ void wait_eq(unsigned a, int v) {
+    const long long t0 = PHI_SPIN_GUARD ? clock64() : 0;
+    int h;
+    while ((h = ld_acquire_s32(a)) != v)
+        if (PHI_SPIN_GUARD && clock64() - t0 > 4000000000LL) spin_fail(2, h, v);
+}
+// x[j]: shared (XSM: byte address base + 8 j) or global
+template <bool XSM>
+__device__ __forceinline__ double xld(const double* xg, unsigned xs, int j) {
+    if constexpr (XSM)
+        return vlds_f64(xs + 8u * j);
+    else
+        return xg[j];
+}
+template <bool XSM>
+__device__ __forceinline__ void xst(double* xg, unsigned xs, int j, double v) {
+    if constexpr (XSM)
+        asm volatile("st.shared.f64 [%0], %1;" ::"r"(xs + 8u * j), "d"(v) : "memory");
+    else
+        xg[j] = v;
+}
+// sum over `m` slots (batches of 4) of vals[q][lane] * x[cols[q][lane]]
+template <bool XSM>
+__device__ __forceinline__ double slot_sum(unsigned cp, unsigned vp, int m, const double* xg, unsigned xs) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int q0 = 0; q0 < m; q0 += 4) {
+        int j[4];
+        double v[4], xj[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            j[q] = vlds_s32(cp + 128u * (q0 + q));
+            v[q] = vlds_f64(vp + 256u * (q0 + q));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xj[q] = xld<XSM>(xg, xs, j[q]);
+        a0 = __fma_rn(v[0], xj[0], a0);
+        a1 = __fma_rn(v[1], xj[1], a1);
+        a0 = __fma_rn(v[2], xj[2], a0);
+        a1 = __fma_rn(v[3], xj[3], a1);
+    }
+    return a0 + a1;
+}
+
+struct __align__(16) BlkSync {
+    double cbuf[kBlkHand * 32];
+    double tb[32];  // 16-byte aligned: read as v2 broadcasts
+    unsigned long long bar[kBlkMaxSlots];
+    int phase[kBlkMaxSlots];  // phases completed per slot since the kernel started
+    int prog;
+    int flag[kBlkHand];
+};
+// One per CTA.  The ring's mbarriers are initialised once per kernel
+// (blk_init) and never re-initialised: every sweep continues their phase
+// sequence from `phase`.
+__shared__ BlkSync g_blk;
+
+__device__ __forceinline__ void blk_init() {
+    if (threadIdx.x == 0) {
+        const unsigned bar = sh_addr(g_blk.bar);
+        for (int k = 0; k < kBlkMaxSlots; ++k) {
+            mbar_init(bar + 8u * k);
+            g_blk.phase[k] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // the callers' next __syncthreads() publishes the initialisation
+}
+
+template <bool XSM, bool RSM>
+__device__ __noinline__ void blk_sweep_t(const DevBlk& T, double* xg, int x_off, const double* rg, int r_off,
+                                         int ring_off, int slot_bytes, int n_slots, BlkSync& sy) {
+    // parity of unit k: (phases slot k % n_slots completed before this sweep
+    // + k / n_slots) & 1
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nb = T.n_blocks, F = T.fresh;
+    const unsigned ring = sh_addr(g_smem + ring_off);
+    const unsigned bar = sh_addr(sy.bar);
+    const unsigned xs = XSM ? sh_addr(g_smem + x_off) : 0u;
+    const unsigned rs = RSM ? sh_addr(g_smem + r_off) : 0u;
+    const unsigned prog = sh_addr(&sy.prog), flag = sh_addr(sy.flag), cbuf = sh_addr(sy.cbuf), tb = sh_addr(sy.tb);
+    const unsigned char* __restrict__ stream = T.stream;
+    const int2* __restrict__ table = T.table;
+    if (w == 0) {
+        // ---- the solver warp
+        int2 nxt = make_int2(0, 0);
+        if (lane == 0 && n_slots < nb) nxt = __ldg(table + n_slots);
+        for (int k = 0; k < nb; ++k) {
+            const int slot = k % n_slots;
+            mbar_wait(bar + 8u * slot, (unsigned)(sy.phase[slot] + k / n_slots) & 1u);
+            const unsigned u = ring + slot * slot_bytes;
+            int mo, mf, bytes, pad;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(mo), "=r"(mf), "=r"(bytes), "=r"(pad) : "r"(u));
+            (void)bytes;
+            (void)pad;
+            const int row = vlds_s32(u + 16u + 4u * lane);
+            const unsigned fc = u + 144u + 384u * mo, fv = fc + 128u * mf, iv = fv + 256u * mf;
+            double inv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                inv[j] = lane >= j ? vlds_f64(iv + 8u * (32 * j - j * (j - 1) / 2 + lane - j)) : 0.0;
+            wait_eq(flag + 4u * (k % kBlkHand), k);
+            double t = vlds_f64(cbuf + 8u * ((k % kBlkHand) * 32 + lane));
+            if (mf > 0) t = t - slot_sum<XSM>(fc + 4u * lane, fv + 8u * lane, mf, xg, xs);
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(t) : "memory");
+            __syncwarp();
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+                double t0, t1;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(t0), "=d"(t1) : "r"(tb + 8u * j));
+                acc[(j >> 1) & 3] = __fma_rn(inv[j], t0, acc[(j >> 1) & 3]);
+                acc[(j >> 1) & 3] = __fma_rn(inv[j + 1], t1, acc[(j >> 1) & 3]);
+            }
+            const double z = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            if (row >= 0) xst<XSM>(xg, xs, row, z);
+            __syncwarp();
+            if (lane == 0) {
+                st_release_s32(prog, k);
+                // block k's unit is consumed by both warps: refill its slot
+                if (k + n_slots < nb) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    bulk_fetch(u, stream + (size_t)nxt.x * 16, nxt.y, bar + 8u * slot);
+                    if (k + 1 + n_slots < nb) nxt = __ldg(table + k + 1 + n_slots);
+                }
+            }
+        }
+    } else {
+        // ---- worker warps: old sums of blocks w-1, w-1+7, ...
+        for (int k = w - 1; k < nb; k += NW - 1) {
+            // block k-F-1 done: the old columns are final, and unit k is in
+            // flight (issued when block k - n_slots was done, n_slots >= F + 2)
+            wait_ge(prog, k - F - 1);
+            const int slot = k % n_slots;
+            mbar_wait(bar + 8u * slot, (unsigned)(sy.phase[slot] + k / n_slots) & 1u);
+            const unsigned u = ring + slot * slot_bytes;
+            const int mo = vlds_s32(u);
+            const int row = vlds_s32(u + 16u + 4u * lane);
+            const double s = mo > 0 ? slot_sum<XSM>(u + 144u + 4u * lane, u + 144u + 128u * mo + 8u * lane, mo, xg, xs) : 0.0;
+            double r = 0.0;
+            if (row >= 0) r = RSM ? vlds_f64(rs + 8u * row) : rg[row];
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(cbuf + 8u * ((k % kBlkHand) * 32 + lane)), "d"(r - s) : "memory");
+            __syncwarp();
+            if (lane == 0) st_release_s32(flag + 4u * (k % kBlkHand), k);
+        }
+    }
+}
+
+// One block sweep: prime, the solver / worker split, closing barrier, phase
+// bookkeeping.  Called by the whole CTA (blk_init ran at kernel start).
+__device__ __forceinline__ void blk_sweep(const DevBlk& T, double* xg, int x_off, const double* rg, int r_off,
+                                          int ring_off, int slot_bytes, int n_slots) {
+    BlkSync& sy = g_blk;
+    const int nb = T.n_blocks;
+    if (nb == 0) return;
+    // the ring overlays buffers written through the generic proxy in other
+    // phases: order those writes before the TMA (async-proxy) writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned bar = sh_addr(sy.bar);
+        sy.prog = -1;
+        for (int k = 0; k < kBlkHand; ++k) sy.flag[k] = -1;
+        const unsigned ring = sh_addr(g_smem + ring_off);
+        for (int k = 0; k < n_slots && k < nb; ++k) {
+            const int2 e = __ldg(T.table + k);
+            bulk_fetch(ring + k * slot_bytes, T.stream + (size_t)e.x * 16, e.y, bar + 8u * k);
+        }
+    }
+    __syncthreads();
+    if (x_off >= 0 && r_off >= 0)
+        blk_sweep_t<true, true>(T, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots, sy);
+    else if (x_off >= 0)
+        blk_sweep_t<true, false>(T, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots, sy);
+    else
+        blk_sweep_t<false, false>(T, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots, sy);
+    __syncthreads();
+    if (threadIdx.x == 0)  // units delivered per slot this sweep
+        for (int k = 0; k < n_slots; ++k) sy.phase[k] += k < nb ? (nb - 1 - k) / n_slots + 1 : 0;
+    // published by the next sweep's (or phase's) __syncthreads()
+}
+
 // Both substitutions of one ILUT application; warp 0 solves, the CTA joins at
 // the closing barrier.  The ring's mbarriers are (re)initialised per call so
 // their phase parity starts at 0.
 __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, double* zg, int z_off, double* xadd,
                                            int ring_off, int slot_bytes, int prod_off, bool exact) {
     __shared__ unsigned long long bars[2 * kTriSlots];
+    if (!exact) __trap();  // the reassociated mode runs ilut_solve_blk
     // the ring overlays buffers written through the generic proxy in other
     // phases: order those writes before the TMA (async-proxy) writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -716,6 +942,18 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
     __syncthreads();
     // the smoother update x += z (axpy(1, z, x), pmultigrid.hpp:315), off the
     // substitution's critical path
+    if (xadd) {
+        const double* z = z_off >= 0 ? g_smem + z_off : zg;
+        for (int i = threadIdx.x; i < L.n; i += NT) xadd[i] = xadd[i] + z[i];
+        __syncthreads();
+    }
+}
+
+// Reassociated mode: both substitutions as block recurrences, then x += z.
+__device__ __forceinline__ void ilut_solve_blk(const DevBlk& L, const DevBlk& U, double* zg, int z_off, double* xadd,
+                                               const Ws& w) {
+    blk_sweep(L, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
+    blk_sweep(U, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
     if (xadd) {
         const double* z = z_off >= 0 ? g_smem + z_off : zg;
         for (int i = threadIdx.x; i < L.n; i += NT) xadd[i] = xadd[i] + z[i];
@@ -861,7 +1099,10 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         double* x = w.hx[l];
         const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + lv.n : -1;
         if (phase[l] == 0) {
-            gs_sweeps(lv, b, x, false, H.gs_pre, H.exact != 0, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+            if (H.exact)
+                gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+            else
+                for (int c = 0; c < H.gs_pre; ++c) blk_sweep(lv.gsb_fwd, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
             stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b, H.exact != 0);
             __syncthreads();
             csr_apply<false>(lv.embed_t, w.hr[l], w.hb[l + 1]);  // rc = E^T r
@@ -875,7 +1116,10 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         } else {
             csr_apply<true>(lv.embed, w.hx[l + 1], x);  // x += E ec
             __syncthreads();
-            gs_sweeps(lv, b, x, true, H.gs_post, H.exact != 0, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+            if (H.exact)
+                gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+            else
+                for (int c = 0; c < H.gs_post; ++c) blk_sweep(lv.gsb_bwd, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
             if (l == 0) break;
             --l;
         }
@@ -890,7 +1134,10 @@ __device__ __noinline__ void smooth(const DevHier& H, const Ws& w) {
     if (threadIdx.x == 0) w.z[H.n_p] = 0.0;                          // neutral padding slot
     __syncthreads();
     pstamp(11);
-    ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, H.exact != 0);
+    if (H.exact)
+        ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, true);
+    else
+        ilut_solve_blk(H.Lb, H.Ub, w.z, w.z_off, w.x, w);
     pstamp(12);
 }
 
@@ -1055,6 +1302,7 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ WaveArgs a_sh;
     if (threadIdx.x == 0) a_sh = a_param;
     const WaveArgs& a = a_sh;
+    blk_init();
     const DevHier& H = hier_shared(H_param);
     const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
     for (int task = blockIdx.x; task < a.n_tasks; task += gridDim.x) {
@@ -1071,6 +1319,7 @@ __global__ void __launch_bounds__(NT, 1)
     vcycle_kernel(const __grid_constant__ DevHier H_param, const double* B, long long ldb, double* X, long long ldx,
                   int nrhs, const __grid_constant__ SmemPlan P, double* ws_base, long long ws_stride) {
     double* smem = g_smem;
+    blk_init();
     const DevHier& H = hier_shared(H_param);
     const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
     const int n = H.n_p;
@@ -1093,6 +1342,7 @@ __global__ void __launch_bounds__(NT, 1)
     unit_kernel(const __grid_constant__ DevHier H_param, int op, int arg, int arg2, const double* in, double* out,
                 const __grid_constant__ SmemPlan P, double* ws_base, long long ws_stride) {
     double* smem = g_smem;
+    blk_init();
     const DevHier& H = hier_shared(H_param);
     const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
     const int n = H.n_p;
@@ -1103,7 +1353,10 @@ __global__ void __launch_bounds__(NT, 1)
         cta_fill(w.x, 0.0, n);
         if (threadIdx.x == 0) w.z[n] = 0.0;
         __syncthreads();
-        ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, H.exact != 0);
+        if (H.exact)
+            ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, true);
+        else
+            ilut_solve_blk(H.Lb, H.Ub, w.z, w.z_off, w.x, w);
         cta_copy(out, w.z, n);
     } else if (op == 2) {
         stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, in, out, H.inv_l1, H.exact != 0);
@@ -1123,7 +1376,11 @@ __global__ void __launch_bounds__(NT, 1)
         if (threadIdx.x == 0) w.hx[arg][lv.n] = 0.0;  // neutral slot of padded sweep entries
         __syncthreads();
         const int bo = w.lvl_off[arg], xo = bo >= 0 ? bo + lv.n : -1;
-        gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, H.exact != 0, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+        if (H.exact)
+            gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+        else
+            blk_sweep(arg2 ? lv.gsb_bwd : lv.gsb_fwd, w.hx[arg], xo, w.hb[arg], bo, w.ring_off, w.gs_slot_bytes,
+                      w.gs_n_slots);
         cta_copy(out, w.hx[arg], lv.n);
     }
 }

@@ -74,33 +74,61 @@ size_t phi_ws_doubles(const DevHier& H) {
 
 SmemPlan phi_smem_plan(const DevHier& H) {
     // Shared memory of one Phi CTA, by V-cycle phase:
-    //   [0, tri)        TMA ring of the level-scheduled sweeps (ILUT factors
-    //                   and Gauss-Seidel) + the exact mode's product scratch;
-    //                   the ordered-dot scratch overlays it (norm phases)
+    //   [0, tri)        TMA ring of the sweeps (ILUT factors and Gauss-Seidel)
+    //                   + the exact mode's product scratch; the ordered-dot
+    //                   scratch overlays it (norm phases)
     //   [tri, total)    the ILUT dependency vector z (smoothing) overlaid by
     //                   the order-1 h-level vectors b, x, r (W-cycle)
+    // Block sweeps (reassociated mode) size the ring per phase: the smoothing
+    // ring holds ILUT blocks in front of z, the W-cycle ring the (smaller)
+    // Gauss-Seidel blocks in front of the h-level vectors.
     SmemPlan P{};
     const size_t budget = kPhiSmemBudgetBytes / 8;  // doubles
     P.ring_off = 0;
     P.dot_off = 0;
-    int slot = std::max(H.L.max_unit_bytes, H.U.max_unit_bytes);
-    for (int l = 0; l + 1 < H.n_h; ++l)
-        slot = std::max(slot, std::max(H.h[l].gs_fwd.max_unit_bytes, H.h[l].gs_bwd.max_unit_bytes));
-    P.slot_bytes = (slot + 127) / 128 * 128;
-    size_t tri = (size_t)kTriSlots * P.slot_bytes / 8;
-    P.prod_off = (int)tri;
-    tri += kTriMaxItems;
-    if (tri * 8 > kPhiSmemBudgetBytes) throw InvalidArgument("triangular-factor blocks exceed shared memory");
-    size_t top = tri;
+    for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
+    size_t tri, gs_tri;
+    if (H.exact) {
+        int slot = std::max(H.L.max_unit_bytes, H.U.max_unit_bytes);
+        for (int l = 0; l + 1 < H.n_h; ++l)
+            slot = std::max(slot, std::max(H.h[l].gs_fwd.max_unit_bytes, H.h[l].gs_bwd.max_unit_bytes));
+        P.slot_bytes = P.gs_slot_bytes = (slot + 127) / 128 * 128;
+        P.n_slots = P.gs_n_slots = kTriSlots;
+        tri = (size_t)kTriSlots * P.slot_bytes / 8;
+        P.prod_off = (int)tri;
+        tri += kTriMaxItems;
+        gs_tri = tri;
+        if (tri * 8 > kPhiSmemBudgetBytes) throw InvalidArgument("triangular-factor blocks exceed shared memory");
+    } else {
+        P.prod_off = -1;
+        const int slot = std::max(H.Lb.max_unit_bytes, H.Ub.max_unit_bytes);
+        int gslot = 16;
+        for (int l = 0; l + 1 < H.n_h; ++l)
+            gslot = std::max(gslot, std::max(H.h[l].gsb_fwd.max_unit_bytes, H.h[l].gsb_bwd.max_unit_bytes));
+        P.slot_bytes = (slot + 127) / 128 * 128;
+        P.gs_slot_bytes = (gslot + 127) / 128 * 128;
+        const int min_slots = std::max(H.Lb.fresh, H.Ub.fresh) + 2;
+        // the ILUT ring leaves room for z when it can
+        const size_t zb = ((size_t)H.n_p + 2) * 8;
+        int ns = (int)std::min<size_t>(kBlkMaxSlots, (kPhiSmemBudgetBytes - std::min(zb, kPhiSmemBudgetBytes)) / P.slot_bytes);
+        if (ns < min_slots) ns = (int)std::min<size_t>(kBlkMaxSlots, kPhiSmemBudgetBytes / P.slot_bytes);
+        if (ns < min_slots) throw InvalidArgument("triangular-factor blocks exceed shared memory");
+        P.n_slots = ns;
+        tri = (size_t)ns * P.slot_bytes / 8;
+        int gfresh = 1;
+        for (int l = 0; l + 1 < H.n_h; ++l) gfresh = std::max(gfresh, std::max(H.h[l].gsb_fwd.fresh, H.h[l].gsb_bwd.fresh));
+        P.gs_n_slots = std::max(gfresh + 2, std::min(kBlkMaxSlots, 6));
+        gs_tri = (size_t)P.gs_n_slots * P.gs_slot_bytes / 8;
+    }
+    size_t top = std::max(tri, gs_tri);
     if (tri + (size_t)H.n_p + 2 <= budget) {
         P.z_off = (int)tri;
         top = std::max(top, tri + H.n_p + 2);
     } else {
         P.z_off = -1;
     }
-    for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
     // coarsest levels first: they are visited most often by the W-cycle
-    size_t lv = tri;
+    size_t lv = gs_tri;
     for (int l = H.n_h - 1; l >= 0; --l) {
         const size_t need = 3 * (size_t)H.h[l].n + 1;
         if (lv + need <= budget) {
@@ -111,8 +139,8 @@ SmemPlan phi_smem_plan(const DevHier& H) {
     top = std::max(top, lv);
     P.total = (int)std::max(top, (size_t)kDotChunk);
     if (std::getenv("PHI_PLAN_DEBUG"))
-        std::fprintf(stderr, "smem plan: slot %d B x %d, prod @%d, z @%d, levels @%d.., total %d doubles\n",
-                     P.slot_bytes, kTriSlots, P.prod_off, P.z_off, P.lvl_off[0], P.total);
+        std::fprintf(stderr, "smem plan: slot %d B x %d, gs slot %d B x %d, prod @%d, z @%d, levels @%d.., total %d doubles\n",
+                     P.slot_bytes, P.n_slots, P.gs_slot_bytes, P.gs_n_slots, P.prod_off, P.z_off, P.lvl_off[0], P.total);
     return P;
 }
 

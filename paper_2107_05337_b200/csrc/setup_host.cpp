@@ -732,4 +732,152 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
     return ts;
 }
 
+
+// ---------------------------------------------------------------------------
+// Block-recurrence sweeps (setup_host.hpp BlkStream)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct BlkRowsView {
+    int n = 0;
+    bool descending = false;
+    // off-diagonal entries of row i and its diagonal (1 for a unit factor)
+    std::function<void(int, std::vector<int>&, std::vector<double>&)> entries;
+    std::function<double(int)> diag;
+};
+
+BlkStream make_blk_stream(const BlkRowsView& rv, int fresh) {
+    const int n = rv.n;
+    BlkStream bs;
+    bs.n = n;
+    bs.fresh = fresh;
+    bs.n_blocks = (n + kBlkRows - 1) / kBlkRows;
+    auto pos_of = [&](int i) { return rv.descending ? n - 1 - i : i; };
+    auto row_at = [&](int pos) { return rv.descending ? n - 1 - pos : pos; };
+    std::vector<int> cols;
+    std::vector<double> vals;
+    std::vector<std::vector<unsigned char>> units(bs.n_blocks);
+    for (int k = 0; k < bs.n_blocks; ++k) {
+        long double B[kBlkRows][kBlkRows] = {};
+        std::vector<std::pair<int, double>> olde[kBlkRows], frsh[kBlkRows];
+        int rows[kBlkRows];
+        size_t mo = 0, mf = 0;
+        for (int l = 0; l < kBlkRows; ++l) {
+            const int pos = k * kBlkRows + l;
+            if (pos >= n) {
+                rows[l] = -1;
+                B[l][l] = 1.0L;
+                continue;
+            }
+            const int i = row_at(pos);
+            rows[l] = i;
+            B[l][l] = rv.diag(i);
+            rv.entries(i, cols, vals);
+            for (size_t e = 0; e < cols.size(); ++e) {
+                const int pj = pos_of(cols[e]), kj = pj / kBlkRows;
+                if (pj < pos && kj == k)
+                    B[l][pj - k * kBlkRows] += vals[e];
+                else if (pj < pos && kj >= k - fresh)
+                    frsh[l].emplace_back(cols[e], vals[e]);
+                else
+                    olde[l].emplace_back(cols[e], vals[e]);
+            }
+            mo = std::max(mo, olde[l].size());
+            mf = std::max(mf, frsh[l].size());
+        }
+        mo = (mo + 3) / 4 * 4;  // whole batches of 4 slots
+        mf = (mf + 3) / 4 * 4;
+        // dense inverse of the lower-triangular block, column by column
+        long double inv[kBlkRows][kBlkRows] = {};
+        for (int j = 0; j < kBlkRows; ++j)
+            for (int l = j; l < kBlkRows; ++l) {
+                long double s = l == j ? 1.0L : 0.0L;
+                for (int m = j; m < l; ++m) s -= B[l][m] * inv[m][j];
+                inv[l][j] = s / B[l][l];
+            }
+        const size_t bytes = 16 + 4 * kBlkRows + 12 * kBlkRows * (mo + mf) + 8 * kBlkInv;
+        std::vector<unsigned char> img(bytes, 0);
+        const int hdr[4] = {static_cast<int>(mo), static_cast<int>(mf), static_cast<int>(bytes), 0};
+        std::memcpy(img.data(), hdr, sizeof hdr);
+        std::memcpy(img.data() + 16, rows, sizeof rows);
+        int* oc = reinterpret_cast<int*>(img.data() + 16 + 4 * kBlkRows);
+        double* ov = reinterpret_cast<double*>(oc + kBlkRows * mo);
+        int* fc = reinterpret_cast<int*>(ov + kBlkRows * mo);
+        double* fv = reinterpret_cast<double*>(fc + kBlkRows * mf);
+        double* iv = fv + kBlkRows * mf;
+        for (size_t s = 0; s < kBlkRows * mo; ++s) oc[s] = n;  // neutral padding (x[n] = +0.0)
+        for (size_t s = 0; s < kBlkRows * mf; ++s) fc[s] = n;
+        for (int l = 0; l < kBlkRows; ++l) {
+            for (size_t e = 0; e < olde[l].size(); ++e) {
+                oc[e * kBlkRows + l] = olde[l][e].first;
+                ov[e * kBlkRows + l] = olde[l][e].second;
+            }
+            for (size_t e = 0; e < frsh[l].size(); ++e) {
+                fc[e * kBlkRows + l] = frsh[l][e].first;
+                fv[e * kBlkRows + l] = frsh[l][e].second;
+            }
+        }
+        for (int j = 0; j < kBlkRows; ++j)
+            for (int l = j; l < kBlkRows; ++l)
+                iv[kBlkRows * j - j * (j - 1) / 2 + (l - j)] = static_cast<double>(inv[l][j]);
+        units[k] = std::move(img);
+    }
+    size_t total = 0;
+    for (const auto& u : units) {
+        bs.table.push_back(static_cast<int>(total / 16));
+        bs.table.push_back(static_cast<int>(u.size()));
+        bs.max_unit_bytes = std::max(bs.max_unit_bytes, static_cast<int>(u.size()));
+        total += u.size();
+    }
+    bs.stream.reserve(total);
+    for (const auto& u : units) bs.stream.insert(bs.stream.end(), u.begin(), u.end());
+    return bs;
+}
+
+}  // namespace
+
+BlkStream blk_lower(const HostCsr& m, int fresh) {
+    BlkRowsView rv;
+    rv.n = m.n_rows;
+    rv.entries = [&m](int i, std::vector<int>& c, std::vector<double>& v) {
+        c.assign(m.col_indices.begin() + m.row_offsets[i], m.col_indices.begin() + m.row_offsets[i + 1]);
+        v.assign(m.values.begin() + m.row_offsets[i], m.values.begin() + m.row_offsets[i + 1]);
+    };
+    rv.diag = [](int) { return 1.0; };
+    return make_blk_stream(rv, fresh);
+}
+
+BlkStream blk_upper(const HostCsr& m, int fresh) {
+    BlkRowsView rv;
+    rv.n = m.n_rows;
+    rv.descending = true;
+    rv.entries = [&m](int i, std::vector<int>& c, std::vector<double>& v) {
+        c.assign(m.col_indices.begin() + m.row_offsets[i] + 1, m.col_indices.begin() + m.row_offsets[i + 1]);
+        v.assign(m.values.begin() + m.row_offsets[i] + 1, m.values.begin() + m.row_offsets[i + 1]);
+    };
+    rv.diag = [&m](int i) { return m.values[m.row_offsets[i]]; };
+    return make_blk_stream(rv, fresh);
+}
+
+BlkStream blk_gauss_seidel(const HostCsr& a, bool backward, int fresh) {
+    BlkRowsView rv;
+    rv.n = a.n_rows;
+    rv.descending = backward;
+    rv.entries = [&a](int i, std::vector<int>& c, std::vector<double>& v) {
+        c.clear();
+        v.clear();
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e)
+            if (a.col_indices[e] != i) {
+                c.push_back(a.col_indices[e]);
+                v.push_back(a.values[e]);
+            }
+    };
+    rv.diag = [&a](int i) {
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e)
+            if (a.col_indices[e] == i) return a.values[e];
+        throw std::runtime_error("gauss_seidel_sweep: zero diagonal entry");
+    };
+    return make_blk_stream(rv, fresh);
+}
+
 }  // namespace phi

@@ -120,4 +120,41 @@ struct TriStream {
 };
 TriStream make_tri_stream(const TriPlan& p, bool fast);
 
+/// Block-recurrence schedule of a sweep (reassociated mode only).  The rows
+/// are taken in solve order in blocks of kBlkRows = 32 consecutive rows, one
+/// per lane.  For block k with rows R_k the sweep
+///     x_i = (rhs_i - sum_{j before i} a_ij x_j(new) - sum_{j after i} a_ij x_j(old)) / d_i
+/// (d_i = 1 for the unit lower ILUT factor) is
+///     x_{R_k} = B_k^{-1} (rhs - old - fresh),   B_k = D + (in-block lower part),
+/// with the dense inverse B_k^{-1} precomputed here.  Entries of a row are
+///   in-block lower  -> folded into B_k;
+///   fresh           -> columns solved by blocks k-F .. k-1 (summed on the
+///                      critical path after block k-1);
+///   old             -> columns solved by blocks <= k-F-1 (final once block
+///                      k-F-1 is done) or solved later (Gauss-Seidel's old
+///                      values, in-block ones included); summed ahead of time
+///                      by a worker warp.
+/// One block = one fetch unit (one cp.async.bulk):
+///   header int32[4]: mo, mf, bytes, 0
+///   rows   int32[32]          at 16 (-1 on padding lanes)
+///   old    cols int32[mo][32], vals double[mo][32]  (slot q of lane L at q*32+L)
+///   fresh  cols int32[mf][32], vals double[mf][32]
+///   inv    double[528]: B_k^{-1} packed by columns, entry (L, j), L >= j, at
+///          32 j - j (j - 1) / 2 + (L - j)
+/// Padding slots are (column n, +0.0) against the zero slot x[n].  `table`
+/// holds (offset / 16, bytes) per block.
+constexpr int kBlkRows = 32;
+constexpr int kBlkInv = kBlkRows * (kBlkRows + 1) / 2;
+struct BlkStream {
+    std::vector<unsigned char> stream;
+    std::vector<int> table;  // 2 per block
+    int n = 0, n_blocks = 0, fresh = 1, max_unit_bytes = 0;
+};
+/// Unit lower ILUT factor (strictly lower entries stored), ascending.
+BlkStream blk_lower(const HostCsr& lower, int fresh);
+/// Upper ILUT factor (diagonal first in each row), descending.
+BlkStream blk_upper(const HostCsr& upper, int fresh);
+/// Lexicographic Gauss-Seidel sweep on A (solvers.hpp:80-99).
+BlkStream blk_gauss_seidel(const HostCsr& a, bool backward, int fresh);
+
 }  // namespace phi

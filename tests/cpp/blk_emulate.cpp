@@ -1,0 +1,130 @@
+// Host-side check of the block-recurrence sweep schedules (setup_host.hpp
+// BlkStream): the stream images are decoded and executed block by block on the
+// CPU, in the order the device runs them (old sums, fresh sums, dense block
+// inverse), and compared with the plain sequential sweeps of the reference
+// (ilut.hpp:146-163 substitutions, solvers.hpp:80-99 Gauss-Seidel).
+// Test infrastructure only (tests/test_blk_schedule.py builds and runs it).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "setup_host.hpp"
+
+using namespace phi;
+
+// 2D tensor stencil of half-width w on an m x m grid (the IgA pattern),
+// diagonally weighted so ILUT and Gauss-Seidel are well defined.
+static HostCsr stencil_matrix(int m, int w, unsigned seed) {
+    std::mt19937 g(seed);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    HostCsr a;
+    a.n_rows = a.n_cols = m * m;  // row_offsets starts as {0}
+    for (int iv = 0; iv < m; ++iv)
+        for (int iu = 0; iu < m; ++iu) {
+            for (int dv = -w; dv <= w; ++dv)
+                for (int du = -w; du <= w; ++du) {
+                    const int jv = iv + dv, ju = iu + du;
+                    if (jv < 0 || jv >= m || ju < 0 || ju >= m) continue;
+                    a.col_indices.push_back(jv * m + ju);
+                    a.values.push_back(dv == 0 && du == 0 ? 4.0 * (2 * w + 1) * (2 * w + 1) : u(g));
+                }
+            a.row_offsets.push_back(static_cast<int>(a.col_indices.size()));
+        }
+    return a;
+}
+
+// Execute a BlkStream sweep on x (rhs: separate vector, or x itself).
+static void run_blk(const BlkStream& bs, std::vector<double>& x, const std::vector<double>& rhs) {
+    const int n = bs.n;
+    x.resize(n + 1);
+    x[n] = 0.0;
+    for (int k = 0; k < bs.n_blocks; ++k) {
+        const unsigned char* u = bs.stream.data() + static_cast<size_t>(bs.table[2 * k]) * 16;
+        int hdr[4];
+        std::memcpy(hdr, u, sizeof hdr);
+        const int mo = hdr[0], mf = hdr[1];
+        if (hdr[2] != bs.table[2 * k + 1]) throw std::runtime_error("unit size mismatch");
+        const int* rows = reinterpret_cast<const int*>(u + 16);
+        const int* oc = reinterpret_cast<const int*>(u + 144);
+        const double* ov = reinterpret_cast<const double*>(u + 144 + 128 * mo);
+        const int* fc = reinterpret_cast<const int*>(u + 144 + 384 * mo);
+        const double* fv = reinterpret_cast<const double*>(u + 144 + 384 * mo + 128 * mf);
+        const double* iv = reinterpret_cast<const double*>(u + 144 + 384 * (mo + mf));
+        double t[32], z[32];
+        for (int l = 0; l < 32; ++l) {  // old sums (final or not-yet-updated columns)
+            double s = 0.0;
+            for (int q = 0; q < mo; ++q) s += ov[q * 32 + l] * x[oc[q * 32 + l]];
+            t[l] = (rows[l] >= 0 ? rhs[rows[l]] : 0.0) - s;
+        }
+        for (int l = 0; l < 32; ++l)  // fresh sums
+            for (int q = 0; q < mf; ++q) t[l] -= fv[q * 32 + l] * x[fc[q * 32 + l]];
+        for (int l = 0; l < 32; ++l) {
+            z[l] = 0.0;
+            for (int j = 0; j <= l; ++j) z[l] += iv[32 * j - j * (j - 1) / 2 + (l - j)] * t[j];
+        }
+        for (int l = 0; l < 32; ++l)
+            if (rows[l] >= 0) x[rows[l]] = z[l];
+    }
+    x.resize(n);
+}
+
+static double rel(const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+    }
+    return std::sqrt(num / den);
+}
+
+int main(int argc, char** argv) {
+    const int m = argc > 1 ? std::atoi(argv[1]) : 40, w = argc > 2 ? std::atoi(argv[2]) : 3;
+    const int fresh = argc > 3 ? std::atoi(argv[3]) : 1;
+    const HostCsr a = stencil_matrix(m, w, 7);
+    const int n = a.n_rows;
+    HostCsr L, U;
+    ilut_factor(a, 1e-13, 0, L, U);
+    std::mt19937 g(3);
+    std::normal_distribution<double> nd;
+    std::vector<double> r(n);
+    for (auto& v : r) v = nd(g);
+    // reference: forward then backward substitution (ilut.hpp:150-162)
+    std::vector<double> z = r;
+    for (int i = 0; i < n; ++i)
+        for (int e = L.row_offsets[i]; e < L.row_offsets[i + 1]; ++e) z[i] -= L.values[e] * z[L.col_indices[e]];
+    for (int i = n - 1; i >= 0; --i) {
+        double s = z[i];
+        for (int e = U.row_offsets[i] + 1; e < U.row_offsets[i + 1]; ++e) s -= U.values[e] * z[U.col_indices[e]];
+        z[i] = s / U.values[U.row_offsets[i]];
+    }
+    std::vector<double> y = r;
+    run_blk(blk_lower(L, fresh), y, r);
+    const std::vector<double> y1 = y;
+    run_blk(blk_upper(U, fresh), y, y1);
+    const double e_ilut = rel(y, z);
+    // Gauss-Seidel forward and backward (solvers.hpp:80-99)
+    double e_gs[2];
+    for (int dir = 0; dir < 2; ++dir) {
+        std::vector<double> x0(n), xr, xb;
+        for (auto& v : x0) v = nd(g);
+        xr = x0;
+        for (int s = 0; s < n; ++s) {
+            const int i = dir ? n - 1 - s : s;
+            double acc = r[i], d = 0.0;
+            for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) {
+                if (a.col_indices[e] == i)
+                    d = a.values[e];
+                else
+                    acc -= a.values[e] * xr[a.col_indices[e]];
+            }
+            xr[i] = acc / d;
+        }
+        xb = x0;
+        run_blk(blk_gauss_seidel(a, dir == 1, fresh), xb, r);
+        e_gs[dir] = rel(xb, xr);
+    }
+    std::printf("n %d ilut %.3e gs_fwd %.3e gs_bwd %.3e\n", n, e_ilut, e_gs[0], e_gs[1]);
+    return (e_ilut < 1e-12 && e_gs[0] < 1e-12 && e_gs[1] < 1e-12) ? 0 : 1;
+}
