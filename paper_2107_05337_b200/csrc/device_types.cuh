@@ -30,11 +30,10 @@ struct DevCsr {
 
 /// Depth of the shared-memory ring that stages triangular-factor blocks.
 constexpr int kTriSlots = 8;
-/// Block sweeps: maximum ring depth, maximum fresh distance F and the depth of
-/// the worker -> solver hand-off ring (>= F + 1).
+/// Block sweeps: maximum ring depth and the depth of the worker -> solver
+/// hand-off ring.
 constexpr int kBlkMaxSlots = 8;
-constexpr int kBlkMaxFresh = 4;
-constexpr int kBlkHand = 8;
+constexpr int kBlkHand = 4;
 /// Warps that take turns on the blocks of a fast (reassociated) sweep.
 constexpr int kSweepWarps = 6;
 /// Bytes per triangular-factor block (TriPlan chunking) and the product
@@ -54,9 +53,9 @@ struct DevTri {
 /// Block-recurrence sweep (BlkStream, setup_host.hpp): one fetch unit per
 /// block of 32 rows in solve order; `table` holds (offset / 16, bytes).
 struct DevBlk {
-    int n, n_blocks, fresh, max_unit_bytes;
+    int n, n_blocks, parts, mf0, lookahead, max_unit_bytes;
     const unsigned char* stream;  // 16-byte aligned
-    const int2* table;
+    const int4* table;  // per block: offset / 16, bytes, fresh slots, 0
 };
 
 struct DevHLevel {

@@ -188,15 +188,10 @@ void upload_blk(const BlkStream& b, Hier::BlkDev& d, cudaStream_t s) {
     d.table = dev(b.table, s);
     d.n = b.n;
     d.n_blocks = b.n_blocks;
-    d.fresh = b.fresh;
+    d.parts = b.parts;
+    d.mf0 = b.mf0;
+    d.lookahead = b.lookahead;
     d.max_unit_bytes = b.max_unit_bytes;
-}
-// Fresh distance F of the block sweeps (blocks whose columns are summed on the
-// critical path).  Developer override: PHI_BLK_FRESH="ilut,gs".
-int blk_fresh(int which) {
-    int f[2] = {1, 2};
-    if (const char* e = std::getenv("PHI_BLK_FRESH")) std::sscanf(e, "%d,%d", &f[0], &f[1]);
-    return std::min(std::max(f[which], 1), kBlkMaxFresh);
 }
 }  // namespace
 
@@ -204,10 +199,12 @@ DevBlk Hier::BlkDev::view() const {
     DevBlk b{};
     b.n = n;
     b.n_blocks = n_blocks;
-    b.fresh = fresh;
+    b.parts = parts;
+    b.mf0 = mf0;
+    b.lookahead = lookahead;
     b.max_unit_bytes = max_unit_bytes;
     b.stream = stream.get();
-    b.table = reinterpret_cast<const int2*>(table.get());
+    b.table = reinterpret_cast<const int4*>(table.get());
     return b;
 }
 
@@ -229,8 +226,8 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
         upload_tri(Lp, false, Ld, s);
         upload_tri(Up, false, Ud, s);
     } else {
-        upload_blk(blk_lower(L_host, blk_fresh(0)), Lbd, s);
-        upload_blk(blk_upper(U_host, blk_fresh(0)), Ubd, s);
+        upload_blk(blk_lower(L_host), Lbd, s);
+        upload_blk(blk_upper(U_host), Ubd, s);
     }
     for (const auto& hl : d.h) {
         StencilBuf a;
@@ -252,7 +249,7 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
                 upload_tri(gs_plans.back(), false, gs_dev.back(), s);
             } else {
                 gsb_dev.emplace_back();
-                upload_blk(blk_gauss_seidel(al, dir == 1, blk_fresh(1)), gsb_dev.back(), s);
+                upload_blk(blk_gauss_seidel(al, dir == 1), gsb_dev.back(), s);
             }
         }
     }

@@ -108,7 +108,7 @@ public:
     struct BlkDev {
         DevBuf<unsigned char> stream;
         DevBuf<int> table;
-        int n = 0, n_blocks = 0, fresh = 1, max_unit_bytes = 0;
+        int n = 0, n_blocks = 0, parts = 1, mf0 = 0, lookahead = 0, max_unit_bytes = 0;
         DevBlk view() const;
     } Lbd, Ubd;
     std::vector<BlkDev> gsb_dev;  // per h-level (but the coarsest): forward, backward

@@ -230,9 +230,71 @@ struct Tree<1> {
     static __device__ __forceinline__ double sum(const double* p) { return p[0]; }
 };
 
+// Reassociated mode: every row issues all of its loads at clamped (in-range)
+// addresses, without branches (entries outside the column grid are selected
+// to zero), in chunks of DVC stencil rows -- enough loads in flight per thread
+// to cover the L2 latency -- and sums them by a tree per stencil row.
+template <int OUT, int W>
+__device__ __noinline__ void stencil_apply_fast(const DevStencil& A, const double* __restrict__ x,
+                                                double* __restrict__ y, const double* __restrict__ aux) {
+    constexpr int DVC = W * W <= 25 ? W : (24 / W > 0 ? 24 / W : 1);
+    const int n = A.ru * A.rv;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        const int iv = i / A.ru;
+        const int iu = i - iv * A.ru;
+        int cu_[W];
+        bool okq[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            const int c = iu + A.lo + q;
+            okq[q] = c >= 0 && c < A.cu;
+            cu_[q] = min(max(c, 0), A.cu - 1);
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int d0 = 0; d0 < W; d0 += DVC) {
+            double pv[DVC][W], px[DVC][W];
+#pragma unroll
+            for (int a = 0; a < DVC; ++a) {
+                if (d0 + a < W) {
+                    const int r = iv + A.lo + d0 + a;
+                    const bool okr = r >= 0 && r < A.cv;
+                    const int rv = min(max(r, 0), A.cv - 1);
+                    const double* vr = A.vals + (size_t)((d0 + a) * W) * n + i;
+                    const double* xr = x + (size_t)rv * A.cu;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) {
+                        const double v = __ldg(vr + (size_t)q * n);
+                        pv[a][q] = okr && okq[q] ? v : 0.0;  // entries outside the column grid
+                        px[a][q] = xr[cu_[q]];
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < DVC; ++a) {
+                if (d0 + a < W) {
+                    double pr[W];
+#pragma unroll
+                    for (int q = 0; q < W; ++q) pr[q] = pv[a][q] * px[a][q];
+                    s = s + Tree<W>::sum(pr);
+                }
+            }
+        }
+        if (OUT == kOutSet) y[i] = s;
+        if (OUT == kOutResid) y[i] = aux[i] - s;             // r = b - A x
+        if (OUT == kOutScale) y[i] = s * aux[i];             // (P^T r) .* 1/M^L
+        if (OUT == kOutAddScaled) y[i] = y[i] + s * aux[i];  // x += (P e) .* 1/M^L
+        if (OUT == kOutAddVec) y[i] = s + aux[i];            // rhs = A- u + load
+    }
+}
+
 template <int OUT, int W>
 __device__ __noinline__ void stencil_apply(const DevStencil& A, const double* __restrict__ x,
                                            double* __restrict__ y, const double* __restrict__ aux, bool exact = true) {
+    if (!exact) {
+        stencil_apply_fast<OUT, W>(A, x, y, aux);
+        return;
+    }
     const int n = A.ru * A.rv;
     for (int i = threadIdx.x; i < n; i += NT) {
         const int iv = i / A.ru;
@@ -697,44 +759,47 @@ __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int 
 }
 
 // ---- block-recurrence sweeps (reassociated mode) ---------------------------
-// One sweep (ILUT substitution or Gauss-Seidel) over a BlkStream
-// (setup_host.hpp): blocks of 32 consecutive rows in solve order, block k
-// solved as x_{R_k} = B_k^{-1} (rhs - old - fresh).
-//  * warp 0 (the solver) runs the dependent chain: per block it waits for the
-//    block's "old" sums, subtracts the fresh entries (columns of the last F
-//    blocks, loaded from x now), multiplies by the dense inverse (the 32
-//    right-hand sides broadcast through shared memory) and stores the 32 new
-//    values;
-//  * warps 1..7 (the workers) take the blocks in turn: once block k-F-1 is
-//    done they sum the block's old entries and hand c = rhs - old over.
+// `count` consecutive sweeps (ILUT substitution or Gauss-Seidel) over one
+// BlkStream (setup_host.hpp): blocks of 32 consecutive rows in solve order,
+// block k solved as x_{R_k} = B_k^{-1} (rhs - old - fresh).  The blocks of
+// the `count` sweeps form one sequence g = s * nb + k.
+//  * warp 0 (the solver) runs the dependent chain.  Per block it waits until
+//    the workers' old sums are in, then -- everything that does not depend on
+//    block g-1 issued first -- gathers the fresh columns (block g-1),
+//    broadcasts t = rhs - old - fresh through shared memory, multiplies by
+//    the dense inverse and stores the 32 new values;
+//  * warps 1..parts (the workers) each sum one interleaved part of the
+//    block's old entries as soon as block g-2 is done (and, for a later
+//    sweep, the previous sweep's rows they read), one block ahead of the
+//    solver.
 // The blocks stream through a shared-memory ring of n_slots units filled by
-// TMA bulk copies; the solver refills the slot of block k (with block k +
-// n_slots) once block k is done -- its worker finished earlier.  Hand-offs
-// are release/acquire flags in shared memory: `prog` (last block done) and
-// flag[k % kBlkHand] = k (old sums of block k ready).
-__device__ __forceinline__ void st_release_s32(unsigned a, int v) {
-    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+// TMA bulk copies: the workers wait for a unit's mbarrier, the solver
+// refills the slot of block g (with block g + n_slots) once block g is done.
+// Hand-offs are plain shared-memory flags: `prog` (last block done) and
+// cnt[g % kBlkHand] (parts of block g summed, shared-memory atomics).  A
+// warp's shared-memory accesses are performed in order, and __syncwarp()
+// orders the lanes' data stores before the flag update of lane 0; a
+// global-memory vector is fenced (__threadfence_block) before its flag.
+__device__ __forceinline__ void st_volatile_s32(unsigned a, int v) {
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire_s32(unsigned a) {
+__device__ __forceinline__ int ld_volatile_s32(unsigned a) {
     int v;
-    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
 __device__ __noinline__ void spin_fail(int what, int have, int want) {
     printf("phi spin guard: block %d thread %d wait %d have %d want %d\n", blockIdx.x, threadIdx.x, what, have, want);
     __trap();
 }
-__device__ __forceinline__ void wait_ge(unsigned a, int v) {
+// spin until *a >= v; returns the value seen
+__device__ __forceinline__ int wait_ge(unsigned a, int v) {
+    int h = ld_volatile_s32(a);
+    if (h >= v) return h;
     const long long t0 = PHI_SPIN_GUARD ? clock64() : 0;
-    int h;
-    while ((h = ld_acquire_s32(a)) < v)
+    while ((h = ld_volatile_s32(a)) < v)
         if (PHI_SPIN_GUARD && clock64() - t0 > 4000000000LL) spin_fail(1, h, v);
-}
-__device__ __forceinline__ void wait_eq(unsigned a, int v) {
-    const long long t0 = PHI_SPIN_GUARD ? clock64() : 0;
-    int h;
-    while ((h = ld_acquire_s32(a)) != v)
-        if (PHI_SPIN_GUARD && clock64() - t0 > 4000000000LL) spin_fail(2, h, v);
+    return h;
 }
 // x[j]: shared (XSM: byte address base + 8 j) or global
 template <bool XSM>
@@ -742,7 +807,7 @@ __device__ __forceinline__ double xld(const double* xg, unsigned xs, int j) {
     if constexpr (XSM)
         return vlds_f64(xs + 8u * j);
     else
-        return xg[j];
+        return *reinterpret_cast<const volatile double*>(xg + j);
 }
 template <bool XSM>
 __device__ __forceinline__ void xst(double* xg, unsigned xs, int j, double v) {
@@ -751,35 +816,23 @@ __device__ __forceinline__ void xst(double* xg, unsigned xs, int j, double v) {
     else
         xg[j] = v;
 }
-// sum over `m` slots (batches of 4) of vals[q][lane] * x[cols[q][lane]]
-template <bool XSM>
-__device__ __forceinline__ double slot_sum(unsigned cp, unsigned vp, int m, const double* xg, unsigned xs) {
-    double a0 = 0.0, a1 = 0.0;
-    for (int q0 = 0; q0 < m; q0 += 4) {
-        int j[4];
-        double v[4], xj[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            j[q] = vlds_s32(cp + 128u * (q0 + q));
-            v[q] = vlds_f64(vp + 256u * (q0 + q));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) xj[q] = xld<XSM>(xg, xs, j[q]);
-        a0 = __fma_rn(v[0], xj[0], a0);
-        a1 = __fma_rn(v[1], xj[1], a1);
-        a0 = __fma_rn(v[2], xj[2], a0);
-        a1 = __fma_rn(v[3], xj[3], a1);
-    }
-    return a0 + a1;
+__device__ __forceinline__ void lds_v2f64(unsigned a, double& x, double& y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ void lds_slot(unsigned a, int& c, double& v) {  // {int32 col, pad, double val}
+    int pad;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(c), "=r"(pad), "=r"(reinterpret_cast<int*>(&v)[0]),
+                 "=r"(reinterpret_cast<int*>(&v)[1]) : "r"(a));
+    (void)pad;
 }
 
 struct __align__(16) BlkSync {
-    double cbuf[kBlkHand * 32];
-    double tb[32];  // 16-byte aligned: read as v2 broadcasts
+    double cbuf[kBlkHand][kBlkMaxParts][32];  // workers' partial old sums
+    double tb[2][32];                         // per-solver broadcast of t (16-byte aligned)
     unsigned long long bar[kBlkMaxSlots];
     int phase[kBlkMaxSlots];  // phases completed per slot since the kernel started
+    int cnt[kBlkHand];
     int prog;
-    int flag[kBlkHand];
 };
 // One per CTA.  The ring's mbarriers are initialised once per kernel
 // (blk_init) and never re-initialised: every sweep continues their phase
@@ -793,97 +846,194 @@ __device__ __forceinline__ void blk_init() {
             mbar_init(bar + 8u * k);
             g_blk.phase[k] = 0;
         }
+        for (int k = 0; k < kBlkHand; ++k) g_blk.cnt[k] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // the callers' next __syncthreads() publishes the initialisation
 }
 
+// named barriers of the solver hand-off: block g done -> solver (g + 1) % 2
+__device__ __forceinline__ void hand_wait(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void hand_signal(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+constexpr int kHandBar = 1;  // ids 1, 2
+
 template <bool XSM, bool RSM>
-__device__ __noinline__ void blk_sweep_t(const DevBlk& T, double* xg, int x_off, const double* rg, int r_off,
-                                         int ring_off, int slot_bytes, int n_slots, BlkSync& sy) {
-    // parity of unit k: (phases slot k % n_slots completed before this sweep
-    // + k / n_slots) & 1
+__device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg, int x_off, const double* rg,
+                                         int r_off, int ring_off, int slot_bytes, int n_slots) {
+    BlkSync& sy = g_blk;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nb = T.n_blocks, F = T.fresh;
+    const int nb = T.n_blocks, P = T.parts, total = count * nb;
     const unsigned ring = sh_addr(g_smem + ring_off);
     const unsigned bar = sh_addr(sy.bar);
     const unsigned xs = XSM ? sh_addr(g_smem + x_off) : 0u;
     const unsigned rs = RSM ? sh_addr(g_smem + r_off) : 0u;
-    const unsigned prog = sh_addr(&sy.prog), flag = sh_addr(sy.flag), cbuf = sh_addr(sy.cbuf), tb = sh_addr(sy.tb);
+    const unsigned prog = sh_addr(&sy.prog), cnt = sh_addr(sy.cnt), cbuf = sh_addr(sy.cbuf);
     const unsigned char* __restrict__ stream = T.stream;
-    const int2* __restrict__ table = T.table;
-    if (w == 0) {
-        // ---- the solver warp
-        int2 nxt = make_int2(0, 0);
-        if (lane == 0 && n_slots < nb) nxt = __ldg(table + n_slots);
-        for (int k = 0; k < nb; ++k) {
-            const int slot = k % n_slots;
-            mbar_wait(bar + 8u * slot, (unsigned)(sy.phase[slot] + k / n_slots) & 1u);
-            const unsigned u = ring + slot * slot_bytes;
-            int mo, mf, bytes, pad;
-            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(mo), "=r"(mf), "=r"(bytes), "=r"(pad) : "r"(u));
-            (void)bytes;
-            (void)pad;
+    const int4* __restrict__ table = T.table;
+    if (w < 2) {
+        // ---- solver warps 0 / 1 take blocks g = w, w + 2, ...  The parts'
+        // count implies the block's unit has landed (each worker waited).
+        const unsigned tb = sh_addr(sy.tb[w]);
+        int slot = w, k = w;
+        int4 info = w < total ? __ldg(table + w) : make_int4(0, 0, 0, 0);  // (off16, bytes, mf, 0)
+        for (int g = w; g < total; g += 2) {
+            const int mf = info.z;
+            int kn2 = k + 2;  // this solver's next block
+            while (kn2 >= nb) kn2 -= nb;
+            if (g + 2 < total) info = __ldg(table + kn2);
+            long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && g < 1024)
+                                ? c_tune.trace + kTriTraceBase + 8 * g
+                                : nullptr;
+            if (tr) tr[0] = clock64();
+            const int seen = wait_ge(cnt + 4u * (g & (kBlkHand - 1)), P);
+            if (tr) tr[1] = clock64();
+            // data dependence on the wait: none of these loads moves above it
+            const unsigned u = ring + slot * slot_bytes + (unsigned)(seen - P);
+            // ---- independent of block g-1: row, rhs, partial sums, inverse, fresh slots
             const int row = vlds_s32(u + 16u + 4u * lane);
-            const unsigned fc = u + 144u + 384u * mo, fv = fc + 128u * mf, iv = fv + 256u * mf;
-            double inv[32];
+            double rhs = 0.0;
+            if (row >= 0) rhs = RSM ? vlds_f64(rs + 8u * row) : *reinterpret_cast<const volatile double*>(rg + row);
+            double part[kBlkMaxParts];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                inv[j] = lane >= j ? vlds_f64(iv + 8u * (32 * j - j * (j - 1) / 2 + lane - j)) : 0.0;
-            wait_eq(flag + 4u * (k % kBlkHand), k);
-            double t = vlds_f64(cbuf + 8u * ((k % kBlkHand) * 32 + lane));
-            if (mf > 0) t = t - slot_sum<XSM>(fc + 4u * lane, fv + 8u * lane, mf, xg, xs);
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(t) : "memory");
-            __syncwarp();
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < kBlkMaxParts; ++q)
+                part[q] = q < P ? vlds_f64(cbuf + 8u * (((g & (kBlkHand - 1)) * kBlkMaxParts + q) * 32 + lane)) : 0.0;
+            double iv[32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-                double t0, t1;
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(t0), "=d"(t1) : "r"(tb + 8u * j));
-                acc[(j >> 1) & 3] = __fma_rn(inv[j], t0, acc[(j >> 1) & 3]);
-                acc[(j >> 1) & 3] = __fma_rn(inv[j + 1], t1, acc[(j >> 1) & 3]);
-            }
-            const double z = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-            if (row >= 0) xst<XSM>(xg, xs, row, z);
-            __syncwarp();
-            if (lane == 0) {
-                st_release_s32(prog, k);
-                // block k's unit is consumed by both warps: refill its slot
-                if (k + n_slots < nb) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    bulk_fetch(u, stream + (size_t)nxt.x * 16, nxt.y, bar + 8u * slot);
-                    if (k + 1 + n_slots < nb) nxt = __ldg(table + k + 1 + n_slots);
+            for (int p2 = 0; p2 < 16; ++p2) lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
+            const unsigned fr = u + kBlkFreshOff + 16u * lane;
+            int fc[8];
+            double fv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q < mf) lds_slot(fr + 512u * q, fc[q], fv[q]);
+                else {
+                    fc[q] = T.n;
+                    fv[q] = 0.0;
                 }
             }
-        }
-    } else {
-        // ---- worker warps: old sums of blocks w-1, w-1+7, ...
-        for (int k = w - 1; k < nb; k += NW - 1) {
-            // block k-F-1 done: the old columns are final, and unit k is in
-            // flight (issued when block k - n_slots was done, n_slots >= F + 2)
-            wait_ge(prog, k - F - 1);
-            const int slot = k % n_slots;
-            mbar_wait(bar + 8u * slot, (unsigned)(sy.phase[slot] + k / n_slots) & 1u);
-            const unsigned u = ring + slot * slot_bytes;
-            const int mo = vlds_s32(u);
-            const int row = vlds_s32(u + 16u + 4u * lane);
-            const double s = mo > 0 ? slot_sum<XSM>(u + 144u + 4u * lane, u + 144u + 128u * mo + 8u * lane, mo, xg, xs) : 0.0;
-            double r = 0.0;
-            if (row >= 0) r = RSM ? vlds_f64(rs + 8u * row) : rg[row];
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(cbuf + 8u * ((k % kBlkHand) * 32 + lane)), "d"(r - s) : "memory");
+            const double c = rhs - (((part[0] + part[1]) + (part[2] + part[3])) + (part[4] + part[5]));
+            // ---- wait for block g-1 (the other solver)
+            if (g > 0) hand_wait(kHandBar + (w ^ 1));
+            if (tr) tr[2] = clock64();
+            // ---- the chain: fresh columns of block g-1, broadcast, inverse
+            double f[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) f[q] = q < mf ? fv[q] * xld<XSM>(xg, xs, fc[q]) : 0.0;
+            for (int q = 8; q < mf; ++q) {  // rare: more than 8 fresh slots
+                int cq;
+                double vq;
+                lds_slot(fr + 512u * q, cq, vq);
+                f[q & 7] = __fma_rn(vq, xld<XSM>(xg, xs, cq), f[q & 7]);
+            }
+            const double t = c - (((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(t) : "memory");
             __syncwarp();
-            if (lane == 0) st_release_s32(flag + 4u * (k % kBlkHand), k);
+            double acc[8];
+#pragma unroll
+            for (int p2 = 0; p2 < 16; ++p2) {
+                double t0, t1;
+                lds_v2f64(tb + 16u * p2, t0, t1);
+                if (p2 < 4) {
+                    acc[2 * p2] = iv[2 * p2] * t0;
+                    acc[2 * p2 + 1] = iv[2 * p2 + 1] * t1;
+                } else {
+                    acc[(2 * p2) & 7] = __fma_rn(iv[2 * p2], t0, acc[(2 * p2) & 7]);
+                    acc[(2 * p2 + 1) & 7] = __fma_rn(iv[2 * p2 + 1], t1, acc[(2 * p2 + 1) & 7]);
+                }
+            }
+            double z = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            if (c_tune.xmask & 2) z = t;  // developer timing: no inverse
+            if (row >= 0) xst<XSM>(xg, xs, row, z);
+            if constexpr (!XSM) __threadfence_block();  // global x: order the stores before the hand-off
+            __syncwarp();
+            if (lane == 0) st_volatile_s32(prog, g);  // monotone: block g+1 starts after the hand-off
+            if (g + 1 < total) hand_signal(kHandBar + w);
+            if (tr) tr[3] = clock64();
+            // ---- off the chain: bookkeeping for this solver's next block
+            if (lane == 0) {
+                st_volatile_s32(cnt + 4u * (g & (kBlkHand - 1)), 0);  // reused by block g + kBlkHand
+                if (g + n_slots < total) {  // block g's unit is consumed: refill its slot
+                    int kn = k + n_slots;
+                    while (kn >= nb) kn -= nb;
+                    const int4 e = __ldg(table + kn);
+                    bulk_fetch(ring + slot * slot_bytes, stream + (size_t)e.x * 16, e.y, bar + 8u * slot);
+                }
+            }
+            slot += 2;
+            if (slot >= n_slots) slot -= n_slots;
+            k = kn2;
+        }
+    } else if (w - 2 < P) {
+        // ---- worker q = w - 2: part q of every block's old sums
+        const int q = w - 2;
+        int k = 0, s = 0, slot = 0, ph = 0;
+        for (int g = 0; g < total; ++g) {
+            long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && q == 0 && g < 1024)
+                                ? c_tune.trace + kTriTraceBase + 8 * g
+                                : nullptr;
+            // unit g was issued when block g - n_slots was done (n_slots >= 3;
+            // this worker saw prog >= g - 3 for its previous block)
+            mbar_wait(bar + 8u * slot, (unsigned)(sy.phase[slot] + ph) & 1u);
+            if (tr) tr[4] = clock64();
+            const unsigned u = ring + slot * slot_bytes;
+            const int mo = vlds_s32(u), mf = vlds_s32(u + 12u);
+            const unsigned oc = u + kBlkFreshOff + 512u * mf + 384u * mo * q + 4u * lane;
+            const unsigned ov = oc + 128u * mo + 4u * lane;
+            // columns solved by blocks <= g-2 of this sweep; for a later sweep
+            // also the previous sweep's rows up to block k + lookahead
+            int need = g - 2;
+            if (s > 0) need = max(need, (s - 1) * nb + min(k + T.lookahead, nb - 1));
+            double a0 = 0.0, a1 = 0.0;
+            if (mo <= 8) {  // the common case: every load issued before the wait
+                int c[8];
+                double v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    c[e] = e < mo ? vlds_s32(oc + 128u * e) : T.n;
+                    v[e] = e < mo ? vlds_f64(ov + 256u * e) : 0.0;
+                }
+                wait_ge(prog, need);
+                if (tr) tr[5] = clock64();
+                double xv[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) xv[e] = e < mo ? xld<XSM>(xg, xs, c[e]) : 0.0;
+                a0 = __fma_rn(v[0], xv[0], v[1] * xv[1]) + __fma_rn(v[4], xv[4], v[5] * xv[5]);
+                a1 = __fma_rn(v[2], xv[2], v[3] * xv[3]) + __fma_rn(v[6], xv[6], v[7] * xv[7]);
+            } else {
+                wait_ge(prog, need);
+                if (tr) tr[5] = clock64();
+                for (int e = 0; e < mo; e += 2) {
+                    const int c0 = vlds_s32(oc + 128u * e), c1 = e + 1 < mo ? vlds_s32(oc + 128u * (e + 1)) : T.n;
+                    const double v0 = vlds_f64(ov + 256u * e), v1 = e + 1 < mo ? vlds_f64(ov + 256u * (e + 1)) : 0.0;
+                    a0 = __fma_rn(v0, xld<XSM>(xg, xs, c0), a0);
+                    a1 = __fma_rn(v1, xld<XSM>(xg, xs, c1), a1);
+                }
+            }
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(cbuf + 8u * (((g & (kBlkHand - 1)) * kBlkMaxParts + q) * 32 + lane)),
+                         "d"(a0 + a1)
+                         : "memory");
+            __syncwarp();
+            if (lane == 0) atomicAdd(&sy.cnt[g & (kBlkHand - 1)], 1);
+            if (tr) tr[6] = clock64();
+            if (++slot == n_slots) {
+                slot = 0;
+                ++ph;
+            }
+            if (++k == nb) {
+                k = 0;
+                ++s;
+            }
         }
     }
 }
 
-// One block sweep: prime, the solver / worker split, closing barrier, phase
-// bookkeeping.  Called by the whole CTA (blk_init ran at kernel start).
-__device__ __forceinline__ void blk_sweep(const DevBlk& T, double* xg, int x_off, const double* rg, int r_off,
-                                          int ring_off, int slot_bytes, int n_slots) {
+// `count` sweeps over T: prime, the solver / worker split, closing barrier,
+// phase bookkeeping.  Called by the whole CTA (blk_init ran at kernel start).
+__device__ __forceinline__ void blk_sweep(const DevBlk& T, int count, double* xg, int x_off, const double* rg,
+                                          int r_off, int ring_off, int slot_bytes, int n_slots) {
     BlkSync& sy = g_blk;
-    const int nb = T.n_blocks;
-    if (nb == 0) return;
+    const int nb = T.n_blocks, total = count * nb;
+    if (total == 0) return;
     // the ring overlays buffers written through the generic proxy in other
     // phases: order those writes before the TMA (async-proxy) writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -891,23 +1041,22 @@ __device__ __forceinline__ void blk_sweep(const DevBlk& T, double* xg, int x_off
     if (threadIdx.x == 0) {
         const unsigned bar = sh_addr(sy.bar);
         sy.prog = -1;
-        for (int k = 0; k < kBlkHand; ++k) sy.flag[k] = -1;
         const unsigned ring = sh_addr(g_smem + ring_off);
-        for (int k = 0; k < n_slots && k < nb; ++k) {
-            const int2 e = __ldg(T.table + k);
-            bulk_fetch(ring + k * slot_bytes, T.stream + (size_t)e.x * 16, e.y, bar + 8u * k);
+        for (int g = 0; g < n_slots && g < total; ++g) {
+            const int4 e = __ldg(T.table + g % nb);
+            bulk_fetch(ring + g * slot_bytes, T.stream + (size_t)e.x * 16, e.y, bar + 8u * g);
         }
     }
     __syncthreads();
     if (x_off >= 0 && r_off >= 0)
-        blk_sweep_t<true, true>(T, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots, sy);
+        blk_sweep_t<true, true>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
     else if (x_off >= 0)
-        blk_sweep_t<true, false>(T, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots, sy);
+        blk_sweep_t<true, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
     else
-        blk_sweep_t<false, false>(T, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots, sy);
+        blk_sweep_t<false, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
     __syncthreads();
-    if (threadIdx.x == 0)  // units delivered per slot this sweep
-        for (int k = 0; k < n_slots; ++k) sy.phase[k] += k < nb ? (nb - 1 - k) / n_slots + 1 : 0;
+    if (threadIdx.x == 0)  // units delivered per slot
+        for (int g = 0; g < n_slots; ++g) sy.phase[g] += g < total ? (total - 1 - g) / n_slots + 1 : 0;
     // published by the next sweep's (or phase's) __syncthreads()
 }
 
@@ -952,8 +1101,8 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
 // Reassociated mode: both substitutions as block recurrences, then x += z.
 __device__ __forceinline__ void ilut_solve_blk(const DevBlk& L, const DevBlk& U, double* zg, int z_off, double* xadd,
                                                const Ws& w) {
-    blk_sweep(L, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
-    blk_sweep(U, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
+    blk_sweep(L, 1, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
+    blk_sweep(U, 1, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
     if (xadd) {
         const double* z = z_off >= 0 ? g_smem + z_off : zg;
         for (int i = threadIdx.x; i < L.n; i += NT) xadd[i] = xadd[i] + z[i];
@@ -1102,7 +1251,7 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             if (H.exact)
                 gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
             else
-                for (int c = 0; c < H.gs_pre; ++c) blk_sweep(lv.gsb_fwd, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+                blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
             stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b, H.exact != 0);
             __syncthreads();
             csr_apply<false>(lv.embed_t, w.hr[l], w.hb[l + 1]);  // rc = E^T r
@@ -1119,7 +1268,7 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             if (H.exact)
                 gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
             else
-                for (int c = 0; c < H.gs_post; ++c) blk_sweep(lv.gsb_bwd, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+                blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
             if (l == 0) break;
             --l;
         }
@@ -1379,7 +1528,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (H.exact)
             gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
         else
-            blk_sweep(arg2 ? lv.gsb_bwd : lv.gsb_fwd, w.hx[arg], xo, w.hb[arg], bo, w.ring_off, w.gs_slot_bytes,
+            blk_sweep(arg2 ? lv.gsb_bwd : lv.gsb_fwd, 1, w.hx[arg], xo, w.hb[arg], bo, w.ring_off, w.gs_slot_bytes,
                       w.gs_n_slots);
         cta_copy(out, w.hx[arg], lv.n);
     }

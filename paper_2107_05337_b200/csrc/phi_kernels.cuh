@@ -14,7 +14,7 @@ namespace phi {
 constexpr int kPhiThreads = 256;
 // Dynamic shared memory one Phi CTA may use for its latency-critical vectors
 // (one CTA per SM; 227 KB is the sm_100 per-block maximum).
-constexpr size_t kPhiSmemBudgetBytes = 216 * 1024;
+constexpr size_t kPhiSmemBudgetBytes = 212 * 1024;
 
 size_t phi_ws_doubles(const DevHier& H);
 SmemPlan phi_smem_plan(const DevHier& H);

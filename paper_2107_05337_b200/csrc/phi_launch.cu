@@ -107,7 +107,7 @@ SmemPlan phi_smem_plan(const DevHier& H) {
             gslot = std::max(gslot, std::max(H.h[l].gsb_fwd.max_unit_bytes, H.h[l].gsb_bwd.max_unit_bytes));
         P.slot_bytes = (slot + 127) / 128 * 128;
         P.gs_slot_bytes = (gslot + 127) / 128 * 128;
-        const int min_slots = std::max(H.Lb.fresh, H.Ub.fresh) + 2;
+        const int min_slots = 3;  // workers wait for unit g once block g - 3 is done
         // the ILUT ring leaves room for z when it can
         const size_t zb = ((size_t)H.n_p + 2) * 8;
         int ns = (int)std::min<size_t>(kBlkMaxSlots, (kPhiSmemBudgetBytes - std::min(zb, kPhiSmemBudgetBytes)) / P.slot_bytes);
@@ -115,9 +115,7 @@ SmemPlan phi_smem_plan(const DevHier& H) {
         if (ns < min_slots) throw InvalidArgument("triangular-factor blocks exceed shared memory");
         P.n_slots = ns;
         tri = (size_t)ns * P.slot_bytes / 8;
-        int gfresh = 1;
-        for (int l = 0; l + 1 < H.n_h; ++l) gfresh = std::max(gfresh, std::max(H.h[l].gsb_fwd.fresh, H.h[l].gsb_bwd.fresh));
-        P.gs_n_slots = std::max(gfresh + 2, std::min(kBlkMaxSlots, 6));
+        P.gs_n_slots = std::min(kBlkMaxSlots, 6);
         gs_tri = (size_t)P.gs_n_slots * P.gs_slot_bytes / 8;
     }
     size_t top = std::max(tri, gs_tri);

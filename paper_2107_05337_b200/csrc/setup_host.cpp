@@ -746,86 +746,116 @@ struct BlkRowsView {
     std::function<double(int)> diag;
 };
 
-BlkStream make_blk_stream(const BlkRowsView& rv, int fresh) {
+BlkStream make_blk_stream(const BlkRowsView& rv) {
     const int n = rv.n;
     BlkStream bs;
     bs.n = n;
-    bs.fresh = fresh;
     bs.n_blocks = (n + kBlkRows - 1) / kBlkRows;
     auto pos_of = [&](int i) { return rv.descending ? n - 1 - i : i; };
     auto row_at = [&](int pos) { return rv.descending ? n - 1 - pos : pos; };
     std::vector<int> cols;
     std::vector<double> vals;
-    std::vector<std::vector<unsigned char>> units(bs.n_blocks);
-    for (int k = 0; k < bs.n_blocks; ++k) {
-        long double B[kBlkRows][kBlkRows] = {};
+    struct Blk {
+        long double B[kBlkRows][kBlkRows];
         std::vector<std::pair<int, double>> olde[kBlkRows], frsh[kBlkRows];
         int rows[kBlkRows];
-        size_t mo = 0, mf = 0;
+        size_t maxold = 0, mf = 0;
+    };
+    std::vector<Blk> blks(bs.n_blocks);
+    size_t maxold_all = 0;
+    for (int k = 0; k < bs.n_blocks; ++k) {
+        Blk& b = blks[k];
+        for (auto& r : b.B)
+            for (auto& v : r) v = 0.0L;
         for (int l = 0; l < kBlkRows; ++l) {
             const int pos = k * kBlkRows + l;
             if (pos >= n) {
-                rows[l] = -1;
-                B[l][l] = 1.0L;
+                b.rows[l] = -1;
+                b.B[l][l] = 1.0L;
                 continue;
             }
             const int i = row_at(pos);
-            rows[l] = i;
-            B[l][l] = rv.diag(i);
+            b.rows[l] = i;
+            b.B[l][l] = rv.diag(i);
             rv.entries(i, cols, vals);
             for (size_t e = 0; e < cols.size(); ++e) {
                 const int pj = pos_of(cols[e]), kj = pj / kBlkRows;
-                if (pj < pos && kj == k)
-                    B[l][pj - k * kBlkRows] += vals[e];
-                else if (pj < pos && kj >= k - fresh)
-                    frsh[l].emplace_back(cols[e], vals[e]);
-                else
-                    olde[l].emplace_back(cols[e], vals[e]);
+                if (pj < pos && kj == k) {
+                    b.B[l][pj - k * kBlkRows] += vals[e];
+                } else if (pj < pos && kj == k - 1) {
+                    b.frsh[l].emplace_back(cols[e], vals[e]);
+                } else {
+                    b.olde[l].emplace_back(cols[e], vals[e]);
+                    if (pj > pos) bs.lookahead = std::max(bs.lookahead, kj - k);
+                }
             }
-            mo = std::max(mo, olde[l].size());
-            mf = std::max(mf, frsh[l].size());
+            b.maxold = std::max(b.maxold, b.olde[l].size());
+            b.mf = std::max(b.mf, b.frsh[l].size());
         }
-        mo = (mo + 3) / 4 * 4;  // whole batches of 4 slots
-        mf = (mf + 3) / 4 * 4;
+        b.mf = (b.mf + 1) / 2 * 2;  // pairs of fresh slots
+        maxold_all = std::max(maxold_all, b.maxold);
+    }
+    // worker parts: about four old slots per part and lane
+    bs.parts = static_cast<int>(std::min<size_t>(kBlkMaxParts, std::max<size_t>(1, (maxold_all + 3) / 4)));
+    const int P = bs.parts;
+    bs.mf0 = bs.n_blocks ? static_cast<int>(blks[0].mf) : 0;
+    std::vector<std::vector<unsigned char>> units(bs.n_blocks);
+    for (int k = 0; k < bs.n_blocks; ++k) {
+        Blk& b = blks[k];
+        const size_t mo = (b.maxold + P - 1) / P;
+        const size_t mf = b.mf;
         // dense inverse of the lower-triangular block, column by column
-        long double inv[kBlkRows][kBlkRows] = {};
+        static long double inv[kBlkRows][kBlkRows];
+        for (auto& r : inv)
+            for (auto& v : r) v = 0.0L;
         for (int j = 0; j < kBlkRows; ++j)
             for (int l = j; l < kBlkRows; ++l) {
-                long double s = l == j ? 1.0L : 0.0L;
-                for (int m = j; m < l; ++m) s -= B[l][m] * inv[m][j];
-                inv[l][j] = s / B[l][l];
+                long double acc = l == j ? 1.0L : 0.0L;
+                for (int m = j; m < l; ++m) acc -= b.B[l][m] * inv[m][j];
+                inv[l][j] = acc / b.B[l][l];
             }
-        const size_t bytes = 16 + 4 * kBlkRows + 12 * kBlkRows * (mo + mf) + 8 * kBlkInv;
+        const size_t bytes = kBlkFreshOff + 512 * mf + static_cast<size_t>(P) * 384 * mo;
         std::vector<unsigned char> img(bytes, 0);
-        const int hdr[4] = {static_cast<int>(mo), static_cast<int>(mf), static_cast<int>(bytes), 0};
+        const int hdr[4] = {static_cast<int>(mo), 0, static_cast<int>(bytes), static_cast<int>(mf)};
         std::memcpy(img.data(), hdr, sizeof hdr);
-        std::memcpy(img.data() + 16, rows, sizeof rows);
-        int* oc = reinterpret_cast<int*>(img.data() + 16 + 4 * kBlkRows);
-        double* ov = reinterpret_cast<double*>(oc + kBlkRows * mo);
-        int* fc = reinterpret_cast<int*>(ov + kBlkRows * mo);
-        double* fv = reinterpret_cast<double*>(fc + kBlkRows * mf);
-        double* iv = fv + kBlkRows * mf;
-        for (size_t s = 0; s < kBlkRows * mo; ++s) oc[s] = n;  // neutral padding (x[n] = +0.0)
-        for (size_t s = 0; s < kBlkRows * mf; ++s) fc[s] = n;
-        for (int l = 0; l < kBlkRows; ++l) {
-            for (size_t e = 0; e < olde[l].size(); ++e) {
-                oc[e * kBlkRows + l] = olde[l][e].first;
-                ov[e * kBlkRows + l] = olde[l][e].second;
+        std::memcpy(img.data() + 16, b.rows, sizeof b.rows);
+        double* iv = reinterpret_cast<double*>(img.data() + kBlkInvOff);
+        for (int pj = 0; pj < kBlkRows / 2; ++pj)
+            for (int l = 0; l < kBlkRows; ++l) {
+                iv[(pj * kBlkRows + l) * 2] = static_cast<double>(inv[l][2 * pj]);
+                iv[(pj * kBlkRows + l) * 2 + 1] = static_cast<double>(inv[l][2 * pj + 1]);
             }
-            for (size_t e = 0; e < frsh[l].size(); ++e) {
-                fc[e * kBlkRows + l] = frsh[l][e].first;
-                fv[e * kBlkRows + l] = frsh[l][e].second;
+        unsigned char* fr = img.data() + kBlkFreshOff;
+        for (size_t q = 0; q < mf; ++q)
+            for (int l = 0; l < kBlkRows; ++l) {
+                int col = n;
+                double v = 0.0;
+                if (q < b.frsh[l].size()) {
+                    col = b.frsh[l][q].first;
+                    v = b.frsh[l][q].second;
+                }
+                std::memcpy(fr + (q * kBlkRows + l) * 16, &col, 4);
+                std::memcpy(fr + (q * kBlkRows + l) * 16 + 8, &v, 8);
             }
+        for (int p = 0; p < P; ++p) {
+            int* oc = reinterpret_cast<int*>(img.data() + kBlkFreshOff + 512 * mf + static_cast<size_t>(p) * 384 * mo);
+            double* ov = reinterpret_cast<double*>(oc + kBlkRows * mo);
+            for (size_t s2 = 0; s2 < kBlkRows * mo; ++s2) oc[s2] = n;  // neutral padding (x[n] = +0.0)
+            for (int l = 0; l < kBlkRows; ++l)
+                for (size_t e = p, q = 0; e < b.olde[l].size(); e += P, ++q) {
+                    oc[q * kBlkRows + l] = b.olde[l][e].first;
+                    ov[q * kBlkRows + l] = b.olde[l][e].second;
+                }
         }
-        for (int j = 0; j < kBlkRows; ++j)
-            for (int l = j; l < kBlkRows; ++l)
-                iv[kBlkRows * j - j * (j - 1) / 2 + (l - j)] = static_cast<double>(inv[l][j]);
         units[k] = std::move(img);
     }
     size_t total = 0;
-    for (const auto& u : units) {
+    for (int k = 0; k < bs.n_blocks; ++k) {
+        const auto& u = units[k];
         bs.table.push_back(static_cast<int>(total / 16));
         bs.table.push_back(static_cast<int>(u.size()));
+        bs.table.push_back(static_cast<int>(blks[k].mf));
+        bs.table.push_back(0);
         bs.max_unit_bytes = std::max(bs.max_unit_bytes, static_cast<int>(u.size()));
         total += u.size();
     }
@@ -836,7 +866,7 @@ BlkStream make_blk_stream(const BlkRowsView& rv, int fresh) {
 
 }  // namespace
 
-BlkStream blk_lower(const HostCsr& m, int fresh) {
+BlkStream blk_lower(const HostCsr& m) {
     BlkRowsView rv;
     rv.n = m.n_rows;
     rv.entries = [&m](int i, std::vector<int>& c, std::vector<double>& v) {
@@ -844,10 +874,10 @@ BlkStream blk_lower(const HostCsr& m, int fresh) {
         v.assign(m.values.begin() + m.row_offsets[i], m.values.begin() + m.row_offsets[i + 1]);
     };
     rv.diag = [](int) { return 1.0; };
-    return make_blk_stream(rv, fresh);
+    return make_blk_stream(rv);
 }
 
-BlkStream blk_upper(const HostCsr& m, int fresh) {
+BlkStream blk_upper(const HostCsr& m) {
     BlkRowsView rv;
     rv.n = m.n_rows;
     rv.descending = true;
@@ -856,10 +886,10 @@ BlkStream blk_upper(const HostCsr& m, int fresh) {
         v.assign(m.values.begin() + m.row_offsets[i] + 1, m.values.begin() + m.row_offsets[i + 1]);
     };
     rv.diag = [&m](int i) { return m.values[m.row_offsets[i]]; };
-    return make_blk_stream(rv, fresh);
+    return make_blk_stream(rv);
 }
 
-BlkStream blk_gauss_seidel(const HostCsr& a, bool backward, int fresh) {
+BlkStream blk_gauss_seidel(const HostCsr& a, bool backward) {
     BlkRowsView rv;
     rv.n = a.n_rows;
     rv.descending = backward;
@@ -877,7 +907,7 @@ BlkStream blk_gauss_seidel(const HostCsr& a, bool backward, int fresh) {
             if (a.col_indices[e] == i) return a.values[e];
         throw std::runtime_error("gauss_seidel_sweep: zero diagonal entry");
     };
-    return make_blk_stream(rv, fresh);
+    return make_blk_stream(rv);
 }
 
 }  // namespace phi

@@ -128,33 +128,36 @@ TriStream make_tri_stream(const TriPlan& p, bool fast);
 ///     x_{R_k} = B_k^{-1} (rhs - old - fresh),   B_k = D + (in-block lower part),
 /// with the dense inverse B_k^{-1} precomputed here.  Entries of a row are
 ///   in-block lower  -> folded into B_k;
-///   fresh           -> columns solved by blocks k-F .. k-1 (summed on the
-///                      critical path after block k-1);
-///   old             -> columns solved by blocks <= k-F-1 (final once block
-///                      k-F-1 is done) or solved later (Gauss-Seidel's old
-///                      values, in-block ones included); summed ahead of time
-///                      by a worker warp.
+///   fresh           -> columns solved by block k-1 (summed on the critical
+///                      path, after block k-1);
+///   old             -> columns solved by blocks <= k-2 (final once block k-2
+///                      is done) or solved later (Gauss-Seidel's old values,
+///                      in-block ones included); summed ahead of time by the
+///                      worker warps, split into `parts` interleaved parts.
 /// One block = one fetch unit (one cp.async.bulk):
-///   header int32[4]: mo, mf, bytes, 0
-///   rows   int32[32]          at 16 (-1 on padding lanes)
-///   old    cols int32[mo][32], vals double[mo][32]  (slot q of lane L at q*32+L)
-///   fresh  cols int32[mf][32], vals double[mf][32]
-///   inv    double[528]: B_k^{-1} packed by columns, entry (L, j), L >= j, at
-///          32 j - j (j - 1) / 2 + (L - j)
+///   header int32[4]: mo (old slots per part), 0, bytes, mf (fresh slots)
+///   rows   int32[32]                 at 16 (-1 on padding lanes)
+///   inv    double[16][32][2]         at 144: entries (L, 2p), (L, 2p+1) of
+///                                    B_k^{-1} at (p * 32 + L) * 16 bytes
+///   fresh  {int32 col, pad, double val}[mf][32] at kBlkFreshOff
+///   old    per part q: cols int32[mo][32], vals double[mo][32] at
+///          kBlkFreshOff + 512 mf + q * 384 mo  (slot s of lane L at s*32+L)
 /// Padding slots are (column n, +0.0) against the zero slot x[n].  `table`
-/// holds (offset / 16, bytes) per block.
+/// holds (offset / 16, bytes, mf, 0) per block.
 constexpr int kBlkRows = 32;
-constexpr int kBlkInv = kBlkRows * (kBlkRows + 1) / 2;
+constexpr int kBlkInvOff = 144;
+constexpr int kBlkFreshOff = kBlkInvOff + 8 * kBlkRows * kBlkRows;
+constexpr int kBlkMaxParts = 6;
 struct BlkStream {
     std::vector<unsigned char> stream;
-    std::vector<int> table;  // 2 per block
-    int n = 0, n_blocks = 0, fresh = 1, max_unit_bytes = 0;
+    std::vector<int> table;  // 4 per block: offset / 16, bytes, fresh slots, 0
+    int n = 0, n_blocks = 0, parts = 1, mf0 = 0, lookahead = 0, max_unit_bytes = 0;
 };
 /// Unit lower ILUT factor (strictly lower entries stored), ascending.
-BlkStream blk_lower(const HostCsr& lower, int fresh);
+BlkStream blk_lower(const HostCsr& lower);
 /// Upper ILUT factor (diagonal first in each row), descending.
-BlkStream blk_upper(const HostCsr& upper, int fresh);
+BlkStream blk_upper(const HostCsr& upper);
 /// Lexicographic Gauss-Seidel sweep on A (solvers.hpp:80-99).
-BlkStream blk_gauss_seidel(const HostCsr& a, bool backward, int fresh);
+BlkStream blk_gauss_seidel(const HostCsr& a, bool backward);
 
 }  // namespace phi

@@ -35,34 +35,43 @@ static HostCsr stencil_matrix(int m, int w, unsigned seed) {
     return a;
 }
 
-// Execute a BlkStream sweep on x (rhs: separate vector, or x itself).
+// Execute a BlkStream sweep on x (rhs: separate vector, or x itself), block
+// by block in the device's order: old sums (per worker part), fresh sums,
+// dense block inverse.
 static void run_blk(const BlkStream& bs, std::vector<double>& x, const std::vector<double>& rhs) {
-    const int n = bs.n;
+    const int n = bs.n, P = bs.parts;
     x.resize(n + 1);
     x[n] = 0.0;
     for (int k = 0; k < bs.n_blocks; ++k) {
-        const unsigned char* u = bs.stream.data() + static_cast<size_t>(bs.table[2 * k]) * 16;
+        const unsigned char* u = bs.stream.data() + static_cast<size_t>(bs.table[4 * k]) * 16;
         int hdr[4];
         std::memcpy(hdr, u, sizeof hdr);
-        const int mo = hdr[0], mf = hdr[1];
-        if (hdr[2] != bs.table[2 * k + 1]) throw std::runtime_error("unit size mismatch");
+        const int mo = hdr[0], mf = hdr[3];
+        if (hdr[2] != bs.table[4 * k + 1] || hdr[3] != bs.table[4 * k + 2]) throw std::runtime_error("unit size mismatch");
         const int* rows = reinterpret_cast<const int*>(u + 16);
-        const int* oc = reinterpret_cast<const int*>(u + 144);
-        const double* ov = reinterpret_cast<const double*>(u + 144 + 128 * mo);
-        const int* fc = reinterpret_cast<const int*>(u + 144 + 384 * mo);
-        const double* fv = reinterpret_cast<const double*>(u + 144 + 384 * mo + 128 * mf);
-        const double* iv = reinterpret_cast<const double*>(u + 144 + 384 * (mo + mf));
+        const double* iv = reinterpret_cast<const double*>(u + kBlkInvOff);
+        const unsigned char* fr = u + kBlkFreshOff;
         double t[32], z[32];
-        for (int l = 0; l < 32; ++l) {  // old sums (final or not-yet-updated columns)
+        for (int l = 0; l < 32; ++l) {
             double s = 0.0;
-            for (int q = 0; q < mo; ++q) s += ov[q * 32 + l] * x[oc[q * 32 + l]];
+            for (int p = 0; p < P; ++p) {  // worker parts
+                const int* oc = reinterpret_cast<const int*>(u + kBlkFreshOff + 512 * mf + p * 384 * mo);
+                const double* ov = reinterpret_cast<const double*>(oc + 32 * mo);
+                for (int q = 0; q < mo; ++q) s += ov[q * 32 + l] * x[oc[q * 32 + l]];
+            }
             t[l] = (rows[l] >= 0 ? rhs[rows[l]] : 0.0) - s;
         }
         for (int l = 0; l < 32; ++l)  // fresh sums
-            for (int q = 0; q < mf; ++q) t[l] -= fv[q * 32 + l] * x[fc[q * 32 + l]];
+            for (int q = 0; q < mf; ++q) {
+                int c;
+                double v;
+                std::memcpy(&c, fr + (q * 32 + l) * 16, 4);
+                std::memcpy(&v, fr + (q * 32 + l) * 16 + 8, 8);
+                t[l] -= v * x[c];
+            }
         for (int l = 0; l < 32; ++l) {
             z[l] = 0.0;
-            for (int j = 0; j <= l; ++j) z[l] += iv[32 * j - j * (j - 1) / 2 + (l - j)] * t[j];
+            for (int j = 0; j < 32; ++j) z[l] += iv[((j / 2) * 32 + l) * 2 + (j & 1)] * t[j];
         }
         for (int l = 0; l < 32; ++l)
             if (rows[l] >= 0) x[rows[l]] = z[l];
@@ -81,8 +90,7 @@ static double rel(const std::vector<double>& a, const std::vector<double>& b) {
 
 int main(int argc, char** argv) {
     const int m = argc > 1 ? std::atoi(argv[1]) : 40, w = argc > 2 ? std::atoi(argv[2]) : 3;
-    const int fresh = argc > 3 ? std::atoi(argv[3]) : 1;
-    const HostCsr a = stencil_matrix(m, w, 7);
+        const HostCsr a = stencil_matrix(m, w, 7);
     const int n = a.n_rows;
     HostCsr L, U;
     ilut_factor(a, 1e-13, 0, L, U);
@@ -100,9 +108,9 @@ int main(int argc, char** argv) {
         z[i] = s / U.values[U.row_offsets[i]];
     }
     std::vector<double> y = r;
-    run_blk(blk_lower(L, fresh), y, r);
+    run_blk(blk_lower(L), y, r);
     const std::vector<double> y1 = y;
-    run_blk(blk_upper(U, fresh), y, y1);
+    run_blk(blk_upper(U), y, y1);
     const double e_ilut = rel(y, z);
     // Gauss-Seidel forward and backward (solvers.hpp:80-99)
     double e_gs[2];
@@ -122,7 +130,7 @@ int main(int argc, char** argv) {
             xr[i] = acc / d;
         }
         xb = x0;
-        run_blk(blk_gauss_seidel(a, dir == 1, fresh), xb, r);
+        run_blk(blk_gauss_seidel(a, dir == 1), xb, r);
         e_gs[dir] = rel(xb, xr);
     }
     std::printf("n %d ilut %.3e gs_fwd %.3e gs_bwd %.3e\n", n, e_ilut, e_gs[0], e_gs[1]);
