@@ -84,6 +84,10 @@ struct DevHier {
     const double* coarse_lu;
     const int* coarse_piv;
     int coarse_n;
+    // reassociated mode: the W-cycle from h-level dense_level down (zero
+    // initial guess) as a dense n x n operator, column-major (-1: none)
+    int dense_level;
+    const double* dense_op;
     int nu_pre, nu_post, gs_pre, gs_post;
     double rel_tol;
     int max_iter;

@@ -256,6 +256,24 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     coarse = dense_lu_factor(stencil_to_csr(a_h.back()));
     coarse_lu = dev(coarse.lu, s);
     coarse_piv = dev(coarse.piv, s);
+    // Reassociated mode: below the first h-level with at most kDenseCoarseMax
+    // rows the W-cycle (zero initial guess, hence linear) is applied as one
+    // dense operator -- the latency-bound small sweeps and the serial LU
+    // become one data-parallel matvec.  Same cycle, different rounding.
+    if (!opt.exact && opt.dense_coarse_max > 0) {
+        const int nh = (int)a_h.size();
+        for (int l = 1; l + 1 < nh; ++l)
+            if (d.h[l].n <= opt.dense_coarse_max) {
+                std::vector<HostCsr> ah, eh;
+                for (int k = 0; k < nh; ++k) {
+                    ah.push_back(stencil_to_csr(a_h[k]));
+                    eh.push_back(d.h[k].E);
+                }
+                dense_op = dev(wcycle_operator(ah, eh, coarse, l, opt.gs_pre, opt.gs_post), s);
+                dense_level = l;
+                break;
+            }
+    }
     PHI_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -299,6 +317,8 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     H.coarse_lu = coarse_lu.get();
     H.coarse_piv = coarse_piv.get();
     H.coarse_n = coarse.n;
+    H.dense_level = dense_level;
+    H.dense_op = dense_op.get();
     H.nu_pre = opt.nu_pre;
     H.nu_post = opt.nu_post;
     H.gs_pre = opt.gs_pre;

@@ -69,6 +69,7 @@ struct HierOptions {  // PMultigridOptions (pmultigrid.hpp:161-168)
     int ilut_fill = 0;
     int nu_pre = 1, nu_post = 1, gs_pre = 2, gs_post = 2;
     int exact = 0;  // 1: the reference's summation order (bit-identical), 0: reassociated sums
+    int dense_coarse_max = 256;  // reassociated mode: dense W-cycle operator from the first h-level this small
 };
 
 struct SolverConfig {  // SpatialSolverConfig (theta.hpp:66-75), pmg kind
@@ -114,6 +115,8 @@ public:
     std::vector<BlkDev> gsb_dev;  // per h-level (but the coarsest): forward, backward
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;
+    int dense_level = -1;      // reassociated mode: W-cycle subtree collapsed to a dense operator
+    DevBuf<double> dense_op;
     DevBuf<int> coarse_piv;
 
     DevHier view(const SolverConfig& cfg) const;

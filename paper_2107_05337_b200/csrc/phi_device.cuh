@@ -97,6 +97,7 @@ __device__ __forceinline__ int lds_s32(unsigned a) {
 constexpr bool kTrace = PHI_TRACE_ON != 0;
 constexpr int kStampBase = 40000, kStampMax = 4000;
 constexpr int kTriTraceBase = 24000;  // 4 x 2048 stamps (< kStampBase)
+constexpr int kAccBase = 33000;       // developer phase accumulators (wcycle)
 __device__ __forceinline__ void pstamp(int id) {
     if (kTrace && c_tune.trace && blockIdx.x == 0 && threadIdx.x == 0) {
         const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(c_tune.trace + kStampBase), 1ULL);
@@ -926,6 +927,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 f[q & 7] = __fma_rn(vq, xld<XSM>(xg, xs, cq), f[q & 7]);
             }
             const double t = c - (((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+            if (tr) tr[7] = clock64() + (long long)(t == 1.2345);
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(t) : "memory");
             __syncwarp();
             double acc[8];
@@ -1220,6 +1222,25 @@ __device__ void coarse_solve(const DevHier& H, const double* b, double* x) {
     __syncthreads();
 }
 
+// x += C r for a dense column-major n x n operator (the collapsed coarse
+// W-cycle subtree).  Thread i owns row i; r is broadcast from shared or
+// global memory.
+__device__ __noinline__ void dense_apply(const double* __restrict__ c, int n, const double* b, double* x) {
+    for (int i = threadIdx.x; i < n; i += NT) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = 0;
+        for (; j + 4 <= n; j += 4) {
+            a0 = __fma_rn(__ldg(c + (size_t)j * n + i), b[j], a0);
+            a1 = __fma_rn(__ldg(c + (size_t)(j + 1) * n + i), b[j + 1], a1);
+            a2 = __fma_rn(__ldg(c + (size_t)(j + 2) * n + i), b[j + 2], a2);
+            a3 = __fma_rn(__ldg(c + (size_t)(j + 3) * n + i), b[j + 3], a3);
+        }
+        for (; j < n; ++j) a0 = __fma_rn(__ldg(c + (size_t)j * n + i), b[j], a0);
+        x[i] = x[i] + ((a0 + a1) + (a2 + a3));
+    }
+    __syncthreads();
+}
+
 // h-multigrid W-cycle (pmultigrid.hpp:184-200) as an explicit per-level
 // phase machine (no device recursion):
 //   phase 0: pre-smooth, restrict, first coarse visit
@@ -1228,6 +1249,18 @@ __device__ void coarse_solve(const DevHier& H, const double* b, double* x) {
 // Solution of level l lives in w.hx[l]; the result of level 0 is w.hx[0].
 template <int DEG>
 __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
+    // developer phase accounting (trace builds, CTA 0 thread 0): cycles per
+    // category at trace[kAccBase + c]: sweeps of level l (c = l), residual +
+    // restriction (20), prolongation (21), coarsest solve (22)
+    long long* acc = (kTrace && c_tune.trace && blockIdx.x == 0 && threadIdx.x == 0) ? c_tune.trace + kAccBase : nullptr;
+    long long ta = acc ? clock64() : 0;
+    auto mark = [&](int c) {
+        if (acc) {
+            const long long t = clock64();
+            acc[c] += t - ta;
+            ta = t;
+        }
+    };
     int phase[kMaxH];
     int l = 0;
     phase[0] = 0;
@@ -1238,7 +1271,21 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
     __syncthreads();
     for (;;) {
         if (l + 1 == H.n_h) {
+            mark(23);
             coarse_solve(H, w.hb[l], w.hx[l]);
+            mark(22);
+            if (l == 0) break;
+            --l;
+            continue;
+        }
+        if (l == H.dense_level && phase[l] == 0) {
+            // the subtree from level l, a linear iteration: x += C (b - A x)
+            // (C: the cycle from a zero guess; x is zero on the first visit)
+            mark(23);
+            stencil_apply<kOutResid, Widths<DEG>::H>(H.h[l].a, w.hx[l], w.hr[l], w.hb[l], false);
+            __syncthreads();
+            dense_apply(H.dense_op, H.h[l].n, w.hr[l], w.hx[l]);
+            mark(22);
             if (l == 0) break;
             --l;
             continue;
@@ -1248,27 +1295,33 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         double* x = w.hx[l];
         const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + lv.n : -1;
         if (phase[l] == 0) {
+            mark(23);
             if (H.exact)
                 gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
             else
                 blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            mark(l);
             stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b, H.exact != 0);
             __syncthreads();
             csr_apply<false>(lv.embed_t, w.hr[l], w.hb[l + 1]);  // rc = E^T r
             cta_fill(w.hx[l + 1], 0.0, H.h[l + 1].n);              // ec = 0
             __syncthreads();
+            mark(20);
             phase[l] = 1;
             phase[++l] = 0;
         } else if (phase[l] == 1) {
             phase[l] = 2;
             phase[++l] = 0;
         } else {
+            mark(23);
             csr_apply<true>(lv.embed, w.hx[l + 1], x);  // x += E ec
             __syncthreads();
+            mark(21);
             if (H.exact)
                 gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
             else
                 blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            mark(l);
             if (l == 0) break;
             --l;
         }

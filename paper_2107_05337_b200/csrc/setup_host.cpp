@@ -357,6 +357,73 @@ DenseLUHost dense_lu_factor(const HostCsr& a) {
 }
 
 namespace {
+void host_spmv(const HostCsr& a, const double* x, double* y) {
+    for (int i = 0; i < a.n_rows; ++i) {
+        double acc = 0.0;
+        for (int k = a.row_offsets[i]; k < a.row_offsets[i + 1]; ++k) acc += a.values[k] * x[a.col_indices[k]];
+        y[i] = acc;
+    }
+}
+void host_gs(const HostCsr& a, const double* b, double* x, bool backward) {  // solvers.hpp:80-99
+    const int n = a.n_rows;
+    for (int s = 0; s < n; ++s) {
+        const int i = backward ? n - 1 - s : s;
+        double acc = b[i], d = 0.0;
+        for (int k = a.row_offsets[i]; k < a.row_offsets[i + 1]; ++k) {
+            if (a.col_indices[k] == i)
+                d = a.values[k];
+            else
+                acc -= a.values[k] * x[a.col_indices[k]];
+        }
+        x[i] = acc / d;
+    }
+}
+void host_lu_solve(const DenseLUHost& f, const double* b, double* x) {  // solvers.hpp:118-133
+    const int n = f.n;
+    for (int i = 0; i < n; ++i) x[i] = b[f.piv[i]];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < i; ++j) x[i] -= f.lu[static_cast<size_t>(i) * n + j] * x[j];
+    for (int i = n - 1; i >= 0; --i) {
+        for (int j = i + 1; j < n; ++j) x[i] -= f.lu[static_cast<size_t>(i) * n + j] * x[j];
+        x[i] /= f.lu[static_cast<size_t>(i) * n + i];
+    }
+}
+void host_wcycle(const std::vector<HostCsr>& a, const std::vector<HostCsr>& e, const DenseLUHost& coarse, int l,
+                 int gs_pre, int gs_post, const double* b, double* x) {
+    if (l + 1 == static_cast<int>(a.size())) {
+        host_lu_solve(coarse, b, x);
+        return;
+    }
+    const int n = a[l].n_rows, nc = e[l].n_cols;
+    for (int s = 0; s < gs_pre; ++s) host_gs(a[l], b, x, false);
+    std::vector<double> r(n), rc(nc, 0.0), ec(nc, 0.0);
+    host_spmv(a[l], x, r.data());
+    for (int i = 0; i < n; ++i) r[i] = b[i] - r[i];
+    for (int i = 0; i < n; ++i)  // rc = E^T r
+        for (int k = e[l].row_offsets[i]; k < e[l].row_offsets[i + 1]; ++k) rc[e[l].col_indices[k]] += e[l].values[k] * r[i];
+    host_wcycle(a, e, coarse, l + 1, gs_pre, gs_post, rc.data(), ec.data());
+    host_wcycle(a, e, coarse, l + 1, gs_pre, gs_post, rc.data(), ec.data());
+    host_spmv(e[l], ec.data(), r.data());
+    for (int i = 0; i < n; ++i) x[i] += r[i];
+    for (int s = 0; s < gs_post; ++s) host_gs(a[l], b, x, true);
+}
+}  // namespace
+
+std::vector<double> wcycle_operator(const std::vector<HostCsr>& a, const std::vector<HostCsr>& e,
+                                    const DenseLUHost& coarse, int lc, int gs_pre, int gs_post) {
+    const int n = a.at(lc).n_rows;
+    std::vector<double> c(static_cast<size_t>(n) * n), b(n), x(n);
+    for (int j = 0; j < n; ++j) {
+        std::fill(b.begin(), b.end(), 0.0);
+        std::fill(x.begin(), x.end(), 0.0);
+        b[j] = 1.0;
+        host_wcycle(a, e, coarse, lc, gs_pre, gs_post, b.data(), x.data());
+        std::copy(x.begin(), x.end(), c.begin() + static_cast<size_t>(j) * n);
+    }
+    return c;
+}
+
+namespace {
 
 // Row view of a level-scheduled sweep: row i's dependency columns, its
 // summed entries (columns ascending = the reference's order) and, for a

@@ -61,6 +61,15 @@ struct DenseLUHost {
 };
 DenseLUHost dense_lu_factor(const HostCsr& a);
 
+/// Operator of the order-1 h-multigrid W-cycle (pmultigrid.hpp:184-200) from
+/// level `lc` down, applied to a zero initial guess: the cycle is then linear
+/// in its right-hand side, x = C b.  Returned column-major (C[j * n + i] =
+/// (C e_j)_i), n = a[lc].n_rows.  a: the level matrices, e: the embeddings
+/// (e[l]: level l+1 -> level l), coarse: the dense LU of the coarsest level.
+/// Host restatement of the same cycle the device runs (setup only).
+std::vector<double> wcycle_operator(const std::vector<HostCsr>& a, const std::vector<HostCsr>& e,
+                                    const DenseLUHost& coarse, int lc, int gs_pre, int gs_post);
+
 /// Level schedule of a triangular factor.  Rows of one level depend only on
 /// rows of earlier levels.  A level is split into chunks of <= kTriRows rows
 /// (one lane of the solving warp each) and <= kTriBlockCap bytes.  Entry e of
