@@ -875,6 +875,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
         // ---- solver warps 0 / 1 take blocks g = w, w + 2, ...  The parts'
         // count implies the block's unit has landed (each worker waited).
         const unsigned tb = sh_addr(sy.tb[w]);
+        const int xn = T.n;  // the zero slot x[n]
         int slot = w, k = w;
         int4 info = w < total ? __ldg(table + w) : make_int4(0, 0, 0, 0);  // (off16, bytes, mf, 0)
         for (int g = w; g < total; g += 2) {
@@ -902,25 +903,27 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
 #pragma unroll
             for (int p2 = 0; p2 < 16; ++p2) lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
             const unsigned fr = u + kBlkFreshOff + 16u * lane;
-            int fc[8];
-            double fv[8];
+            constexpr int FB = 16;  // fresh slots held in registers (the rest: rare)
+            int fc[FB];
+            double fv[FB];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < FB; ++q) {
+                fc[q] = xn;
+                fv[q] = 0.0;
                 if (q < mf) lds_slot(fr + 512u * q, fc[q], fv[q]);
-                else {
-                    fc[q] = T.n;
-                    fv[q] = 0.0;
-                }
             }
             const double c = rhs - (((part[0] + part[1]) + (part[2] + part[3])) + (part[4] + part[5]));
             // ---- wait for block g-1 (the other solver)
             if (g > 0) hand_wait(kHandBar + (w ^ 1));
             if (tr) tr[2] = clock64();
             // ---- the chain: fresh columns of block g-1, broadcast, inverse
+            double xf[FB];
+#pragma unroll
+            for (int q = 0; q < FB; ++q) xf[q] = q < mf ? xld<XSM>(xg, xs, fc[q]) : 0.0;
             double f[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) f[q] = q < mf ? fv[q] * xld<XSM>(xg, xs, fc[q]) : 0.0;
-            for (int q = 8; q < mf; ++q) {  // rare: more than 8 fresh slots
+            for (int q = 0; q < 8; ++q) f[q] = __fma_rn(fv[q + 8], xf[q + 8], fv[q] * xf[q]);
+            for (int q = FB; q < mf; ++q) {  // rare: more than FB fresh slots
                 int cq;
                 double vq;
                 lds_slot(fr + 512u * q, cq, vq);

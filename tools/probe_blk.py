@@ -34,10 +34,10 @@ for name, f, n in [("ilut(U)", lambda: h.ilut_apply(b), d.n_free), ("gs0", lambd
     t0 = t[0, 0]
     per = np.diff(t[:, 3])
     print(f"{name}: nb {nb}, total {t[-1, 3] - t0} cyc, per block median {np.median(per):.0f} mean {per.mean():.0f}")
-    seg = {"cntwait": t[:, 1] - t[:, 0], "chain": t[:, 2] - t[:, 1], "publish": t[:, 3] - t[:, 2],
-           "gap_next": np.r_[t[1:, 0] - t[:-1, 3], 0],
+    seg = {"cntwait": t[:, 1] - t[:, 0], "pre+handwait": t[:, 2] - t[:, 1], "chain": t[:, 3] - t[:, 2], " fresh->t": t[:, 7] - t[:, 2], " t->done": t[:, 3] - t[:, 7],
+           "handoff(next start - done)": np.r_[t[1:, 2] - t[:-1, 3], 0],
            "wk_mbar_done->prog": t[:, 5] - t[:, 4], "wk_prog->cnt": t[:, 6] - t[:, 5],
-           "wk_cnt_vs_solver_wait": t[:, 6] - t[:, 0]}
+           "wk_cnt_vs_solver_cntwait": t[:, 6] - t[:, 0]}
     for kname, v in seg.items():
         print(f"   {kname:24s} median {np.median(v):8.0f}  mean {v.mean():8.0f}  max {v.max():8.0f}")
     print("   first blocks:", (t[:6] - t0).tolist())

@@ -38,3 +38,12 @@ show("vcycle_kernel", stamps())
 E.dev_tuning(8, 8, -1)
 h.solve(b, None, fixed_cycles=1)
 show("wave_kernel  ", stamps())
+
+import time
+E.dev_tuning(8, 8, 0)
+x0 = np.zeros(d.n_free)
+for reps in (1, 20):
+    t = time.perf_counter()
+    for _ in range(reps):
+        h.vcycle(b, x0)
+    print(f"vcycle wall {1e3 * (time.perf_counter() - t) / reps:.3f} ms/call (reps {reps})", flush=True)
