@@ -278,6 +278,35 @@ void launch_stencil_transpose(const DevStencil& a, double* out, cudaStream_t s) 
     PHI_CUDA(cudaGetLastError());
 }
 
+// Line Gauss-Seidel coefficients of a 9-point order-1 level (stencil planes
+// e = (dv + 1) * 3 + (du + 1), nf x nf rows): per row, forward then backward,
+// {alpha, f1, f2, f3} = {-a_inline / d, a_prev(-1) / d, a_prev(0) / d,
+// a_prev(+1) / d} (zero outside the grid), then 1 / d.  The in-line entry
+// is W (forward) / E (backward); the previous line is v-1 / v+1.
+__global__ void gs_line_coeffs_kernel(const double* __restrict__ a, int nf, double* out) {
+    const int n = nf * nf;
+    double4* fw = reinterpret_cast<double4*>(out);
+    double4* bw = fw + n;
+    double* rd = out + 8 * (size_t)n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int iv = i / nf, iu = i - iv * nf;
+        auto at = [&](int dv, int du) -> double {
+            const int u = iu + du, v = iv + dv;
+            return (u >= 0 && u < nf && v >= 0 && v < nf) ? a[(size_t)((dv + 1) * 3 + (du + 1)) * n + i] : 0.0;
+        };
+        const double d = at(0, 0), r = 1.0 / d;
+        fw[i] = make_double4(-at(0, -1) * r, at(-1, -1) * r, at(-1, 0) * r, at(-1, 1) * r);
+        bw[i] = make_double4(-at(0, 1) * r, at(1, -1) * r, at(1, 0) * r, at(1, 1) * r);
+        rd[i] = r;
+    }
+}
+
+void launch_gs_line_coeffs(const double* a, int nf, double* out, cudaStream_t s) {
+    const int n = nf * nf;
+    gs_line_coeffs_kernel<<<(n + 255) / 256, 256, 0, s>>>(a, nf, out);
+    PHI_CUDA(cudaGetLastError());
+}
+
 void launch_axpby(const double* a, double c, const double* b, double* out, size_t n, cudaStream_t s) {
     axpby_kernel<<<grid_for((long long)n), 256, 0, s>>>(a, c, b, out, n);
     PHI_CUDA(cudaGetLastError());

@@ -62,12 +62,20 @@ struct DevHLevel {
     DevStencil a;    // M_l + c K_l, 9-point
     DevTri gs_fwd, gs_bwd;  // Gauss-Seidel sweeps as level-scheduled streams (exact mode; empty on the coarsest)
     DevBlk gsb_fwd, gsb_bwd;  // the same sweeps as block recurrences (reassociated mode)
+    // reassociated mode, nf <= kLineMax: line sweeps (gs_line_coeffs_kernel
+    // layout: double4 forward[n], double4 backward[n], double rd[n]); null: none
+    const double* gsl;
+    int nf;
     DevCsr embed;    // level l+1 -> level l (empty on the coarsest)
     DevCsr embed_t;  // its transpose (restriction rows, ascending fine index)
     int n;
 };
 
 constexpr int kMaxH = 12;
+/// Longest grid line of a line Gauss-Seidel sweep (32 lanes x 8 rows).
+constexpr int kLineMax = 256;
+/// Shortest grid line swept by lines (shorter levels: block sweeps).
+constexpr int kLineMin = 48;
 
 /// One p-multigrid hierarchy (PMultigridHierarchy, pmultigrid.hpp:215-324)
 /// plus the spatial solver settings of its ThetaStepper (theta.hpp:66-75).

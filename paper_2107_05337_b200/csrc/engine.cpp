@@ -252,6 +252,11 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
                 upload_blk(blk_gauss_seidel(al, dir == 1), gsb_dev.back(), s);
             }
         }
+        gsl_dev.emplace_back();
+        if (!opt.exact && d.h[l].nf <= kLineMax && d.h[l].nf >= kLineMin) {
+            gsl_dev.back().alloc((size_t)9 * d.h[l].n);
+            launch_gs_line_coeffs(a_h[l].vals.get(), d.h[l].nf, gsl_dev.back().get(), s);
+        }
     }
     coarse = dense_lu_factor(stencil_to_csr(a_h.back()));
     coarse_lu = dev(coarse.lu, s);
@@ -307,7 +312,9 @@ DevHier Hier::view(const SolverConfig& cfg) const {
         } else if (l + 1 < H.n_h) {
             H.h[l].gsb_fwd = gsb_dev[2 * l].view();
             H.h[l].gsb_bwd = gsb_dev[2 * l + 1].view();
+            H.h[l].gsl = gsl_dev[l].get();
         }
+        H.h[l].nf = hl.nf;
         H.h[l].n = hl.n;
         if (l + 1 < H.n_h) {
             H.h[l].embed = DevCsr{hl.E.n_rows, hl.E.n_cols, hl.e_ro.get(), hl.e_ci.get(), hl.e_v.get()};

@@ -113,6 +113,7 @@ public:
         DevBlk view() const;
     } Lbd, Ubd;
     std::vector<BlkDev> gsb_dev;  // per h-level (but the coarsest): forward, backward
+    std::vector<DevBuf<double>> gsl_dev;  // per h-level: line Gauss-Seidel coefficients (reassociated mode)
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;
     int dense_level = -1;      // reassociated mode: W-cycle subtree collapsed to a dense operator

@@ -1225,6 +1225,176 @@ __device__ void coarse_solve(const DevHier& H, const double* b, double* x) {
     __syncthreads();
 }
 
+// Lexicographic Gauss-Seidel sweeps of a 9-point order-1 level along grid
+// lines (reassociated mode; solvers.hpp:80-99 restated per line).  For a
+// forward sweep the row (iu, v) reads new values of its west neighbour and of
+// line v-1, old values of its east neighbour and of line v+1:
+//   1. prologue, all threads: o_i = (b_i - sum_old a_ij x_j) / d_i;
+//   2. warp 0, line by line: beta_i = o_i - sum_{prev line} (a_ij / d_i) x_j,
+//      then the in-line recurrence x_i = beta_i + alpha_i x_{i-1} (alpha =
+//      -a_W / d) as a warp scan of affine maps (R = ceil(nf / 32) rows per
+//      lane, composed locally first).  The next line's o and coefficients are
+//      loaded while the current line is solved.
+// A backward sweep mirrors both orders (lines v descending, iu descending).
+template <bool SM, int RM>
+__device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double* b, double* x, double* o,
+                                              bool backward, int count) {
+    // SM: x and o in shared memory (explicit shared accesses on the chain)
+    const unsigned xs = SM ? sh_addr(x) : 0u, os = SM ? sh_addr(o) : 0u;
+    auto ldx = [&](int j) -> double { return SM ? vlds_f64(xs + 8u * j) : x[j]; };
+    // RM: rows per lane (compile time), R = RM
+    const int nf = lv.nf, n = nf * nf;
+    constexpr int R = RM;
+    const double* __restrict__ a = lv.a.vals;
+    const double4* __restrict__ cf = reinterpret_cast<const double4*>(lv.gsl) + (backward ? n : 0);
+    const double* __restrict__ rd = lv.gsl + 8 * (size_t)n;
+    const int sv = backward ? 1 : -1;  // the previous line in sweep order is v + sv
+    for (int c = 0; c < count; ++c) {
+        // ---- 1. old part, scaled by 1/d
+        constexpr int U = 4;  // rows per thread and pass: independent loads in flight
+        for (int i0 = threadIdx.x; i0 < n; i0 += U * NT) {
+            double acc[U], sc[U];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const int i = min(i0 + uu * NT, n - 1);
+                const int iv = i / nf, iu = i - iv * nf;
+                double t = b[i];
+                // forward: E, NW, N, NE (old); backward: W, SW, S, SE
+                const int du_in = backward ? -1 : 1, dv = -sv;
+                const int u1 = iu + du_in;
+                if (u1 >= 0 && u1 < nf) t -= a[(size_t)(4 + du_in) * n + i] * x[i + du_in];
+                const int v1 = iv + dv;
+                if (v1 >= 0 && v1 < nf) {
+#pragma unroll
+                    for (int du = -1; du <= 1; ++du) {
+                        const int u = iu + du;
+                        if (u >= 0 && u < nf) t -= a[(size_t)((dv + 1) * 3 + du + 1) * n + i] * x[i + dv * nf + du];
+                    }
+                }
+                acc[uu] = t;
+                sc[uu] = rd[i];
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu)
+                if (i0 + uu * NT < n) o[i0 + uu * NT] = acc[uu] * sc[uu];
+        }
+        __syncthreads();
+        // ---- 2. the line chain
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            double on[RM];
+            double4 cn[RM];
+            auto load_line = [&](int q) {
+                const int v = backward ? nf - 1 - q : q;
+#pragma unroll
+                for (int r = 0; r < RM; ++r) {
+                    const int p = lane * R + r;
+                    if (p < nf) {
+                        const int i = v * nf + (backward ? nf - 1 - p : p);
+                        on[r] = SM ? vlds_f64(os + 8u * i) : o[i];
+                        const double2* c2 = reinterpret_cast<const double2*>(cf + i);
+                        const double2 lo = __ldg(c2), hi = __ldg(c2 + 1);
+                        cn[r] = make_double4(lo.x, lo.y, hi.x, hi.y);
+                    } else {
+                        on[r] = 0.0;
+                        cn[r] = make_double4(0.0, 0.0, 0.0, 0.0);
+                    }
+                }
+            };
+            load_line(0);
+            for (int q = 0; q < nf; ++q) {
+                long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && q < 1024)
+                                    ? c_tune.trace + kTriTraceBase + 8 * q
+                                    : nullptr;
+                if (tr) tr[0] = clock64();
+                const int v = backward ? nf - 1 - q : q, vp = v + sv;
+                double oc[RM];
+                double4 cc[RM];
+#pragma unroll
+                for (int r = 0; r < RM; ++r) {
+                    oc[r] = on[r];
+                    cc[r] = cn[r];
+                }
+                if (q + 1 < nf) load_line(q + 1);
+                // beta: fresh entries of the previous line (zero coefficients
+                // outside the grid; clamped addresses)
+                double bl[RM], al[RM];
+#pragma unroll
+                for (int r = 0; r < RM; ++r) {
+                    const int p = lane * R + r;
+                    const int iu = backward ? nf - 1 - p : p;
+                    double beta = oc[r];
+                    if (q > 0 && p < nf) {
+                        const int j0 = vp * nf + iu;
+                        const double xm = ldx(j0 - (iu > 0)), x0 = ldx(j0), xq = ldx(j0 + (iu + 1 < nf));
+                        beta = beta - ((cc[r].y * xm + cc[r].z * x0) + cc[r].w * xq);
+                    }
+                    bl[r] = beta;
+                    al[r] = cc[r].x;
+                }
+                if (tr) tr[1] = clock64() + (long long)(bl[0] == 1.2345) + (long long)(al[0] == 1.5);
+                // in-line recurrence: compose the lane's rows, scan the lanes
+                double B = bl[0], A = al[0];
+#pragma unroll
+                for (int r = 1; r < RM; ++r) {
+                    B = __fma_rn(al[r], B, bl[r]);
+                    A = al[r] * A;
+                    bl[r] = B;
+                    al[r] = A;
+                }
+                double Bs = B, As = A;
+#pragma unroll
+                for (int sft = 1; sft < 32; sft <<= 1) {
+                    const double Bp = __shfl_up_sync(0xffffffffu, Bs, sft), Ap = __shfl_up_sync(0xffffffffu, As, sft);
+                    if (lane >= sft) {
+                        Bs = __fma_rn(As, Bp, Bs);
+                        As = As * Ap;
+                    }
+                }
+                double prev = __shfl_up_sync(0xffffffffu, Bs, 1);
+                if (lane == 0) prev = 0.0;
+                if (tr) tr[2] = clock64() + (long long)(prev == 1.2345);
+#pragma unroll
+                for (int r = 0; r < RM; ++r) {
+                    const int p = lane * R + r;
+                    if (p < nf) {
+                        const double xval = r + 1 == R ? Bs : __fma_rn(al[r], prev, bl[r]);
+                        const int j = v * nf + (backward ? nf - 1 - p : p);
+                        if (SM)
+                            asm volatile("st.shared.f64 [%0], %1;" ::"r"(xs + 8u * j), "d"(xval) : "memory");
+                        else
+                            x[j] = xval;
+                    }
+                }
+                __syncwarp();
+                if (tr) tr[3] = clock64();
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int RM>
+__device__ __forceinline__ void gs_line_sweeps_r(const DevHLevel& lv, const double* b, double* x, double* o,
+                                                 bool backward, int count) {
+    if (__isShared(x) && __isShared(o))
+        gs_line_sweeps_t<true, RM>(lv, b, x, o, backward, count);
+    else
+        gs_line_sweeps_t<false, RM>(lv, b, x, o, backward, count);
+}
+__device__ __forceinline__ void gs_line_sweeps(const DevHLevel& lv, const double* b, double* x, double* o,
+                                               bool backward, int count) {
+    const int r = (lv.nf + 31) / 32;
+    if (r <= 1)
+        gs_line_sweeps_r<1>(lv, b, x, o, backward, count);
+    else if (r <= 2)
+        gs_line_sweeps_r<2>(lv, b, x, o, backward, count);
+    else if (r <= 4)
+        gs_line_sweeps_r<4>(lv, b, x, o, backward, count);
+    else
+        gs_line_sweeps_r<8>(lv, b, x, o, backward, count);
+}
+
 // x += C r for a dense column-major n x n operator (the collapsed coarse
 // W-cycle subtree).  Thread i owns row i; r is broadcast from shared or
 // global memory.
@@ -1301,6 +1471,8 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             mark(23);
             if (H.exact)
                 gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+            else if (lv.gsl)
+                gs_line_sweeps(lv, b, x, w.hr[l], false, H.gs_pre);
             else
                 blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
             mark(l);
@@ -1322,6 +1494,8 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             mark(21);
             if (H.exact)
                 gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+            else if (lv.gsl)
+                gs_line_sweeps(lv, b, x, w.hr[l], true, H.gs_post);
             else
                 blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
             mark(l);
@@ -1583,6 +1757,8 @@ __global__ void __launch_bounds__(NT, 1)
         const int bo = w.lvl_off[arg], xo = bo >= 0 ? bo + lv.n : -1;
         if (H.exact)
             gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+        else if (lv.gsl)
+            gs_line_sweeps(lv, w.hb[arg], w.hx[arg], w.hr[arg], arg2 != 0, 1);
         else
             blk_sweep(arg2 ? lv.gsb_bwd : lv.gsb_fwd, 1, w.hx[arg], xo, w.hb[arg], bo, w.ring_off, w.gs_slot_bytes,
                       w.gs_n_slots);

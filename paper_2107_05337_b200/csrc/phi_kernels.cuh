@@ -88,6 +88,8 @@ void launch_assemble_transfer(const DevTables1D& tu, const DevTables1D& tv, cons
 void launch_stencil_transpose(const DevStencil& a, double* out, cudaStream_t s);
 /// out = a + c * b elementwise (sparse_add on a shared pattern, sparse.hpp:148-178).
 void launch_axpby(const double* a, double c, const double* b, double* out, size_t n, cudaStream_t s);
+/// Line Gauss-Seidel coefficients of a 9-point order-1 level (9 n doubles).
+void launch_gs_line_coeffs(const double* a, int nf, double* out, cudaStream_t s);
 /// Load vector (assembly.hpp:365-371 + restrict_vector) for free dofs.
 /// kind: 0 constant(c0); 1 ((c0 * c1) * sx) * sy  [amp * exp(-t) * sin * sin];
 /// 2 (c0 * sx) * sy [amp * sin * sin]; 3 sx * sy; 4 spline with free coeffs.
