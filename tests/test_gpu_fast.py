@@ -99,3 +99,21 @@ def test_fast_and_exact_modes_agree_on_config2_shape():
     rf, re_ = fast.solve(), exact.solve()
     assert abs(rf.iterations - re_.iterations) <= 1
     assert _rel(fast.trajectory(), exact.trajectory()) <= TOL_TRAJ
+
+
+@pytest.mark.parametrize("p,k,nt,m", [(4, 7, 32, 4), (5, 8, 16, 8)])
+def test_fast_and_exact_modes_agree_on_config3_4_shapes(p, k, nt, m):
+    """Config-3 / config-4 operators (p=4 h=2^-7; p=5 h=2^-8) at reduced Nt:
+    the large-grid paths (global-memory vectors, 4- and 8-row line scans, big
+    triangular blocks, the dense coarse operator) against the exact mode,
+    which is bit-identical to the reference."""
+    coeffs = np.random.default_rng(12345).uniform(-1, 1, (2 ** k + p - 2) ** 2)
+    kw = dict(cycle=E.CYCLE_TWO_LEVEL, m=m, source_kind=E.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2,
+              init_kind=E.INIT_COEFFS, init_coeffs=coeffs)
+    d = E.SpatialDiscretization.build(p, k)
+    fast, exact = E.MgritSolver(d, nt, **kw), E.MgritSolver(d, nt, exact=True, **kw)
+    rf, re_ = fast.solve(), exact.solve()
+    assert rf.converged and re_.converged
+    assert abs(rf.iterations - re_.iterations) <= 1
+    assert abs(rf.mean_spatial_iterations - re_.mean_spatial_iterations) <= 1.0
+    assert _rel(fast.trajectory(), exact.trajectory()) <= TOL_TRAJ
