@@ -829,7 +829,7 @@ __device__ __forceinline__ void lds_slot(unsigned a, int& c, double& v) {  // {i
 
 struct __align__(16) BlkSync {
     double cbuf[kBlkHand][kBlkMaxParts][32];  // workers' partial old sums
-    double tb[2][32];                         // per-solver broadcast of t (16-byte aligned)
+    double tb[kBlkSolvers][32];               // per-solver broadcast of t (16-byte aligned)
     unsigned long long bar[kBlkMaxSlots];
     int phase[kBlkMaxSlots];  // phases completed per slot since the kernel started
     int cnt[kBlkHand];
@@ -856,7 +856,7 @@ __device__ __forceinline__ void blk_init() {
 // named barriers of the solver hand-off: block g done -> solver (g + 1) % 2
 __device__ __forceinline__ void hand_wait(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void hand_signal(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
-constexpr int kHandBar = 1;  // ids 1, 2
+constexpr int kHandBar = 1;  // ids 1 .. kBlkSolvers
 
 template <bool XSM, bool RSM>
 __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg, int x_off, const double* rg,
@@ -871,20 +871,31 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
     const unsigned prog = sh_addr(&sy.prog), cnt = sh_addr(sy.cnt), cbuf = sh_addr(sy.cbuf);
     const unsigned char* __restrict__ stream = T.stream;
     const int4* __restrict__ table = T.table;
-    if (w < 2) {
-        // ---- solver warps 0 / 1 take blocks g = w, w + 2, ...  The parts'
+    constexpr int NS = kBlkSolvers, F = kBlkFresh;
+    if (w < NS) {
+        // ---- solver warps 0 .. NS-1 take blocks g = w, w + NS, ...  The parts'
         // count implies the block's unit has landed (each worker waited).
         const unsigned tb = sh_addr(sy.tb[w]);
         const int xn = T.n;  // the zero slot x[n]
-        int slot = w, k = w;
-        int4 info = w < total ? __ldg(table + w) : make_int4(0, 0, 0, 0);  // (off16, bytes, mf, 0)
-        for (int g = w; g < total; g += 2) {
+        int slot = w % n_slots, k = w % nb;
+        int4 info = w < total ? __ldg(table + k) : make_int4(0, 0, 0, 0);  // (off16, bytes, mf, 0)
+        int4 refill_next = make_int4(0, 0, 0, 0);
+        if (lane == 0 && w + n_slots < total) refill_next = __ldg(table + (k + n_slots) % nb);
+        for (int g = w; g < total; g += NS) {
             const int mf = info.z;
-            int kn2 = k + 2;  // this solver's next block
+            int kn2 = k + NS;  // this solver's next block
             while (kn2 >= nb) kn2 -= nb;
-            if (g + 2 < total) info = __ldg(table + kn2);
-            long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && g < 1024)
-                                ? c_tune.trace + kTriTraceBase + 8 * g
+            if (g + NS < total) info = __ldg(table + kn2);
+            // the unit that refills this block's slot after the block: its
+            // table entry was loaded one turn earlier (no L2 latency here)
+            const int4 refill = refill_next;
+            if (lane == 0 && g + NS + n_slots < total) {
+                int kn = kn2 + n_slots;
+                while (kn >= nb) kn -= nb;
+                refill_next = __ldg(table + kn);
+            }
+            long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && g < 512)
+                                ? c_tune.trace + kTriTraceBase + 16 * g
                                 : nullptr;
             if (tr) tr[0] = clock64();
             const int seen = wait_ge(cnt + 4u * (g & (kBlkHand - 1)), P);
@@ -912,9 +923,12 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 fv[q] = 0.0;
                 if (q < mf) lds_slot(fr + 512u * q, fc[q], fv[q]);
             }
-            const double c = rhs - (((part[0] + part[1]) + (part[2] + part[3])) + (part[4] + part[5]));
+            double old = 0.0;
+#pragma unroll
+            for (int q = 0; q < kBlkMaxParts; ++q) old = old + part[q];
+            const double c = rhs - old;
             // ---- wait for block g-1 (the other solver)
-            if (g > 0) hand_wait(kHandBar + (w ^ 1));
+            if (g > 0) hand_wait(kHandBar + (w == 0 ? NS - 1 : w - 1));
             if (tr) tr[2] = clock64();
             // ---- the chain: fresh columns of block g-1, broadcast, inverse
             double xf[FB];
@@ -930,7 +944,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 f[q & 7] = __fma_rn(vq, xld<XSM>(xg, xs, cq), f[q & 7]);
             }
             const double t = c - (((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
-            if (tr) tr[7] = clock64() + (long long)(t == 1.2345);
+            if (tr) tr[3] = clock64() + (long long)(t == 1.2345);
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(t) : "memory");
             __syncwarp();
             double acc[8];
@@ -953,43 +967,45 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             __syncwarp();
             if (lane == 0) st_volatile_s32(prog, g);  // monotone: block g+1 starts after the hand-off
             if (g + 1 < total) hand_signal(kHandBar + w);
-            if (tr) tr[3] = clock64();
+            if (tr) tr[5] = clock64();
             // ---- off the chain: bookkeeping for this solver's next block
             if (lane == 0) {
                 st_volatile_s32(cnt + 4u * (g & (kBlkHand - 1)), 0);  // reused by block g + kBlkHand
-                if (g + n_slots < total) {  // block g's unit is consumed: refill its slot
-                    int kn = k + n_slots;
-                    while (kn >= nb) kn -= nb;
-                    const int4 e = __ldg(table + kn);
-                    bulk_fetch(ring + slot * slot_bytes, stream + (size_t)e.x * 16, e.y, bar + 8u * slot);
-                }
+                if (g + n_slots < total)  // block g's unit is consumed: refill its slot
+                    bulk_fetch(ring + slot * slot_bytes, stream + (size_t)refill.x * 16, refill.y, bar + 8u * slot);
             }
-            slot += 2;
-            if (slot >= n_slots) slot -= n_slots;
+            if (tr) tr[6] = clock64();
+            slot += NS;
+            while (slot >= n_slots) slot -= n_slots;
             k = kn2;
         }
-    } else if (w - 2 < P) {
-        // ---- worker q = w - 2: part q of every block's old sums
-        const int q = w - 2;
+    } else if (w - NS < P) {
+        // ---- worker q = w - NS: part q of every block's old sums
+        const int q = w - NS;
         int k = 0, s = 0, slot = 0, ph = 0;
         for (int g = 0; g < total; ++g) {
-            long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && q == 0 && g < 1024)
-                                ? c_tune.trace + kTriTraceBase + 8 * g
+            long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && q == 0 && g < 512)
+                                ? c_tune.trace + kTriTraceBase + 16 * g
                                 : nullptr;
-            // unit g was issued when block g - n_slots was done (n_slots >= 3;
-            // this worker saw prog >= g - 3 for its previous block)
+            // columns solved by blocks <= g-F-1 of this sweep; for a later
+            // sweep also the previous sweep's rows up to block k + lookahead
+            int need = g - F - 1;
+            if (s > 0) need = max(need, (s - 1) * nb + min(k + T.lookahead, nb - 1));
+            // unit g was issued when block g - n_slots was done: with
+            // n_slots >= F + 2 it is in flight already (this worker saw
+            // prog >= g - F - 2 for its previous block); a shallower ring
+            // waits for `need` first
+            if (n_slots < F + 2) wait_ge(prog, need);
             mbar_wait(bar + 8u * slot, (unsigned)(sy.phase[slot] + ph) & 1u);
-            if (tr) tr[4] = clock64();
+            if (tr) tr[8] = clock64();
             const unsigned u = ring + slot * slot_bytes;
             const int mo = vlds_s32(u), mf = vlds_s32(u + 12u);
             const unsigned oc = u + kBlkFreshOff + 512u * mf + 384u * mo * q + 4u * lane;
             const unsigned ov = oc + 128u * mo + 4u * lane;
-            // columns solved by blocks <= g-2 of this sweep; for a later sweep
-            // also the previous sweep's rows up to block k + lookahead
-            int need = g - 2;
-            if (s > 0) need = max(need, (s - 1) * nb + min(k + T.lookahead, nb - 1));
             double a0 = 0.0, a1 = 0.0;
-            if (mo <= 8) {  // the common case: every load issued before the wait
+            if (c_tune.xmask & 8) {  // developer timing: no old sums
+                wait_ge(prog, need);
+            } else if (mo <= 8) {  // the common case: every load issued before the wait
                 int c[8];
                 double v[8];
 #pragma unroll
@@ -997,16 +1013,18 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                     c[e] = e < mo ? vlds_s32(oc + 128u * e) : T.n;
                     v[e] = e < mo ? vlds_f64(ov + 256u * e) : 0.0;
                 }
+                if (tr) tr[9] = clock64();
                 wait_ge(prog, need);
-                if (tr) tr[5] = clock64();
+                if (tr) tr[10] = clock64();
                 double xv[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) xv[e] = e < mo ? xld<XSM>(xg, xs, c[e]) : 0.0;
                 a0 = __fma_rn(v[0], xv[0], v[1] * xv[1]) + __fma_rn(v[4], xv[4], v[5] * xv[5]);
                 a1 = __fma_rn(v[2], xv[2], v[3] * xv[3]) + __fma_rn(v[6], xv[6], v[7] * xv[7]);
             } else {
+                if (tr) tr[9] = clock64();
                 wait_ge(prog, need);
-                if (tr) tr[5] = clock64();
+                if (tr) tr[10] = clock64();
                 for (int e = 0; e < mo; e += 2) {
                     const int c0 = vlds_s32(oc + 128u * e), c1 = e + 1 < mo ? vlds_s32(oc + 128u * (e + 1)) : T.n;
                     const double v0 = vlds_f64(ov + 256u * e), v1 = e + 1 < mo ? vlds_f64(ov + 256u * (e + 1)) : 0.0;
@@ -1019,7 +1037,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                          : "memory");
             __syncwarp();
             if (lane == 0) atomicAdd(&sy.cnt[g & (kBlkHand - 1)], 1);
-            if (tr) tr[6] = clock64();
+            if (tr) tr[11] = clock64();
             if (++slot == n_slots) {
                 slot = 0;
                 ++ph;
@@ -1506,10 +1524,16 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
 }
 
 // x += S (b - A x), S = ILUT application (pmultigrid.hpp:311-316).
+// r_valid: w.r already holds b - A x for the current x (the solve loop's
+// residual check), so z = r is a copy -- the same values the product would
+// give, in both summation modes.
 template <int DEG>
-__device__ __noinline__ void smooth(const DevHier& H, const Ws& w) {
+__device__ __noinline__ void smooth(const DevHier& H, const Ws& w, bool r_valid = false) {
     pstamp(10);
-    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.z, w.b, H.exact != 0);  // z = r = b - A x
+    if (r_valid)
+        cta_copy(w.z, w.r, H.n_p);
+    else
+        stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.z, w.b, H.exact != 0);  // z = r = b - A x
     if (threadIdx.x == 0) w.z[H.n_p] = 0.0;                          // neutral padding slot
     __syncthreads();
     pstamp(11);
@@ -1522,8 +1546,8 @@ __device__ __noinline__ void smooth(const DevHier& H, const Ws& w) {
 
 // One V(nu_pre, nu_post) cycle (pmultigrid.hpp:256-267).
 template <int DEG>
-__device__ __noinline__ void vcycle(const DevHier& H, const Ws& w) {
-    for (int s = 0; s < H.nu_pre; ++s) smooth<DEG>(H, w);
+__device__ __noinline__ void vcycle(const DevHier& H, const Ws& w, bool r_valid = false) {
+    for (int s = 0; s < H.nu_pre; ++s) smooth<DEG>(H, w, r_valid && s == 0);
     stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0);
     __syncthreads();
     stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, w.r, w.hb[0], H.inv_l1, H.exact != 0);  // restrict_to_linear
@@ -1603,7 +1627,7 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
             conv = 1;
         } else {
             for (int it = 1; it <= H.max_iter; ++it) {
-                vcycle<DEG>(H, w);
+                vcycle<DEG>(H, w, true);  // w.r = b - A x from the residual check
                 rel = rel_residual<DEG>(H, w, bnorm, sh);
                 iters = it;
                 if (rel <= H.rel_tol) {

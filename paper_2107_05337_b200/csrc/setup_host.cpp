@@ -849,7 +849,7 @@ BlkStream make_blk_stream(const BlkRowsView& rv) {
                 const int pj = pos_of(cols[e]), kj = pj / kBlkRows;
                 if (pj < pos && kj == k) {
                     b.B[l][pj - k * kBlkRows] += vals[e];
-                } else if (pj < pos && kj == k - 1) {
+                } else if (pj < pos && kj >= k - kBlkFresh) {
                     b.frsh[l].emplace_back(cols[e], vals[e]);
                 } else {
                     b.olde[l].emplace_back(cols[e], vals[e]);

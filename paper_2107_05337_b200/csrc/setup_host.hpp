@@ -137,10 +137,10 @@ TriStream make_tri_stream(const TriPlan& p, bool fast);
 ///     x_{R_k} = B_k^{-1} (rhs - old - fresh),   B_k = D + (in-block lower part),
 /// with the dense inverse B_k^{-1} precomputed here.  Entries of a row are
 ///   in-block lower  -> folded into B_k;
-///   fresh           -> columns solved by block k-1 (summed on the critical
-///                      path, after block k-1);
-///   old             -> columns solved by blocks <= k-2 (final once block k-2
-///                      is done) or solved later (Gauss-Seidel's old values,
+///   fresh           -> columns solved by blocks k-F .. k-1 (summed on the
+///                      critical path, after block k-1);
+///   old             -> columns solved by blocks <= k-F-1 (final once block
+///                      k-F-1 is done) or solved later (Gauss-Seidel's old values,
 ///                      in-block ones included); summed ahead of time by the
 ///                      worker warps, split into `parts` interleaved parts.
 /// One block = one fetch unit (one cp.async.bulk):
@@ -156,7 +156,9 @@ TriStream make_tri_stream(const TriPlan& p, bool fast);
 constexpr int kBlkRows = 32;
 constexpr int kBlkInvOff = 144;
 constexpr int kBlkFreshOff = kBlkInvOff + 8 * kBlkRows * kBlkRows;
-constexpr int kBlkMaxParts = 6;
+constexpr int kBlkMaxParts = 6;  // worker warps (8 - kBlkSolvers)
+constexpr int kBlkSolvers = 2;   // solver warps in rotation
+constexpr int kBlkFresh = 1;     // fresh distance F: columns of blocks k-F .. k-1
 struct BlkStream {
     std::vector<unsigned char> stream;
     std::vector<int> table;  // 4 per block: offset / 16, bytes, fresh slots, 0
