@@ -27,9 +27,9 @@ print("blk  start  cnt   hand   t      z      sig    post | wk: unit  loads  pro
 for g in range(40, 52):
     r = t[g] - t0
     print(g, " ".join(f"{v:6d}" for v in r[:7]), "|", " ".join(f"{v:6d}" for v in r[8:12]))
-per = np.diff(t[:, 4])
+per = np.diff(t[:, 5])
 print("per block median", np.median(per[10:-10]))
-for nm, a, bb in [("cntwait", 0, 1), ("pre", 1, 2), ("fresh", 2, 3), ("inverse+store", 3, 4), ("signal", 4, 5), ("post", 5, 6),
+for nm, a, bb in [("cntwait", 0, 1), ("pre (y ready)", 1, 2), ("handwait", 2, 3), ("chain", 3, 5), ("post", 5, 6),
                   ("wk unit->loads", 8, 9), ("wk loads->prog", 9, 10), ("wk prog->cnt", 10, 11)]:
     v = t[10:-10, bb] - t[10:-10, a]
     print(f"  {nm:16s} median {np.median(v):7.0f}")
