@@ -40,6 +40,8 @@ CONFIGS = {
     "c2": dict(p=3, k=6, nt=1000, m=8, cycle=2, source_kind=1, source_param=2 * np.pi ** 2, init_kind=2),
     "c3": dict(p=4, k=7, nt=2500, m=4, cycle=0, source_kind=0, source_param=0.0, init_kind=2),
     "c4": dict(p=5, k=8, nt=10000, m=8, cycle=0, source_kind=1, source_param=2 * np.pi ** 2, init_kind=0),
+    # BASELINE.json configs[4]: kernel microbenchmark (SpMV/SpMM and one V(1,1)), p = 2..5, h = 2^-8
+    "c5": dict(p=5, k=8, c=1e-4),
 }
 SEED = 12345
 
@@ -222,6 +224,47 @@ def run_reference(args, cfg, name):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def run_c5(args, cfg):
+    """BASELINE config 5: A x for B in {1, 16, 64} right-hand sides (SpMV / SpMM
+    of A = M + 1e-4 K, p = 2..5, h = 2^-8) and one V(1,1) cycle from x0 = 0,
+    device-timed (CUDA events), L2 flushed between repetitions.  Algorithmic
+    bytes per SURVEY 8(d): SpMM 8 nnz(A) + 16 B n; V-cycle: matrix part
+    (wave_report's per-cycle model) + 37 x 8 B n per right-hand side."""
+    import paper_2107_05337_b200 as P
+    from paper_2107_05337_b200.engine import lib
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    lib().phi_set_device(local)
+    peak, peak_kind = peaks()
+    rows = []
+    for p in (2, 3, 4, 5):
+        d = P.SpatialDiscretization.build(p, cfg["k"])
+        h = P.PMultigridHierarchy(d, cfg["c"])
+        n = d.n_free
+        side = int(round(n ** 0.5))
+        nnz = (side * (2 * p + 1) - p * (p + 1)) ** 2
+        for b in (1, 16, 64):
+            ms = h.time_kernel(0, b, reps=max(3, args.steps))
+            by = 8 * nnz + b * 16 * n
+            rows.append({"p": p, "B": b, "kernel": "spmm", "us": ms * 1e3, "alg_MB": by / 1e6,
+                         "GBs": by / ms / 1e6, "frac": by / ms / 1e6 / peak})
+        for b in (1, 16, 64):
+            ms = h.time_kernel(1, b, reps=max(2, args.steps))
+            rows.append({"p": p, "B": b, "kernel": "vcycle", "us": ms * 1e3,
+                         "cycles_per_s": b / (ms * 1e-3)})
+    spmm5 = [r for r in rows if r["kernel"] == "spmm" and r["p"] == 5 and r["B"] == 1][0]
+    line = {"metric": "SpMV/SpMM HBM GB/s (config 5 kernel microbenchmark)", "value": spmm5["GBs"], "unit": "GB/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": 1, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1) right-hand sides)",
+            "config": {"workload": "config5: A x and one V(1,1) on A = M + 1e-4 K, p=2..5, h=2^-8, B in {1,16,64}",
+                       "l2": "flushed between repetitions (256 MB write)"},
+            "roofline": {"kernel": "spmv_kernel (p=5, B=1)", "bound": "hbm", "achieved": spmm5["GBs"], "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": spmm5["frac"], "traffic": None},
+            "table": rows}
+    print(json.dumps(line), flush=True)
+
+
 def run_phi(args, cfg, name):
     rank, world, local = dist_env()
     import torch
@@ -372,7 +415,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-    if args.impl == "reference":
+    if args.config == "c5":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 5 is a GPU kernel microbenchmark"}))
+        else:
+            run_c5(args, cfg)
+    elif args.impl == "reference":
         run_reference(args, cfg, args.config)
     else:
         run_phi(args, cfg, args.config)

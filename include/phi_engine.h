@@ -132,6 +132,15 @@ int phi_hier_vcycle(phi_hier* h, const double* b, double* x, int nrhs, long long
 int phi_hier_solve(phi_hier* h, const double* b, double* x, int nrhs, long long ld, double rel_tol,
                    int max_iter, int fixed_cycles, int x0_empty, int* iters, int* converged,
                    double* final_rel, int device_ptrs);
+/* Y = A_p X for nrhs in {1, 16, 32, 64} vectors at once (spmv, sparse.hpp:114-124,
+ * batched): X, Y are [n][nrhs] (right-hand sides contiguous); the SpMV / SpMM
+ * kernels (reassociated sums). device_ptrs as above. */
+int phi_hier_spmm(phi_hier* h, const double* x, double* y, int nrhs, int device_ptrs);
+/* Kernel microbenchmark (BASELINE config 5): average device time (CUDA events)
+ * of `reps` launches on seeded N(0,1) inputs -- which 0: the SpMM above,
+ * which 1: one V(nu_pre, nu_post) cycle (pmultigrid.hpp:256-267) from x0 = 0
+ * on nrhs right-hand sides (one CTA each).  flush_l2: write 256 MB between reps. */
+int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, double* ms_out);
 /* Building blocks for parity tests (single vector, host arrays):
  * op 0 y = A_p x; 1 z = ilut_apply(r); 2 r1 = restrict_to_linear(r);
  * 3 x += prolong_from_linear(e1) (x in/out); 4 x1 = hmg_wcycle(b1, x1);

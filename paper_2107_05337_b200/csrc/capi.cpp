@@ -2,6 +2,7 @@
 // reference's exception types onto status codes and keeps the message
 // thread-local, worded as the reference's exception text.
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -326,6 +327,74 @@ int phi_hier_solve(phi_hier* h, const double* b, double* x, int nrhs, long long 
             if (converged) converged[r] = hc[r];
             if (final_rel) final_rel[r] = hf[r];
         }
+    });
+}
+
+int phi_hier_spmm(phi_hier* h, const double* x, double* y, int nrhs, int device_ptrs) {
+    return guarded([&] {
+        const StencilBuf& A = h->h->A;
+        const size_t n = (size_t)A.ru * A.rv, len = n * (size_t)nrhs;
+        const double* At = h->h->a_tiled(h->s);
+        if (device_ptrs) {
+            launch_spmm(A.view(), At, x, y, nrhs, h->s);
+        } else {
+            DevBuf<double> dx(len), dy(len);
+            PHI_CUDA(cudaMemcpyAsync(dx.get(), x, sizeof(double) * len, cudaMemcpyHostToDevice, h->s));
+            launch_spmm(A.view(), At, dx.get(), dy.get(), nrhs, h->s);
+            PHI_CUDA(cudaMemcpyAsync(y, dy.get(), sizeof(double) * len, cudaMemcpyDeviceToHost, h->s));
+        }
+        PHI_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, double* ms_out) {
+    return guarded([&] {
+        if (reps < 1 || nrhs < 1) throw InvalidArgument("phi_hier_time: reps and nrhs must be positive");
+        const StencilBuf& A = h->h->A;
+        const size_t n = (size_t)A.ru * A.rv, len = n * (size_t)nrhs;
+        // seeded N(0,1) right-hand sides (mt19937_64 + Box-Muller, portable)
+        std::vector<double> hb(len);
+        unsigned long long st = 0x9E3779B97F4A7C15ULL;
+        auto next = [&]() {
+            st ^= st >> 12;
+            st ^= st << 25;
+            st ^= st >> 27;
+            return (double)((st * 2685821657736338717ULL) >> 11) * (1.0 / 9007199254740992.0);
+        };
+        for (size_t i = 0; i < len; i += 2) {
+            const double u1 = std::max(next(), 1e-300), u2 = next();
+            const double r = std::sqrt(-2.0 * std::log(u1));
+            hb[i] = r * std::cos(2.0 * M_PI * u2);
+            if (i + 1 < len) hb[i + 1] = r * std::sin(2.0 * M_PI * u2);
+        }
+        DevBuf<double> b(len), x(len), flush;
+        PHI_CUDA(cudaMemcpyAsync(b.get(), hb.data(), sizeof(double) * len, cudaMemcpyHostToDevice, h->s));
+        if (flush_l2) flush.alloc((size_t)32 << 20);  // 256 MB > L2
+        SolverConfig cfg;
+        const DevHier H = h->h->view(cfg);
+        if (which == 1) h->ws.ensure(H);
+        cudaEvent_t e0, e1;
+        PHI_CUDA(cudaEventCreate(&e0));
+        PHI_CUDA(cudaEventCreate(&e1));
+        double total = 0.0;
+        for (int r = -1; r < reps; ++r) {  // r = -1: warm-up
+            if (flush_l2) PHI_CUDA(cudaMemsetAsync(flush.get(), r & 0xff, sizeof(double) * ((size_t)32 << 20), h->s));
+            if (which == 1) PHI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * len, h->s));  // x0 = 0
+            PHI_CUDA(cudaEventRecord(e0, h->s));
+            if (which == 0)
+                launch_spmm(A.view(), h->h->a_tiled(h->s), b.get(), x.get(), nrhs, h->s);  // X, Y: [n][nrhs]
+            else
+                launch_vcycle(H, b.get(), (long long)n, x.get(), (long long)n, nrhs, h->ws.buf.get(), h->ws.stride,
+                              h->ws.slots, h->s);
+            PHI_CUDA(cudaEventRecord(e1, h->s));
+            PHI_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            PHI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (r >= 0) total += ms;
+        }
+        PHI_CUDA(cudaEventDestroy(e0));
+        PHI_CUDA(cudaEventDestroy(e1));
+        *ms_out = total / reps;
     });
 }
 

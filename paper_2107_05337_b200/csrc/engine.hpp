@@ -117,6 +117,14 @@ public:
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;
     int dense_level = -1;      // reassociated mode: W-cycle subtree collapsed to a dense operator
+    DevBuf<double> a_tile;     // tiled copy of A for the streaming SpMV / SpMM (built on first use)
+    const double* a_tiled(cudaStream_t s) {
+        if (!a_tile.get()) {
+            a_tile.alloc(tile_doubles(A.view()));
+            launch_tile(A.view(), a_tile.get(), s);
+        }
+        return a_tile.get();
+    }
     DevBuf<double> dense_op;
     DevBuf<int> coarse_piv;
 

@@ -29,7 +29,8 @@ EXPORTED = [
     "phi_last_error", "phi_default_solver_config", "phi_default_mgrit_config", "phi_default_problem",
     "phi_device_count", "phi_set_device", "phi_synchronize", "phi_disc_build", "phi_disc_free",
     "phi_disc_info", "phi_disc_export", "phi_disc_vector", "phi_hier_create", "phi_hier_free",
-    "phi_hier_export", "phi_hier_vcycle", "phi_hier_solve", "phi_hier_unit", "phi_stepper_create",
+    "phi_hier_export", "phi_hier_vcycle", "phi_hier_solve", "phi_hier_unit", "phi_hier_spmm", "phi_hier_time",
+    "phi_stepper_create",
     "phi_stepper_free", "phi_stepper_step", "phi_sequential_integrate", "phi_mgrit_create",
     "phi_mgrit_free", "phi_mgrit_levels", "phi_mgrit_solve", "phi_mgrit_trajectory",
     "phi_mgrit_initial", "phi_mgrit_initialize", "phi_mgrit_cycle", "phi_mgrit_residual_norm",
@@ -108,6 +109,8 @@ def lib():
         L.phi_hier_vcycle.argtypes = [_vp, _vp, _vp, _i, _ll, _i]
         L.phi_hier_solve.argtypes = [_vp, _vp, _vp, _i, _ll, _d, _i, _i, _i, _vp, _vp, _vp, _i]
         L.phi_hier_unit.argtypes = [_vp, _i, _i, _i, _vp, _i, _vp, _i]
+        L.phi_hier_spmm.argtypes = [_vp, _vp, _vp, _i, _i]
+        L.phi_hier_time.argtypes = [_vp, _i, _i, _i, _i, _vp]
         L.phi_stepper_create.argtypes = [_vp, _d, _d, _d, _vp, _vp]
         L.phi_stepper_free.argtypes = [_vp]
         L.phi_stepper_free.restype = None
@@ -288,6 +291,22 @@ class PMultigridHierarchy:
         o = np.zeros(n_out) if out is None else np.array(out, dtype=np.float64, copy=True)
         _check(lib().phi_hier_unit(self.h, op, arg, arg2, _p(vin), vin.size, _p(o), o.size))
         return o
+
+    def spmm(self, X):
+        """Y = A_p X for X of shape (n, nrhs), nrhs in {1, 16, 32, 64} (batched
+        spmv, sparse.hpp:114-124; right-hand sides contiguous)."""
+        X = np.ascontiguousarray(X, np.float64)
+        nrhs = 1 if X.ndim == 1 else X.shape[1]
+        Y = np.empty_like(X)
+        _check(lib().phi_hier_spmm(self.h, _p(X), _p(Y), nrhs, 0))
+        return Y
+
+    def time_kernel(self, which: int, nrhs: int, reps: int = 5, flush_l2: bool = True) -> float:
+        """Average device ms of one SpMM (which 0) or one V-cycle from x0 = 0
+        (which 1) on nrhs seeded N(0,1) right-hand sides (BASELINE config 5)."""
+        ms = C.c_double()
+        _check(lib().phi_hier_time(self.h, which, nrhs, reps, int(flush_l2), C.byref(ms)))
+        return ms.value
 
     def spmv(self, x):
         return self._unit(0, x, self.n)

@@ -117,3 +117,20 @@ def test_fast_and_exact_modes_agree_on_config3_4_shapes(p, k, nt, m):
     assert abs(rf.iterations - re_.iterations) <= 1
     assert abs(rf.mean_spatial_iterations - re_.mean_spatial_iterations) <= 1.0
     assert _rel(fast.trajectory(), exact.trajectory()) <= TOL_TRAJ
+
+
+@pytest.mark.parametrize("p,k", [(2, 5), (3, 6), (5, 5)])
+@pytest.mark.parametrize("nrhs", [1, 16, 32, 64])
+def test_spmm_matches_reference_spmv(p, k, nrhs):
+    """The batched SpMV / SpMM kernels (spmm.cu) against the reference spmv
+    (sparse.hpp:114-124) applied column by column; reassociated sums."""
+    _ref_or_skip()
+    d = E.SpatialDiscretization.build(p, k)
+    h = E.PMultigridHierarchy(d, 1e-4)
+    r = O.RefHier(O.RefDisc(p, k), 1e-4)
+    A = r.csr(0)
+    X = np.random.default_rng(5).standard_normal((d.n_free, nrhs))
+    Y = h.spmm(X if nrhs > 1 else X[:, 0])
+    Y = Y.reshape(d.n_free, nrhs)
+    ref = np.stack([A.spmv(X[:, j]) for j in range(nrhs)], axis=1)
+    assert _rel(Y, ref) <= TOL_BLOCK
