@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_types.cuh"
 #include "phi_kernels.cuh"
@@ -146,9 +147,51 @@ __device__ __forceinline__ double div_rn(double s, double d, double r) {
 }
 
 // ---------------------------------------------------------------------------
+// Thread-block clusters (single-right-hand-side waves, reassociated mode):
+// the CTAs of a cluster run the same Phi application in lock step.  The
+// data-parallel phases (operator products, copies, epilogues) are split over
+// the CTAs by row (part = cluster rank); the sweeps and the W-cycle run on the
+// main CTA (rank 0) while the others wait at the next cluster barrier.  Dot
+// products are computed by every CTA over the whole vector (same code, same
+// data: identical control decisions).  Without clusters rank = 0, size = 1.
+// ---------------------------------------------------------------------------
+__shared__ int g_cl[2];  // cluster rank, cluster size
+__device__ __forceinline__ void cl_init() {
+    if (threadIdx.x == 0) {
+        unsigned r, n;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+        asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+        g_cl[0] = (int)r;
+        g_cl[1] = (int)n;
+    }
+}
+__device__ __forceinline__ int cl_rank() { return g_cl[0]; }
+__device__ __forceinline__ int cl_size() { return g_cl[1]; }
+// barrier of every thread of the cluster (memory ordered at cluster scope)
+__device__ __forceinline__ void cl_sync() {
+    if (g_cl[1] > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        __syncthreads();
+    }
+}
+// generic pointer to the main CTA's copy of a shared-memory address
+__device__ __forceinline__ double* cl_main(double* p) {
+    if (g_cl[1] <= 1 || !__isShared(p)) return p;
+    unsigned long long out;
+    asm volatile("mapa.u64 %0, %1, 0;" : "=l"(out) : "l"(reinterpret_cast<unsigned long long>(p)));
+    return reinterpret_cast<double*>(out);
+}
+
+// ---------------------------------------------------------------------------
 // per-CTA workspace (generic pointers: shared memory or global per SmemPlan)
 // ---------------------------------------------------------------------------
 struct Ws {
+    // cluster-visible views of the vectors that live in the main CTA's shared
+    // memory (z and the first h-level's b, x); equal to z / hb[0] / hx[0] when
+    // the kernel runs without clusters
+    double *zc, *hb0c, *hx0c;
     double *b, *x, *r, *zg;  // global
     double* z;               // in-place triangular-solve vector (n_p + 1 slots)
     double* dot;             // shared scratch for ordered dots
@@ -186,6 +229,9 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
         w.hr[l] = s + 2 * (size_t)nl + 1;  // x has a zero slot x[n] (padded sweep entries)
         g += 3 * (size_t)nl + 1;
     }
+    w.zc = cl_main(w.z);
+    w.hb0c = cl_main(w.hb[0]);
+    w.hx0c = cl_main(w.hx[0]);
     return w;
 }
 
@@ -237,10 +283,11 @@ struct Tree<1> {
 // to cover the L2 latency -- and sums them by a tree per stencil row.
 template <int OUT, int W>
 __device__ __noinline__ void stencil_apply_fast(const DevStencil& A, const double* __restrict__ x,
-                                                double* __restrict__ y, const double* __restrict__ aux) {
+                                                double* __restrict__ y, const double* __restrict__ aux, int part,
+                                                int parts) {
     constexpr int DVC = W * W <= 25 ? W : (24 / W > 0 ? 24 / W : 1);
     const int n = A.ru * A.rv;
-    for (int i = threadIdx.x; i < n; i += NT) {
+    for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
         const int iv = i / A.ru;
         const int iu = i - iv * A.ru;
         int cu_[W];
@@ -289,11 +336,13 @@ __device__ __noinline__ void stencil_apply_fast(const DevStencil& A, const doubl
     }
 }
 
+// part / parts: rows interleaved over the CTAs of a cluster (fast mode only)
 template <int OUT, int W>
 __device__ __noinline__ void stencil_apply(const DevStencil& A, const double* __restrict__ x,
-                                           double* __restrict__ y, const double* __restrict__ aux, bool exact = true) {
+                                           double* __restrict__ y, const double* __restrict__ aux, bool exact = true,
+                                           int part = 0, int parts = 1) {
     if (!exact) {
-        stencil_apply_fast<OUT, W>(A, x, y, aux);
+        stencil_apply_fast<OUT, W>(A, x, y, aux, part, parts);
         return;
     }
     const int n = A.ru * A.rv;
@@ -1216,11 +1265,11 @@ __device__ __noinline__ double cta_ordered_dot(const double* a, const double* b,
     return v;
 }
 
-__device__ void cta_fill(double* y, double v, int n) {
-    for (int i = threadIdx.x; i < n; i += NT) y[i] = v;
+__device__ void cta_fill(double* y, double v, int n, int part = 0, int parts = 1) {
+    for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) y[i] = v;
 }
-__device__ void cta_copy(double* y, const double* x, int n) {
-    for (int i = threadIdx.x; i < n; i += NT) y[i] = x[i];
+__device__ void cta_copy(double* y, const double* x, int n, int part = 0, int parts = 1) {
+    for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) y[i] = x[i];
 }
 
 // Dense LU solve of the coarsest h-level (solvers.hpp:118-133), thread 0.
@@ -1530,34 +1579,42 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
 template <int DEG>
 __device__ __noinline__ void smooth(const DevHier& H, const Ws& w, bool r_valid = false) {
     pstamp(10);
+    const int part = cl_rank(), parts = cl_size();
     if (r_valid)
-        cta_copy(w.z, w.r, H.n_p);
+        cta_copy(w.zc, w.r, H.n_p, part, parts);
     else
-        stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.z, w.b, H.exact != 0);  // z = r = b - A x
-    if (threadIdx.x == 0) w.z[H.n_p] = 0.0;                          // neutral padding slot
-    __syncthreads();
+        stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.zc, w.b, H.exact != 0, part, parts);  // z = r = b - A x
+    if (threadIdx.x == 0 && part == 0) w.z[H.n_p] = 0.0;  // neutral padding slot
+    cl_sync();
     pstamp(11);
-    if (H.exact)
-        ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, true);
-    else
-        ilut_solve_blk(H.Lb, H.Ub, w.z, w.z_off, w.x, w);
+    if (part == 0) {  // the sweeps: main CTA
+        if (H.exact)
+            ilut_solve(H.L, H.U, w.z, w.z_off, w.x, w.ring_off, w.slot_bytes, w.prod_off, true);
+        else
+            ilut_solve_blk(H.Lb, H.Ub, w.z, w.z_off, w.x, w);
+    }
+    cl_sync();
     pstamp(12);
 }
 
 // One V(nu_pre, nu_post) cycle (pmultigrid.hpp:256-267).
 template <int DEG>
 __device__ __noinline__ void vcycle(const DevHier& H, const Ws& w, bool r_valid = false) {
+    const int part = cl_rank(), parts = cl_size();
     for (int s = 0; s < H.nu_pre; ++s) smooth<DEG>(H, w, r_valid && s == 0);
-    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0);
-    __syncthreads();
-    stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, w.r, w.hb[0], H.inv_l1, H.exact != 0);  // restrict_to_linear
-    cta_fill(w.hx[0], 0.0, H.n_1);
-    __syncthreads();
+    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0, part, parts);
+    cl_sync();
+    stencil_apply<kOutScale, Widths<DEG>::T>(H.Tt, w.r, w.hb0c, H.inv_l1, H.exact != 0, part,
+                                             parts);  // restrict_to_linear
+    cta_fill(w.hx0c, 0.0, H.n_1, part, parts);
+    cl_sync();
     pstamp(20);
-    wcycle<DEG>(H, w);
+    if (part == 0) wcycle<DEG>(H, w);  // the W-cycle: main CTA
+    cl_sync();
     pstamp(21);
-    stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, w.hx[0], w.x, H.inv_lp, H.exact != 0);  // x += prolong_from_linear
-    __syncthreads();
+    stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, w.hx0c, w.x, H.inv_lp, H.exact != 0, part,
+                                                 parts);  // x += prolong_from_linear
+    cl_sync();
     pstamp(22);
     for (int s = 0; s < H.nu_post; ++s) smooth<DEG>(H, w);
 }
@@ -1565,7 +1622,8 @@ __device__ __noinline__ void vcycle(const DevHier& H, const Ws& w, bool r_valid 
 template <int DEG>
 __device__ double rel_residual(const DevHier& H, const Ws& w, double bnorm, double* sh) {
     pstamp(30);
-    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0);
+    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, w.x, w.r, w.b, H.exact != 0, cl_rank(), cl_size());
+    cl_sync();  // every CTA reads the whole residual
     const double d = cta_ordered_dot(w.r, w.r, H.n_p, w.dot, sh, H.exact != 0);
     pstamp(31);
     return sqrt(d) / bnorm;
@@ -1576,6 +1634,7 @@ template <int DEG>
 __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs& a, const Ws& w, int task,
                           int k, double* sh) {
     const int n = H.n_p;
+    const int part = cl_rank(), parts = cl_size();
     // ---- right-hand side and initial guess
     if (a.mode == kModeStep) {
         const double* uprev = a.U ? a.U + (size_t)(k - 1) * n : a.UPREV + (size_t)task * a.ldu;
@@ -1585,37 +1644,38 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
         else if (a.LOADV)
             load = a.LOADV + (size_t)task * a.ldl;
         if (load)
-            stencil_apply<kOutAddVec, Widths<DEG>::A>(Am, uprev, w.b, load, H.exact != 0);  // rhs = A- u + load
+            stencil_apply<kOutAddVec, Widths<DEG>::A>(Am, uprev, w.b, load, H.exact != 0, part,
+                                                      parts);  // rhs = A- u + load
         else
-            stencil_apply<kOutSet, Widths<DEG>::A>(Am, uprev, w.b, nullptr, H.exact != 0);
+            stencil_apply<kOutSet, Widths<DEG>::A>(Am, uprev, w.b, nullptr, H.exact != 0, part, parts);
         const double* guess =
             a.U ? a.U + (size_t)(a.guess_prev ? k - 1 : k) * n : (a.x0_empty ? nullptr : a.X + (size_t)task * a.ldx);
         if (guess)
-            cta_copy(w.x, guess, n);
+            cta_copy(w.x, guess, n, part, parts);
         else
-            cta_fill(w.x, 0.0, n);
+            cta_fill(w.x, 0.0, n, part, parts);
     } else {
         const double* bsrc;
         if (a.B)
             bsrc = a.B + (size_t)task * a.ldb;
         else
             bsrc = a.load_steady ? a.LOAD : a.LOAD + (size_t)(k - 1) * n;
-        cta_copy(w.b, bsrc, n);
+        cta_copy(w.b, bsrc, n, part, parts);
         if (a.x0_empty)
-            cta_fill(w.x, 0.0, n);
+            cta_fill(w.x, 0.0, n, part, parts);
         else
-            cta_copy(w.x, a.X + (size_t)task * a.ldx, n);
+            cta_copy(w.x, a.X + (size_t)task * a.ldx, n, part, parts);
     }
-    __syncthreads();
+    cl_sync();
 
     // ---- p-multigrid solve
     int iters = 0, conv = 0;
     double rel = 0.0;
     const double bnorm = sqrt(cta_ordered_dot(w.b, w.b, n, w.dot, sh, H.exact != 0));
     if (bnorm == 0.0) {
-        cta_fill(w.x, 0.0, n);  // zero rhs -> zero solution, not the guess
+        cta_fill(w.x, 0.0, n, part, parts);  // zero rhs -> zero solution, not the guess
         conv = 1;
-        __syncthreads();
+        cl_sync();
     } else if (H.fixed_cycles > 0) {
         for (int c = 0; c < H.fixed_cycles; ++c) vcycle<DEG>(H, w);
         iters = H.fixed_cycles;
@@ -1639,7 +1699,7 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
     }
 
     // ---- bookkeeping (SolveStats::record, theta.hpp:81-84)
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && part == 0) {
         if (a.stat) {
             atomicAdd(a.stat, 1ULL);
             atomicAdd(a.stat + 1, (unsigned long long)iters);
@@ -1666,33 +1726,34 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
     const double* g = a.G ? a.G + (size_t)k * n : nullptr;
     if (a.epi == kEpiStore) {
         double* out = a.U + (size_t)k * n;
-        for (int i = threadIdx.x; i < n; i += NT) out[i] = g ? w.x[i] + g[i] : w.x[i];
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) out[i] = g ? w.x[i] + g[i] : w.x[i];
     } else if (a.epi == kEpiRestrict) {
         const int j = k / a.m;
         const double* u = a.U + (size_t)k * n;
         double* cg = a.CG + (size_t)j * n;
         double* cu = a.CU + (size_t)j * n;
-        for (int i = threadIdx.x; i < n; i += NT) {
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
             const double wv = g ? w.x[i] + g[i] : w.x[i];
             cg[i] = wv - u[i];
             cu[i] = 0.0;
         }
     } else if (a.epi == kEpiResid) {
         const double* u = a.U + (size_t)k * n;
-        for (int i = threadIdx.x; i < n; i += NT) {
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
             const double wv = g ? w.x[i] + g[i] : w.x[i];
             w.r[i] = wv - u[i];
         }
+        cl_sync();
         const double d = cta_ordered_dot(w.r, w.r, n, w.dot, sh, H.exact != 0);
-        if (threadIdx.x == 0) a.SQ[k] = d;
+        if (threadIdx.x == 0 && part == 0) a.SQ[k] = d;
     } else if (a.epi == kEpiNorm) {
         const double d = cta_ordered_dot(w.x, w.x, n, w.dot, sh, H.exact != 0);
-        if (threadIdx.x == 0) a.SQ[k] = d;
+        if (threadIdx.x == 0 && part == 0) a.SQ[k] = d;
     } else {
         double* out = a.X + (size_t)task * a.ldx;
-        for (int i = threadIdx.x; i < n; i += NT) out[i] = w.x[i];
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) out[i] = w.x[i];
     }
-    __syncthreads();
+    cl_sync();
 }
 
 template <int DEG>
@@ -1705,10 +1766,13 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ WaveArgs a_sh;
     if (threadIdx.x == 0) a_sh = a_param;
     const WaveArgs& a = a_sh;
+    cl_init();
     blk_init();
     const DevHier& H = hier_shared(H_param);
-    const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
-    for (int task = blockIdx.x; task < a.n_tasks; task += gridDim.x) {
+    // one workspace per cluster (the main CTA's); cluster c takes tasks c, c + nclusters, ...
+    const int cid = blockIdx.x / cl_size(), ncl = gridDim.x / cl_size();
+    const Ws& w = carve_shared(ws_base + (size_t)cid * ws_stride, H, P, smem);
+    for (int task = cid; task < a.n_tasks; task += ncl) {
         for (int s = 0; s < a.task_len; ++s) {
             const int k = a.task_k0 ? a.task_k0[task] + s : task;
             phi_point<DEG>(H, Am, a, w, task, k, sh);
@@ -1722,6 +1786,7 @@ __global__ void __launch_bounds__(NT, 1)
     vcycle_kernel(const __grid_constant__ DevHier H_param, const double* B, long long ldb, double* X, long long ldx,
                   int nrhs, const __grid_constant__ SmemPlan P, double* ws_base, long long ws_stride) {
     double* smem = g_smem;
+    cl_init();
     blk_init();
     const DevHier& H = hier_shared(H_param);
     const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
@@ -1745,6 +1810,7 @@ __global__ void __launch_bounds__(NT, 1)
     unit_kernel(const __grid_constant__ DevHier H_param, int op, int arg, int arg2, const double* in, double* out,
                 const __grid_constant__ SmemPlan P, double* ws_base, long long ws_stride) {
     double* smem = g_smem;
+    cl_init();
     blk_init();
     const DevHier& H = hier_shared(H_param);
     const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
@@ -1889,7 +1955,34 @@ void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs
     const SmemPlan P = phi_smem_plan(H);
     const size_t smem = (size_t)P.total * 8;
     occupancy_grid(phi_wave_kernel<DEG>, smem, grid);
-    phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
+    // a wave of few right-hand sides (the coarse march: one) runs each task on
+    // a cluster of CTAs (reassociated mode): the data-parallel phases spread
+    // over the cluster's SMs (developer override: PHI_CLUSTER=<size>, 0/1 off)
+    static int cl = -1;
+    if (cl < 0) {
+        cl = kPhiCluster;
+        if (const char* e = std::getenv("PHI_CLUSTER")) cl = std::atoi(e);
+    }
+    int n_sm = 0, dev = 0;
+    PHI_CUDA(cudaGetDevice(&dev));
+    PHI_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    if (!H.exact && cl > 1 && a.n_tasks * cl <= n_sm) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(a.n_tasks * cl));
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PHI_CUDA(cudaLaunchKernelEx(&cfg, phi_wave_kernel<DEG>, H, Am, a, P, ws, ws_stride));
+    } else {
+        phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
+    }
     PHI_CUDA(cudaGetLastError());
 }
 

@@ -15,6 +15,8 @@ constexpr int kPhiThreads = 256;
 // Dynamic shared memory one Phi CTA may use for its latency-critical vectors
 // (one CTA per SM; 227 KB is the sm_100 per-block maximum).
 constexpr size_t kPhiSmemBudgetBytes = 212 * 1024;
+/// CTAs per cluster for waves of few right-hand sides (reassociated mode).
+constexpr int kPhiCluster = 8;
 
 size_t phi_ws_doubles(const DevHier& H);
 SmemPlan phi_smem_plan(const DevHier& H);
