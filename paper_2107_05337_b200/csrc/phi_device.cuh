@@ -634,177 +634,18 @@ __device__ __noinline__ void tri_solve_warp_t(const DevTri& T, double* zg, int z
     }
 }
 
-// Warps that take turns on the blocks of a fast sweep (setup_host.hpp
-// kSweepWarps: the host classifies entries as "fresh" against this distance).
+// Warps that meet at the closing barrier of an exact-mode sweep.
 constexpr int kSW = kSweepWarps;
 constexpr int kSweepBar = kSW + 1;  // named barrier of all sweep warps
-__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void sweep_sync() { asm volatile("bar.sync %0, %1;" ::"r"(kSweepBar), "r"(32 * kSW) : "memory"); }
-
-// Fast (reassociated) sweep on kSW warps taking turns: block b is solved by
-// warp b % kSW.  A warp prepares its next block while the others run theirs:
-// header, per-lane tables, right-hand sides, the complete sum of the block's
-// "old" entries (columns solved kSW or more blocks earlier -- final once the
-// warp's own previous block is done) and the columns and values of its
-// "fresh" entries.  Only the fresh entries' z loads, a short tree, the update
-// and the store remain on the critical path.  Hand-off: the warp that
-// finished block b arrives on named barrier 1 + b % kSW; the warp of block
-// b + 1 syncs on it (bar.sync orders the shared-memory stores).  All warps
-// walk the TMA ring; the slot of a finished unit is refilled by the warp that
-// opens the next unit once the unit's last block is done.
-template <bool UPPER, bool ZSM>
-__device__ __noinline__ void tri_solve_pp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
-                                          int ring_off, int slot_bytes, unsigned bar) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // w < kSW
-    const unsigned ring = sh_addr(g_smem + ring_off);
-    const unsigned zs = ZSM ? sh_addr(g_smem + z_off) : 0u;
-    const unsigned rs = ZSM ? sh_addr(g_smem + r_off) : 0u;
-    const int n_units = T.n_units;
-    const unsigned char* __restrict__ stream = T.stream;
-    if (n_units == 0) return;
-    if (threadIdx.x == 0)
-        for (int k = 0; k < kTriSlots - 1 && k < n_units; ++k)
-            bulk_fetch(ring + k * slot_bytes, stream + (size_t)T.prime[2 * k] * 16, T.prime[2 * k + 1],
-                       bar + 8u * k);
-    // Each warp touches only the units that hold its own blocks b = w,
-    // w + kSW, ..: the block table (global, prefetched one turn ahead) gives
-    // a block's unit and offset, so no warp ever reads a unit whose slot may
-    // already be recycled (a slot is refilled once all of its blocks are done).
-    const int n_blocks = T.n_blocks;
-    const int4* __restrict__ table = T.blocks;
-    int u = -1, noff = 0, nbytes = 0;
-    unsigned unit = 0;
-    if (threadIdx.x == 0) {  // unit kTriSlots - 1 goes to the one slot the prime left empty
-        mbar_wait(bar, 0u);
-        int nb, pad;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nb), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(ring));
-        (void)nb;
-        (void)pad;
-        if (nbytes > 0)
-            bulk_fetch(ring + (kTriSlots - 1) * slot_bytes, stream + (size_t)noff * 16, nbytes,
-                       bar + 8u * (kTriSlots - 1));
-    }
-    int4 nxt = w < n_blocks ? __ldg(table + w) : make_int4(0, 0, 0, 0);
-    for (int b = w; b < n_blocks; b += kSW) {
-        const int4 info = nxt;
-        if (b + kSW < n_blocks) nxt = __ldg(table + b + kSW);
-        if (info.x != u) {  // open the block's unit: wait for its TMA, read its refill fields
-            u = info.x;
-            const int slot = u % kTriSlots;
-            mbar_wait(bar + 8u * slot, (unsigned)(u / kTriSlots) & 1u);
-            unit = ring + slot * slot_bytes;
-            int nb, pad;
-            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nb), "=r"(noff), "=r"(nbytes), "=r"(pad) : "r"(unit));
-            (void)nb;
-            (void)pad;
-        }
-        const unsigned blk = unit + (unsigned)info.y;
-        const bool last = b + 1 == n_blocks;
-        const int k = info.z ? 0 : 1;  // 0: first block of its unit
-        int nr, m, lg, bytes;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(nr), "=r"(m), "=r"(lg), "=r"(bytes) : "r"(blk));
-        (void)nr;
-        (void)bytes;
-        long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && b < 1024)
-                            ? c_tune.trace + kTriTraceBase + 8 * b
-                            : nullptr;
-        if (tr) tr[0] = clock64();
-        {
-            // ---- prepare block b: everything but its fresh entries
-            int cols_off, vals_off, diag_off, fp;
-            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(cols_off), "=r"(vals_off), "=r"(diag_off), "=r"(fp)
-                         : "r"(blk + 16));
-            const int i = lds_s32(blk + 32u + 4u * lane);  // row index on a row's first lane, -1 elsewhere
-            double rd = 1.0, z0 = 0.0;
-            if (i >= 0) {
-                z0 = ZSM ? lds_f64(rs + 8u * i) : rg[i];  // a row's right-hand side is final from the start
-                if (UPPER) rd = lds_f64(blk + diag_off + 8u * lane);
-            }
-            // old entries: solved kSW or more blocks ago (this warp's previous
-            // block b - kSW is done, so they are final)
-            const unsigned cp = blk + cols_off + 4u * lane, vp = blk + vals_off + 8u * lane;
-            double t_old = 0.0;
-            for (int q0 = 0; q0 < m; q0 += 8) {
-                int j[8];
-                double v[8], zj[8], pr[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    j[q] = lds_s32(cp + 128u * (q0 + q));
-                    v[q] = lds_f64(vp + 256u * (q0 + q));
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * j[q]) : zg[j[q]];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) pr[q] = v[q] * zj[q];
-                t_old = t_old + (((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7])));
-            }
-            if (lg > 0) t_old = bfly_sum(t_old, lg);  // idle lanes hold zero slots
-            // fresh entries (solved by blocks b - kSW + 1 .. b - 1): columns
-            // and values now, their z after the hand-off
-            const unsigned fc = (vals_off + 256u * m + 15u) & ~15u;
-            const unsigned fv = (fc + 128u * fp + 15u) & ~15u;
-            const unsigned fcp = blk + fc + 4u * lane, fvp = blk + fv + 8u * lane;
-            int fj[8];
-            double fvv[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                fj[q] = fp > 0 ? lds_s32(fcp + 128u * q) : T.n;
-                fvv[q] = fp > 0 ? lds_f64(fvp + 256u * q) : 0.0;
-            }
-            // ---- wait for block b - 1, then the critical path
-            if (tr) tr[1] = clock64() + (long long)(t_old == 12345.678) + (long long)(fj[7] == -7) + (long long)(fvv[7] == 1.5);
-            if (b > 0) nbar_sync(1 + (b - 1) % kSW);
-            if (tr) tr[2] = clock64();
-            // the first block of unit u refills unit u - 1's slot (all of its
-            // blocks are done now) with unit u + kTriSlots - 1
-            if (k == 0 && u > 0 && lane == 0 && nbytes > 0)
-                bulk_fetch(ring + ((u + kTriSlots - 1) % kTriSlots) * slot_bytes, stream + (size_t)noff * 16, nbytes,
-                           bar + 8u * ((u + kTriSlots - 1) % kTriSlots));
-            double zj[8], pr[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * fj[q]) : zg[fj[q]];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) pr[q] = fvv[q] * zj[q];
-            double t_new = ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
-            for (int q0 = 8; q0 < fp; q0 += 8) {  // rare: more than 8 fresh entries
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    fj[q] = lds_s32(fcp + 128u * (q0 + q));
-                    fvv[q] = lds_f64(fvp + 256u * (q0 + q));
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) zj[q] = ZSM ? lds_f64(zs + 8u * fj[q]) : zg[fj[q]];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) pr[q] = fvv[q] * zj[q];
-                t_new = t_new + (((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7])));
-            }
-            if (i >= 0) {
-                double s = z0 - (t_old + t_new);
-                if (UPPER) s = s * rd;  // reassociated mode: within one ulp of the quotient
-                if (ZSM)
-                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(zs + 8u * i), "d"(s) : "memory");
-                else
-                    zg[i] = s;
-            }
-            if (tr) tr[3] = clock64();
-            if (!last) nbar_arrive(1 + b % kSW);  // block b done
-        }
-        if (last) return;
-    }
-}
 
 template <bool UPPER, bool ZSM>
 __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int z_off, const double* rg, int r_off,
                                                int ring_off, int slot_bytes, int prod_off, unsigned bar, bool exact) {
-    // called by the kSW sweep warps: the exact sweep runs on warp 0, the fast one on all
-    if (exact) {
-        if (threadIdx.x < 32)
-            tri_solve_warp_t<UPPER, ZSM, true>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
-    } else {
-        tri_solve_pp<UPPER, ZSM>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, bar);
-    }
+    // exact mode only (the reassociated mode runs block sweeps): warp 0 solves
+    (void)exact;
+    if (threadIdx.x < 32)
+        tri_solve_warp_t<UPPER, ZSM, true>(T, zg, z_off, rg, r_off, ring_off, slot_bytes, prod_off, bar);
     sweep_sync();  // all sweep warps done (the next sweep reuses the ring and mbarriers)
 }
 

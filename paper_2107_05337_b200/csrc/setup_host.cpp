@@ -556,95 +556,6 @@ TriPlan plan_gauss_seidel(const HostCsr& a, bool backward) {
     return make_plan(a.n_rows, backward, rv);
 }
 
-namespace {
-// Cost model of a fast block (cycles): per batch of 8 slots per lane, per
-// butterfly round.  Developer override: PHI_TRI_COST="batch,round".
-double tri_cost(int which) {
-    static double v[2] = {-1.0, -1.0};
-    if (v[0] < 0.0) {
-        v[0] = 180.0;
-        v[1] = 85.0;
-        if (const char* e = std::getenv("PHI_TRI_COST")) std::sscanf(e, "%lf,%lf", &v[0], &v[1]);
-    }
-    return v[which];
-}
-double tri_cost_batch() { return tri_cost(0); }
-double tri_cost_round() { return tri_cost(1); }
-}  // namespace
-
-// Fast block c: every entry of its rows is either "old" (its column was
-// solved kSweepWarps or more blocks earlier, or is solved later) or "fresh"
-// (solved by one of the kSweepWarps - 1 blocks just before c).  Old
-// entries: G = 2^lg lanes per row, slot q of lane L at q * 32 + L over m
-// slots; they are summed while the previous block is still being solved.
-// Fresh entries sit on the row's first lane (Fp slots, same layout) and are
-// the only loads on the critical path.  Header: nr, m, lg, bytes, cols_off,
-// vals_off, diag_off, Fp; fresh columns at align16(vals_off + 256 m), fresh
-// values at align16(that + 128 Fp).
-static std::vector<unsigned char> fast_block(const TriPlan& p, int c, const std::vector<int>& block_of, bool upper) {
-    const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
-    std::vector<std::vector<std::pair<int, double>>> olde(nr), frsh(nr);
-    int maxold = 0, maxfresh = 0;
-    for (int l = 0; l < nr; ++l) {
-        for (int e = 0; e < p.lens[row0 + l]; ++e) {
-            const size_t src = static_cast<size_t>(base) + static_cast<size_t>(e) * nr + l;
-            const int col = p.cols[src];
-            // solved by one of the kSweepWarps - 1 blocks before this one
-            const bool fresh = col < p.n && block_of[col] < c && block_of[col] > c - kSweepWarps;
-            (fresh ? frsh : olde)[l].emplace_back(col, p.vals[src]);
-        }
-        maxold = std::max(maxold, static_cast<int>(olde[l].size()));
-        maxfresh = std::max(maxfresh, static_cast<int>(frsh[l].size()));
-    }
-    int lg = 0, m = 0;
-    if (maxold > 0) {
-        double best = 1e30;
-        for (int g = 0; (nr << g) <= 32; ++g) {
-            const int mm = (std::max(1, (maxold + (1 << g) - 1) >> g) + 7) / 8 * 8;
-            const double cost = tri_cost_batch() * (mm / 8) + tri_cost_round() * g;
-            if (cost < best) {
-                best = cost;
-                lg = g;
-                m = mm;
-            }
-        }
-    }
-    const int fp = (maxfresh + 7) / 8 * 8;
-    const int diag_off = 32 + 4 * 32;
-    const int cols_off = diag_off + (upper ? 8 * 32 : 0);
-    const int vals_off = (cols_off + 128 * m + 15) / 16 * 16;
-    const int fcols_off = (vals_off + 256 * m + 15) / 16 * 16;
-    const int fvals_off = (fcols_off + 128 * fp + 15) / 16 * 16;
-    const int bytes = (fvals_off + 256 * fp + 15) / 16 * 16;
-    std::vector<unsigned char> img(bytes, 0);  // may exceed kTriUnitCap: then it is a unit of its own
-    const int hdr[8] = {nr, m, lg, bytes, cols_off, vals_off, diag_off, fp};
-    std::memcpy(img.data(), hdr, sizeof hdr);
-    int* rws = reinterpret_cast<int*>(img.data() + 32);
-    double* rd = reinterpret_cast<double*>(img.data() + diag_off);
-    int* cols = reinterpret_cast<int*>(img.data() + cols_off);
-    double* vals = reinterpret_cast<double*>(img.data() + vals_off);
-    int* fcols = reinterpret_cast<int*>(img.data() + fcols_off);
-    double* fvals = reinterpret_cast<double*>(img.data() + fvals_off);
-    for (int s = 0; s < 32 * m; ++s) cols[s] = p.n;  // neutral dummies (z[n] = +0.0, value +0.0)
-    for (int s = 0; s < 32 * fp; ++s) fcols[s] = p.n;
-    for (int L = 0; L < 32; ++L) rws[L] = -1;
-    for (int l = 0; l < nr; ++l) {
-        const int i = p.rows[row0 + l], lane0 = l << lg;
-        rws[lane0] = i;
-        if (upper) rd[lane0] = 1.0 / p.diag[i];  // IEEE round-to-nearest reciprocal
-        for (size_t e = 0; e < olde[l].size(); ++e) {
-            const size_t dst = (e % m) * 32 + lane0 + e / m;
-            cols[dst] = olde[l][e].first;
-            vals[dst] = olde[l][e].second;
-        }
-        for (size_t e = 0; e < frsh[l].size(); ++e) {
-            fcols[e * 32 + lane0] = frsh[l][e].first;
-            fvals[e * 32 + lane0] = frsh[l][e].second;
-        }
-    }
-    return img;
-}
-
 TriStream make_tri_stream(const TriPlan& p, bool fast) {
     const bool upper = !p.diag.empty();
     std::vector<int> block_of(p.n, -1);  // plan chunk (stream block) of every row
@@ -653,32 +564,10 @@ TriStream make_tri_stream(const TriPlan& p, bool fast) {
     // ---- block images
     std::vector<std::vector<unsigned char>> blocks;
     for (int c = 0; c < p.n_chunks; ++c) {
-        if (fast) {
-            blocks.push_back(fast_block(p, c, block_of, upper));
-            continue;
-        }
+        if (fast) throw InvalidArgument("make_tri_stream: the reassociated mode uses block recurrences (BlkStream)");
         const int row0 = p.chunk_meta[4 * c], nr = p.chunk_meta[4 * c + 1], base = p.chunk_meta[4 * c + 2];
         const int span = p.chunk_meta[4 * c + 3];
         int lg = 0, m = span;
-        if (fast) {
-            // lanes per row: minimise the batches of 8 entries per lane plus the
-            // pairwise reduction of the G slice sums
-            int maxlen = 0;
-            for (int l = 0; l < nr; ++l) maxlen = std::max(maxlen, p.lens[row0 + l]);
-            double best = 1e30;
-            for (int g = 0; (nr << g) <= 32; ++g) {
-                // slots per lane padded to whole batches of 8 (unpredicated
-                // loads); measured (tools/block_probe.cu): ~180 cycles per
-                // batch, ~45 per butterfly round
-                const int mm = (std::max(1, (maxlen + (1 << g) - 1) >> g) + 7) / 8 * 8;
-                const double cost = tri_cost_batch() * (mm / 8) + tri_cost_round() * g;
-                if (cost < best) {
-                    best = cost;
-                    lg = g;
-                    m = mm;
-                }
-            }
-        }
         // fast: entry-major over a full warp (slot q of lane L at q * 32 + L),
         // so that one load instruction reads one slot of every lane
         // conflict-free; exact: entry e of row l at e * nr + l
