@@ -267,7 +267,7 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     // become one data-parallel matvec.  Same cycle, different rounding.
     if (!opt.exact && opt.dense_coarse_max > 0) {
         const int nh = (int)a_h.size();
-        for (int l = 1; l + 1 < nh; ++l)
+        for (int l = 0; l + 1 < nh; ++l)
             if (d.h[l].n <= opt.dense_coarse_max) {
                 std::vector<HostCsr> ah, eh;
                 for (int k = 0; k < nh; ++k) {
