@@ -96,6 +96,8 @@ struct DevHier {
     // initial guess) as a dense n x n operator, column-major (-1: none)
     int dense_level;
     const double* dense_op;
+    int dense_level_cl;  // the same for cluster mode (larger: split over the cluster)
+    const double* dense_op_cl;
     int nu_pre, nu_post, gs_pre, gs_post;
     double rel_tol;
     int max_iter;

@@ -265,19 +265,23 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     // rows the W-cycle (zero initial guess, hence linear) is applied as one
     // dense operator -- the latency-bound small sweeps and the serial LU
     // become one data-parallel matvec.  Same cycle, different rounding.
-    if (!opt.exact && opt.dense_coarse_max > 0) {
+    if (!opt.exact && (opt.dense_coarse_max > 0 || opt.dense_cluster_max > 0)) {
         const int nh = (int)a_h.size();
-        for (int l = 0; l + 1 < nh; ++l)
-            if (d.h[l].n <= opt.dense_coarse_max) {
-                std::vector<HostCsr> ah, eh;
-                for (int k = 0; k < nh; ++k) {
-                    ah.push_back(stencil_to_csr(a_h[k]));
-                    eh.push_back(d.h[k].E);
-                }
-                dense_op = dev(wcycle_operator(ah, eh, coarse, l, opt.gs_pre, opt.gs_post), s);
-                dense_level = l;
-                break;
-            }
+        std::vector<HostCsr> ah, eh;
+        for (int k = 0; k < nh; ++k) {
+            ah.push_back(stencil_to_csr(a_h[k]));
+            eh.push_back(d.h[k].E);
+        }
+        auto first = [&](int cap) {
+            for (int l = 0; l + 1 < nh; ++l)
+                if (d.h[l].n <= cap) return l;
+            return -1;
+        };
+        dense_level = opt.dense_coarse_max > 0 ? first(opt.dense_coarse_max) : -1;
+        dense_level_cl = opt.dense_cluster_max > 0 ? first(opt.dense_cluster_max) : -1;
+        if (dense_level >= 0) dense_op = dev(wcycle_operator(ah, eh, coarse, dense_level, opt.gs_pre, opt.gs_post), s);
+        if (dense_level_cl >= 0 && dense_level_cl != dense_level)
+            dense_op_cl = dev(wcycle_operator(ah, eh, coarse, dense_level_cl, opt.gs_pre, opt.gs_post), s);
     }
     PHI_CUDA(cudaStreamSynchronize(s));
 }
@@ -326,6 +330,8 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     H.coarse_n = coarse.n;
     H.dense_level = dense_level;
     H.dense_op = dense_op.get();
+    H.dense_level_cl = dense_level_cl;
+    H.dense_op_cl = dense_level_cl == dense_level ? dense_op.get() : dense_op_cl.get();
     H.nu_pre = opt.nu_pre;
     H.nu_post = opt.nu_post;
     H.gs_pre = opt.gs_pre;

@@ -69,7 +69,8 @@ struct HierOptions {  // PMultigridOptions (pmultigrid.hpp:161-168)
     int ilut_fill = 0;
     int nu_pre = 1, nu_post = 1, gs_pre = 2, gs_post = 2;
     int exact = 0;  // 1: the reference's summation order (bit-identical), 0: reassociated sums
-    int dense_coarse_max = 256;  // reassociated mode: dense W-cycle operator from the first h-level this small
+    int dense_coarse_max = 256;    // reassociated mode: dense W-cycle operator from the first h-level this small
+    int dense_cluster_max = 1024;  // ... in cluster mode (the product is split over the cluster's SMs)
 };
 
 struct SolverConfig {  // SpatialSolverConfig (theta.hpp:66-75), pmg kind
@@ -126,6 +127,8 @@ public:
         return a_tile.get();
     }
     DevBuf<double> dense_op;
+    int dense_level_cl = -1;   // the same for cluster mode (single-right-hand-side waves)
+    DevBuf<double> dense_op_cl;
     DevBuf<int> coarse_piv;
 
     DevHier view(const SolverConfig& cfg) const;

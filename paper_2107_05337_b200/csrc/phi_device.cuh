@@ -192,6 +192,9 @@ struct Ws {
     // memory (z and the first h-level's b, x); equal to z / hb[0] / hx[0] when
     // the kernel runs without clusters
     double *zc, *hb0c, *hx0c;
+    double* hbc[kMaxH];
+    double* hxc[kMaxH];
+    double* hrc[kMaxH];
     double *b, *x, *r, *zg;  // global
     double* z;               // in-place triangular-solve vector (n_p + 1 slots)
     double* dot;             // shared scratch for ordered dots
@@ -232,6 +235,11 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     w.zc = cl_main(w.z);
     w.hb0c = cl_main(w.hb[0]);
     w.hx0c = cl_main(w.hx[0]);
+    for (int l = 0; l < H.n_h; ++l) {
+        w.hbc[l] = cl_main(w.hb[l]);
+        w.hxc[l] = cl_main(w.hx[l]);
+        w.hrc[l] = cl_main(w.hr[l]);
+    }
     return w;
 }
 
@@ -400,8 +408,9 @@ struct Widths {
 
 // y = A x (CSR, row order) or y += A x.
 template <bool ADD>
-__device__ __forceinline__ void csr_apply(const DevCsr& A, const double* __restrict__ x, double* __restrict__ y) {
-    for (int i = threadIdx.x; i < A.n_rows; i += NT) {
+__device__ __forceinline__ void csr_apply(const DevCsr& A, const double* __restrict__ x, double* __restrict__ y,
+                                          int part = 0, int parts = 1) {
+    for (int i = threadIdx.x + part * NT; i < A.n_rows; i += NT * parts) {
         const int e0 = A.ro[i], e1 = A.ro[i + 1];
         double pv[4], px[4];
 #pragma unroll
@@ -1306,8 +1315,9 @@ __device__ __forceinline__ void gs_line_sweeps(const DevHLevel& lv, const double
 // x += C r for a dense column-major n x n operator (the collapsed coarse
 // W-cycle subtree).  Thread i owns row i; r is broadcast from shared or
 // global memory.
-__device__ __noinline__ void dense_apply(const double* __restrict__ c, int n, const double* b, double* x) {
-    for (int i = threadIdx.x; i < n; i += NT) {
+__device__ __noinline__ void dense_apply(const double* __restrict__ c, int n, const double* b, double* x,
+                                         int part = 0, int parts = 1) {
+    for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int j = 0;
         for (; j + 4 <= n; j += 4) {
@@ -1319,7 +1329,6 @@ __device__ __noinline__ void dense_apply(const double* __restrict__ c, int n, co
         for (; j < n; ++j) a0 = __fma_rn(__ldg(c + (size_t)j * n + i), b[j], a0);
         x[i] = x[i] + ((a0 + a1) + (a2 + a3));
     }
-    __syncthreads();
 }
 
 // h-multigrid W-cycle (pmultigrid.hpp:184-200) as an explicit per-level
@@ -1342,30 +1351,41 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             ta = t;
         }
     };
+    // Cluster mode (cl_size() > 1): the sweeps and the coarsest LU run on the
+    // main CTA, every other phase is split by row over the cluster (the level
+    // vectors live in the main CTA's shared memory: hbc / hxc / hrc are their
+    // cluster-visible views), with cluster barriers in between; the dense
+    // coarse operator then starts at the cluster's own (larger) level.
+    const int part = cl_rank(), parts = cl_size();
+    const bool main = part == 0;
+    const int dl = parts > 1 ? H.dense_level_cl : H.dense_level;
+    const double* dop = parts > 1 ? H.dense_op_cl : H.dense_op;
     int phase[kMaxH];
     int l = 0;
     phase[0] = 0;
     // neutral slots x[n] of the padded sweep entries (the vectors overlay the
     // smoother's shared memory)
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0 && main)
         for (int k = 0; k < H.n_h; ++k) w.hx[k][H.h[k].n] = 0.0;
-    __syncthreads();
+    cl_sync();
     for (;;) {
         if (l + 1 == H.n_h) {
             mark(23);
-            coarse_solve(H, w.hb[l], w.hx[l]);
+            if (main) coarse_solve(H, w.hb[l], w.hx[l]);
+            cl_sync();
             mark(22);
             if (l == 0) break;
             --l;
             continue;
         }
-        if (l == H.dense_level && phase[l] == 0) {
+        if (l == dl && phase[l] == 0) {
             // the subtree from level l, a linear iteration: x += C (b - A x)
             // (C: the cycle from a zero guess; x is zero on the first visit)
             mark(23);
-            stencil_apply<kOutResid, Widths<DEG>::H>(H.h[l].a, w.hx[l], w.hr[l], w.hb[l], false);
-            __syncthreads();
-            dense_apply(H.dense_op, H.h[l].n, w.hr[l], w.hx[l]);
+            stencil_apply<kOutResid, Widths<DEG>::H>(H.h[l].a, w.hxc[l], w.hrc[l], w.hbc[l], false, part, parts);
+            cl_sync();
+            dense_apply(dop, H.h[l].n, w.hrc[l], w.hxc[l], part, parts);
+            cl_sync();
             mark(22);
             if (l == 0) break;
             --l;
@@ -1377,18 +1397,21 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + lv.n : -1;
         if (phase[l] == 0) {
             mark(23);
-            if (H.exact)
-                gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
-            else if (lv.gsl)
-                gs_line_sweeps(lv, b, x, w.hr[l], false, H.gs_pre);
-            else
-                blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            if (main) {
+                if (H.exact)
+                    gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+                else if (lv.gsl)
+                    gs_line_sweeps(lv, b, x, w.hr[l], false, H.gs_pre);
+                else
+                    blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            }
+            cl_sync();
             mark(l);
-            stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, x, w.hr[l], b, H.exact != 0);
-            __syncthreads();
-            csr_apply<false>(lv.embed_t, w.hr[l], w.hb[l + 1]);  // rc = E^T r
-            cta_fill(w.hx[l + 1], 0.0, H.h[l + 1].n);              // ec = 0
-            __syncthreads();
+            stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, w.hxc[l], w.hrc[l], w.hbc[l], H.exact != 0, part, parts);
+            cl_sync();
+            csr_apply<false>(lv.embed_t, w.hrc[l], w.hbc[l + 1], part, parts);  // rc = E^T r
+            cta_fill(w.hxc[l + 1], 0.0, H.h[l + 1].n, part, parts);             // ec = 0
+            cl_sync();
             mark(20);
             phase[l] = 1;
             phase[++l] = 0;
@@ -1397,15 +1420,18 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             phase[++l] = 0;
         } else {
             mark(23);
-            csr_apply<true>(lv.embed, w.hx[l + 1], x);  // x += E ec
-            __syncthreads();
+            csr_apply<true>(lv.embed, w.hxc[l + 1], w.hxc[l], part, parts);  // x += E ec
+            cl_sync();
             mark(21);
-            if (H.exact)
-                gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
-            else if (lv.gsl)
-                gs_line_sweeps(lv, b, x, w.hr[l], true, H.gs_post);
-            else
-                blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            if (main) {
+                if (H.exact)
+                    gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+                else if (lv.gsl)
+                    gs_line_sweeps(lv, b, x, w.hr[l], true, H.gs_post);
+                else
+                    blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            }
+            cl_sync();
             mark(l);
             if (l == 0) break;
             --l;
@@ -1450,8 +1476,7 @@ __device__ __noinline__ void vcycle(const DevHier& H, const Ws& w, bool r_valid 
     cta_fill(w.hx0c, 0.0, H.n_1, part, parts);
     cl_sync();
     pstamp(20);
-    if (part == 0) wcycle<DEG>(H, w);  // the W-cycle: main CTA
-    cl_sync();
+    wcycle<DEG>(H, w);  // cluster-aware: sweeps on the main CTA
     pstamp(21);
     stencil_apply<kOutAddScaled, Widths<DEG>::T>(H.T, w.hx0c, w.x, H.inv_lp, H.exact != 0, part,
                                                  parts);  // x += prolong_from_linear
