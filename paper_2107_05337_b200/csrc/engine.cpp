@@ -498,7 +498,7 @@ void Mgrit::project_initial() {
     const DevStencil M = disc->M.view();
     const int p = disc->degree, w = 2 * p + 1;
     const double* diag = disc->M.vals.get() + (size_t)(p * w + p) * n;  // center entries
-    launch_cg(M, diag, b.get(), u0.get(), work.get(), 1e-13, 2000, res.get(), stream);
+    launch_cg(M, diag, b.get(), u0.get(), work.get(), 1e-13, 2000, res.get(), scfg.pmg.exact, stream);
     launches += 2;
     const auto r = res.download(stream);
     if (r[0] < 0) throw std::runtime_error("cg_solve: breakdown, matrix not SPD");

@@ -1723,11 +1723,12 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ---- IC projection: Jacobi-preconditioned CG on M (solvers.hpp:21-75) ------
-// Single CTA; all dot products index-ordered.  work: 4 vectors of n.
+// Single CTA; exact: index-ordered dot products and operator rows (the
+// reference's rounding), else reassociated sums.  work: 4 vectors of n.
 template <int DEG>
 __global__ void __launch_bounds__(NT, 1)
     cg_kernel(const __grid_constant__ DevStencil A, const double* __restrict__ diag, const double* __restrict__ b,
-              double* x, double* work, double rel_tol, int max_iter, int* result) {
+              double* x, double* work, double rel_tol, int max_iter, int* result, int exact) {
     __shared__ double sh[4];
     __shared__ double scratch[kDotChunk];
     const int n = A.ru * A.rv;
@@ -1735,7 +1736,7 @@ __global__ void __launch_bounds__(NT, 1)
     double* z = work + n;
     double* p = work + 2 * (size_t)n;
     double* q = work + 3 * (size_t)n;
-    const double bnorm = sqrt(cta_ordered_dot(b, b, n, scratch, sh));
+    const double bnorm = sqrt(cta_ordered_dot(b, b, n, scratch, sh, exact != 0));
     if (bnorm == 0.0) {
         cta_fill(x, 0.0, n);
         if (threadIdx.x == 0) {
@@ -1746,8 +1747,8 @@ __global__ void __launch_bounds__(NT, 1)
     }
     cta_fill(x, 0.0, n);
     __syncthreads();
-    stencil_apply<kOutResid, Widths<DEG>::A>(A, x, r, b);
-    double rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh));
+    stencil_apply<kOutResid, Widths<DEG>::A>(A, x, r, b, exact != 0);
+    double rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh, exact != 0));
     if (rnorm <= rel_tol * bnorm) {
         if (threadIdx.x == 0) {
             result[0] = 1;
@@ -1759,11 +1760,11 @@ __global__ void __launch_bounds__(NT, 1)
         z[i] = r[i] / diag[i];
         p[i] = z[i];
     }
-    double rz = cta_ordered_dot(r, z, n, scratch, sh);
+    double rz = cta_ordered_dot(r, z, n, scratch, sh, exact != 0);
     int conv = 0, it = 1;
     for (; it <= max_iter; ++it) {
-        stencil_apply<kOutSet, Widths<DEG>::A>(A, p, q, nullptr);
-        const double pq = cta_ordered_dot(p, q, n, scratch, sh);
+        stencil_apply<kOutSet, Widths<DEG>::A>(A, p, q, nullptr, exact != 0);
+        const double pq = cta_ordered_dot(p, q, n, scratch, sh, exact != 0);
         if (pq <= 0.0) {
             conv = -1;
             break;
@@ -1773,13 +1774,13 @@ __global__ void __launch_bounds__(NT, 1)
             x[i] += alpha * p[i];
             r[i] += -alpha * q[i];
         }
-        rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh));
+        rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh, exact != 0));
         if (rnorm <= rel_tol * bnorm) {
             conv = 1;
             break;
         }
         for (int i = threadIdx.x; i < n; i += NT) z[i] = r[i] / diag[i];
-        const double rz_new = cta_ordered_dot(r, z, n, scratch, sh);
+        const double rz_new = cta_ordered_dot(r, z, n, scratch, sh, exact != 0);
         const double beta = rz_new / rz;
         rz = rz_new;
         for (int i = threadIdx.x; i < n; i += NT) p[i] = z[i] + beta * p[i];
@@ -1874,8 +1875,8 @@ void DegLaunch<DEG>::unit(const DevHier& H, int op, int arg, int arg2, const dou
 
 template <int DEG>
 void DegLaunch<DEG>::cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
-                        double rel_tol, int max_iter, int* result, cudaStream_t s) {
-    cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result);
+                        double rel_tol, int max_iter, int* result, int exact, cudaStream_t s) {
+    cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result, exact);
     PHI_CUDA(cudaGetLastError());
 }
 

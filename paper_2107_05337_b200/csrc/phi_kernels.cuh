@@ -36,7 +36,7 @@ struct DegLaunch {
     static void unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
                      long long ws_stride, cudaStream_t s);
     static void cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
-                   double rel_tol, int max_iter, int* result, cudaStream_t s);
+                   double rel_tol, int max_iter, int* result, int exact, cudaStream_t s);
     static void set_trace(long long* trace, int xmask);
 };
 extern template struct DegLaunch<1>;
@@ -57,7 +57,7 @@ void launch_vcycle(const DevHier& H, const double* B, long long ldb, double* X, 
 void launch_unit(const DevHier& H, int op, int arg, int arg2, const double* in, double* out, double* ws,
                  long long ws_stride, cudaStream_t s);
 void launch_cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
-               double rel_tol, int max_iter, int* result, cudaStream_t s);
+               double rel_tol, int max_iter, int* result, int exact, cudaStream_t s);
 void launch_restrict_first(const double* fg, const double* fu, double* cg, double* cu, int n,
                            cudaStream_t s);
 void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s);

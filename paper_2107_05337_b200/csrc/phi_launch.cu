@@ -186,8 +186,8 @@ void launch_unit(const DevHier& H, int op, int arg, int arg2, const double* in, 
 }
 
 void launch_cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work, double rel_tol,
-               int max_iter, int* result, cudaStream_t s) {
-    PHI_DEG_DISPATCH(degree_of(A), DegLaunch<DEG>::cg(A, diag, b, x, work, rel_tol, max_iter, result, s));
+               int max_iter, int* result, int exact, cudaStream_t s) {
+    PHI_DEG_DISPATCH(degree_of(A), DegLaunch<DEG>::cg(A, diag, b, x, work, rel_tol, max_iter, result, exact, s));
 }
 
 static DevBuf<long long> g_trace;
