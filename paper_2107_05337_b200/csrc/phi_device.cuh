@@ -1846,6 +1846,7 @@ void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (cl > 8) PHI_CUDA(cudaFuncSetAttribute(phi_wave_kernel<DEG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         PHI_CUDA(cudaLaunchKernelEx(&cfg, phi_wave_kernel<DEG>, H, Am, a, P, ws, ws_stride));
     } else {
         phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
