@@ -1155,7 +1155,12 @@ __device__ void coarse_solve(const DevHier& H, const double* b, double* x) {
 // A backward sweep mirrors both orders (lines v descending, iu descending).
 template <bool SM, int RM>
 __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double* b, double* x, double* o,
-                                              bool backward, int count) {
+                                              const double* bc, const double* xc, double* oc, bool backward,
+                                              int count) {
+    // cluster mode: the prologue is split over the cluster (bc, xc, oc: the
+    // main CTA's vectors as the cluster sees them), the chain runs on the
+    // main CTA; without clusters part = 0, parts = 1 and bc = b, ...
+    const int part = cl_rank(), parts = cl_size();
     // SM: x and o in shared memory (explicit shared accesses on the chain)
     const unsigned xs = SM ? sh_addr(x) : 0u, os = SM ? sh_addr(o) : 0u;
     auto ldx = [&](int j) -> double { return SM ? vlds_f64(xs + 8u * j) : x[j]; };
@@ -1169,23 +1174,23 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
     for (int c = 0; c < count; ++c) {
         // ---- 1. old part, scaled by 1/d
         constexpr int U = 4;  // rows per thread and pass: independent loads in flight
-        for (int i0 = threadIdx.x; i0 < n; i0 += U * NT) {
+        for (int i0 = threadIdx.x + part * U * NT; i0 < n; i0 += U * NT * parts) {
             double acc[U], sc[U];
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int i = min(i0 + uu * NT, n - 1);
                 const int iv = i / nf, iu = i - iv * nf;
-                double t = b[i];
+                double t = bc[i];
                 // forward: E, NW, N, NE (old); backward: W, SW, S, SE
                 const int du_in = backward ? -1 : 1, dv = -sv;
                 const int u1 = iu + du_in;
-                if (u1 >= 0 && u1 < nf) t -= a[(size_t)(4 + du_in) * n + i] * x[i + du_in];
+                if (u1 >= 0 && u1 < nf) t -= a[(size_t)(4 + du_in) * n + i] * xc[i + du_in];
                 const int v1 = iv + dv;
                 if (v1 >= 0 && v1 < nf) {
 #pragma unroll
                     for (int du = -1; du <= 1; ++du) {
                         const int u = iu + du;
-                        if (u >= 0 && u < nf) t -= a[(size_t)((dv + 1) * 3 + du + 1) * n + i] * x[i + dv * nf + du];
+                        if (u >= 0 && u < nf) t -= a[(size_t)((dv + 1) * 3 + du + 1) * n + i] * xc[i + dv * nf + du];
                     }
                 }
                 acc[uu] = t;
@@ -1193,11 +1198,11 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
             }
 #pragma unroll
             for (int uu = 0; uu < U; ++uu)
-                if (i0 + uu * NT < n) o[i0 + uu * NT] = acc[uu] * sc[uu];
+                if (i0 + uu * NT < n) oc[i0 + uu * NT] = acc[uu] * sc[uu];
         }
-        __syncthreads();
+        cl_sync();
         // ---- 2. the line chain
-        if (threadIdx.x < 32) {
+        if (threadIdx.x < 32 && part == 0) {
             const int lane = threadIdx.x;
             double on[RM];
             double4 cn[RM];
@@ -1287,29 +1292,32 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                 if (tr) tr[3] = clock64();
             }
         }
-        __syncthreads();
+        cl_sync();
     }
 }
 
 template <int RM>
 __device__ __forceinline__ void gs_line_sweeps_r(const DevHLevel& lv, const double* b, double* x, double* o,
-                                                 bool backward, int count) {
+                                                 const double* bc, const double* xc, double* oc, bool backward,
+                                                 int count) {
     if (__isShared(x) && __isShared(o))
-        gs_line_sweeps_t<true, RM>(lv, b, x, o, backward, count);
+        gs_line_sweeps_t<true, RM>(lv, b, x, o, bc, xc, oc, backward, count);
     else
-        gs_line_sweeps_t<false, RM>(lv, b, x, o, backward, count);
+        gs_line_sweeps_t<false, RM>(lv, b, x, o, bc, xc, oc, backward, count);
 }
+// Called by every CTA of the cluster (by the CTA alone without clusters).
 __device__ __forceinline__ void gs_line_sweeps(const DevHLevel& lv, const double* b, double* x, double* o,
-                                               bool backward, int count) {
+                                               const double* bc, const double* xc, double* oc, bool backward,
+                                               int count) {
     const int r = (lv.nf + 31) / 32;
     if (r <= 1)
-        gs_line_sweeps_r<1>(lv, b, x, o, backward, count);
+        gs_line_sweeps_r<1>(lv, b, x, o, bc, xc, oc, backward, count);
     else if (r <= 2)
-        gs_line_sweeps_r<2>(lv, b, x, o, backward, count);
+        gs_line_sweeps_r<2>(lv, b, x, o, bc, xc, oc, backward, count);
     else if (r <= 4)
-        gs_line_sweeps_r<4>(lv, b, x, o, backward, count);
+        gs_line_sweeps_r<4>(lv, b, x, o, bc, xc, oc, backward, count);
     else
-        gs_line_sweeps_r<8>(lv, b, x, o, backward, count);
+        gs_line_sweeps_r<8>(lv, b, x, o, bc, xc, oc, backward, count);
 }
 
 // x += C r for a dense column-major n x n operator (the collapsed coarse
@@ -1397,15 +1405,17 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + lv.n : -1;
         if (phase[l] == 0) {
             mark(23);
-            if (main) {
-                if (H.exact)
-                    gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
-                else if (lv.gsl)
-                    gs_line_sweeps(lv, b, x, w.hr[l], false, H.gs_pre);
-                else
-                    blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            if (!H.exact && lv.gsl) {  // every CTA: the prologues are split over the cluster
+                gs_line_sweeps(lv, b, x, w.hr[l], w.hbc[l], w.hxc[l], w.hrc[l], false, H.gs_pre);
+            } else {
+                if (main) {
+                    if (H.exact)
+                        gs_sweeps(lv, b, x, false, H.gs_pre, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+                    else
+                        blk_sweep(lv.gsb_fwd, H.gs_pre, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+                }
+                cl_sync();
             }
-            cl_sync();
             mark(l);
             stencil_apply<kOutResid, Widths<DEG>::H>(lv.a, w.hxc[l], w.hrc[l], w.hbc[l], H.exact != 0, part, parts);
             cl_sync();
@@ -1423,15 +1433,17 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             csr_apply<true>(lv.embed, w.hxc[l + 1], w.hxc[l], part, parts);  // x += E ec
             cl_sync();
             mark(21);
-            if (main) {
-                if (H.exact)
-                    gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
-                else if (lv.gsl)
-                    gs_line_sweeps(lv, b, x, w.hr[l], true, H.gs_post);
-                else
-                    blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+            if (!H.exact && lv.gsl) {
+                gs_line_sweeps(lv, b, x, w.hr[l], w.hbc[l], w.hxc[l], w.hrc[l], true, H.gs_post);
+            } else {
+                if (main) {
+                    if (H.exact)
+                        gs_sweeps(lv, b, x, true, H.gs_post, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
+                    else
+                        blk_sweep(lv.gsb_bwd, H.gs_post, x, xo, b, bo, w.ring_off, w.gs_slot_bytes, w.gs_n_slots);
+                }
+                cl_sync();
             }
-            cl_sync();
             mark(l);
             if (l == 0) break;
             --l;
@@ -1714,7 +1726,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (H.exact)
             gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
         else if (lv.gsl)
-            gs_line_sweeps(lv, w.hb[arg], w.hx[arg], w.hr[arg], arg2 != 0, 1);
+            gs_line_sweeps(lv, w.hb[arg], w.hx[arg], w.hr[arg], w.hb[arg], w.hx[arg], w.hr[arg], arg2 != 0, 1);
         else
             blk_sweep(arg2 ? lv.gsb_bwd : lv.gsb_fwd, 1, w.hx[arg], xo, w.hb[arg], bo, w.ring_off, w.gs_slot_bytes,
                       w.gs_n_slots);
