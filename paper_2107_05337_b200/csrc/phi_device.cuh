@@ -797,18 +797,15 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                                 ? c_tune.trace + kTriTraceBase + 16 * g
                                 : nullptr;
             if (tr) tr[0] = clock64();
-            const int seen = wait_ge(cnt + 4u * (g & (kBlkHand - 1)), P);
+            // one part in: the unit has landed (each worker waited for it)
+            const int seen = wait_ge(cnt + 4u * (g & (kBlkHand - 1)), 1);
             if (tr) tr[1] = clock64();
             // data dependence on the wait: none of these loads moves above it
-            const unsigned u = ring + slot * slot_bytes + (unsigned)(seen - P);
-            // ---- independent of block g-1: row, rhs, partial sums, inverse, fresh slots
+            const unsigned u = ring + slot * slot_bytes + (unsigned)(seen > 0 ? 0 : 1);
+            // ---- independent of block g-1: row, rhs, inverse, mid slots
             const int row = vlds_s32(u + 16u + 4u * lane);
             double rhs = 0.0;
             if (row >= 0) rhs = RSM ? vlds_f64(rs + 8u * row) : *reinterpret_cast<const volatile double*>(rg + row);
-            double part[kBlkMaxParts];
-#pragma unroll
-            for (int q = 0; q < kBlkMaxParts; ++q)
-                part[q] = q < P ? vlds_f64(cbuf + 8u * (((g & (kBlkHand - 1)) * kBlkMaxParts + q) * 32 + lane)) : 0.0;
             double iv[32];
 #pragma unroll
             for (int p2 = 0; p2 < 16; ++p2) lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
@@ -822,6 +819,14 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 fv[q] = 0.0;
                 if (q < mf) lds_slot(fr + 512u * q, fc[q], fv[q]);
             }
+            // ---- all parts in: the partial old sums
+            const int all = wait_ge(cnt + 4u * (g & (kBlkHand - 1)), P);
+            double part[kBlkMaxParts];
+#pragma unroll
+            for (int q = 0; q < kBlkMaxParts; ++q)
+                part[q] = q < P ? vlds_f64(cbuf + 8u * (((g & (kBlkHand - 1)) * kBlkMaxParts + q) * 32 + lane) +
+                                           (unsigned)(all - P))
+                                : 0.0;
             double old = 0.0;
 #pragma unroll
             for (int q = 0; q < kBlkMaxParts; ++q) old = old + part[q];
