@@ -72,6 +72,8 @@ struct DevHLevel {
 };
 
 constexpr int kMaxH = 12;
+/// Scratch of the cluster dense coarse product: r copy (<= 1024) + 128 partials.
+constexpr int kClScratch = 1024 + 160;
 /// Longest grid line of a line Gauss-Seidel sweep (32 lanes x 8 rows).
 constexpr int kLineMax = 256;
 /// Shortest grid line swept by lines (shorter levels: block sweeps).
@@ -117,6 +119,7 @@ struct SmemPlan {
     int dot_off;           // ordered-dot scratch
     int z_off;             // in-place triangular-solve vector (n_p + 1)
     int lvl_off[kMaxH];    // per h-level: b, x, r (3 n_l)
+    int cl_scr_off;        // cluster dense-apply scratch (kClScratch doubles) free during the W-cycle, -1: none
     int total;             // doubles
 };
 

@@ -200,6 +200,7 @@ struct Ws {
     double* dot;             // shared scratch for ordered dots
     int z_off, ring_off, slot_bytes, prod_off;  // g_smem offsets (-1: global)
     int n_slots, gs_slot_bytes, gs_n_slots;     // block-sweep rings (SmemPlan)
+    int cl_scr_off;                             // cluster dense-apply scratch (SmemPlan), -1: none
     int lvl_off[kMaxH];  // g_smem offset of level l's vectors (b, x, r), -1: global
     double* hb[kMaxH];
     double* hx[kMaxH];
@@ -222,6 +223,7 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     w.n_slots = P.n_slots;
     w.gs_slot_bytes = P.gs_slot_bytes;
     w.gs_n_slots = P.gs_n_slots;
+    w.cl_scr_off = P.cl_scr_off;
     double* g = base + 6 * np;
     for (int l = 0; l < H.n_h; ++l) {
         const int nl = H.h[l].n;
@@ -1344,6 +1346,44 @@ __device__ __noinline__ void dense_apply(const double* __restrict__ c, int n, co
     }
 }
 
+// Cluster version of dense_apply (scr: SmemPlan::cl_scr_off, free during the
+// W-cycle; without it the main CTA sits out): the rows are cut into `parts`
+// contiguous ranges; in each CTA four warps cover up to 128 rows and the other
+// four the second half of the columns; r (in the main CTA) is first copied
+// into this CTA's shared memory so that the column loop broadcasts it.
+// Caller: cl_sync after.
+__device__ __noinline__ void dense_apply_cl(const double* __restrict__ c, int n, const double* r_main,
+                                            double* x_main, int part, int parts, double* scr) {
+    double* rl = scr;           // n doubles
+    double* pp = scr + n + 1;   // 128 partial sums of the second column half
+    for (int j = threadIdx.x; j < n; j += NT) rl[j] = r_main[j];
+    __syncthreads();
+    const int chunk = (n + parts - 1) / parts;
+    const int r0 = part * chunk, r1 = min(n, r0 + chunk);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int jh = (n + 1) / 2;
+    for (int base = r0; base < r1; base += 128) {
+        const int i = base + (w & 3) * 32 + lane;  // this thread's row
+        const int j0 = (w >> 2) ? jh : 0, j1 = (w >> 2) ? n : jh;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (i < r1) {
+            int j = j0;
+            for (; j + 4 <= j1; j += 4) {
+                a0 = __fma_rn(__ldg(c + (size_t)j * n + i), rl[j], a0);
+                a1 = __fma_rn(__ldg(c + (size_t)(j + 1) * n + i), rl[j + 1], a1);
+                a2 = __fma_rn(__ldg(c + (size_t)(j + 2) * n + i), rl[j + 2], a2);
+                a3 = __fma_rn(__ldg(c + (size_t)(j + 3) * n + i), rl[j + 3], a3);
+            }
+            for (; j < j1; ++j) a0 = __fma_rn(__ldg(c + (size_t)j * n + i), rl[j], a0);
+        }
+        const double s = (a0 + a1) + (a2 + a3);
+        if (w >= 4) pp[(w & 3) * 32 + lane] = s;
+        __syncthreads();
+        if (w < 4 && i < r1) x_main[i] = x_main[i] + (s + pp[(w & 3) * 32 + lane]);
+        __syncthreads();
+    }
+}
+
 // h-multigrid W-cycle (pmultigrid.hpp:184-200) as an explicit per-level
 // phase machine (no device recursion):
 //   phase 0: pre-smooth, restrict, first coarse visit
@@ -1397,7 +1437,14 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             mark(23);
             stencil_apply<kOutResid, Widths<DEG>::H>(H.h[l].a, w.hxc[l], w.hrc[l], w.hbc[l], false, part, parts);
             cl_sync();
-            dense_apply(dop, H.h[l].n, w.hrc[l], w.hxc[l], part, parts);
+            if (parts > 1) {
+                double* scr = g_smem + (w.cl_scr_off >= 0 ? w.cl_scr_off : 0);
+                if (w.cl_scr_off >= 0)
+                    dense_apply_cl(dop, H.h[l].n, w.hrc[l], w.hxc[l], part, parts, scr);
+                else if (part > 0)  // the helpers' shared memory is free: they never sweep
+                    dense_apply_cl(dop, H.h[l].n, w.hrc[l], w.hxc[l], part - 1, parts - 1, scr);
+            } else
+                dense_apply(dop, H.h[l].n, w.hrc[l], w.hxc[l]);
             cl_sync();
             mark(22);
             if (l == 0) break;

@@ -135,6 +135,14 @@ SmemPlan phi_smem_plan(const DevHier& H) {
         }
     }
     top = std::max(top, lv);
+    // scratch of the cluster dense coarse product (W-cycle phase): the sweep
+    // ring below the level vectors if it is large enough, else above them
+    if (gs_tri >= (size_t)kClScratch)
+        P.cl_scr_off = 0;
+    else if (lv + kClScratch <= budget)
+        P.cl_scr_off = (int)lv, top = std::max(top, lv + kClScratch);
+    else
+        P.cl_scr_off = -1;
     P.total = (int)std::max(top, (size_t)kDotChunk);
     if (std::getenv("PHI_PLAN_DEBUG"))
         std::fprintf(stderr, "smem plan: slot %d B x %d, gs slot %d B x %d, prod @%d, z @%d, levels @%d.., total %d doubles\n",
