@@ -866,8 +866,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                     acc[(2 * p2 + 1) & 7] = __fma_rn(iv[2 * p2 + 1], t1, acc[(2 * p2 + 1) & 7]);
                 }
             }
-            double z = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-            if (c_tune.xmask & 2) z = t;  // developer timing: no inverse
+            const double z = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
             if (row >= 0) xst<XSM>(xg, xs, row, z);
             if constexpr (!XSM) __threadfence_block();  // global x: order the stores before the hand-off
             __syncwarp();
@@ -909,9 +908,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             const unsigned oc = u + kBlkFreshOff + 512u * mf + 384u * mo * q + 4u * lane;
             const unsigned ov = oc + 128u * mo + 4u * lane;
             double a0 = 0.0, a1 = 0.0;
-            if (c_tune.xmask & 8) {  // developer timing: no old sums
-                wait_ge(prog, need);
-            } else if (mo <= 8) {  // the common case: every load issued before the wait
+            if (mo <= 8) {  // the common case: every load issued before the wait
                 int c[8];
                 double v[8];
 #pragma unroll
