@@ -1228,6 +1228,9 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                 }
             };
             load_line(0);
+            double xp[RM];  // the previous line's new values (sweep order); none before line 0
+#pragma unroll
+            for (int r = 0; r < RM; ++r) xp[r] = 0.0;
             for (int q = 0; q < nf; ++q) {
                 long long* tr = (kTrace && c_tune.trace && blockIdx.x == 0 && lane == 0 && q < 1024)
                                     ? c_tune.trace + kTriTraceBase + 8 * q
@@ -1242,20 +1245,20 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                     cc[r] = cn[r];
                 }
                 if (q + 1 < nf) load_line(q + 1);
-                // beta: fresh entries of the previous line (zero coefficients
-                // outside the grid; clamped addresses)
+                // beta: fresh entries of the previous line, whose values this
+                // warp holds in registers (xp, sweep order); the neighbours
+                // across a lane boundary come by shuffle; positions outside
+                // the line hold zero (and carry zero coefficients)
+                const double lft = __shfl_up_sync(0xffffffffu, xp[RM - 1], 1);
+                const double rgt = __shfl_down_sync(0xffffffffu, xp[0], 1);
                 double bl[RM], al[RM];
 #pragma unroll
                 for (int r = 0; r < RM; ++r) {
-                    const int p = lane * R + r;
-                    const int iu = backward ? nf - 1 - p : p;
-                    double beta = oc[r];
-                    if (q > 0 && p < nf) {
-                        const int j0 = vp * nf + iu;
-                        const double xm = ldx(j0 - (iu > 0)), x0 = ldx(j0), xq = ldx(j0 + (iu + 1 < nf));
-                        beta = beta - ((cc[r].y * xm + cc[r].z * x0) + cc[r].w * xq);
-                    }
-                    bl[r] = beta;
+                    const double xl = r > 0 ? xp[r - 1] : (lane > 0 ? lft : 0.0);
+                    const double xr = r + 1 < RM ? xp[r + 1] : (lane < 31 ? rgt : 0.0);
+                    // coefficients in natural order: iu-1, iu, iu+1
+                    const double xm = backward ? xr : xl, xq = backward ? xl : xr;
+                    bl[r] = oc[r] - ((cc[r].y * xm + cc[r].z * xp[r]) + cc[r].w * xq);
                     al[r] = cc[r].x;
                 }
                 if (tr) tr[1] = clock64() + (long long)(bl[0] == 1.2345) + (long long)(al[0] == 1.5);
@@ -1283,8 +1286,9 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
 #pragma unroll
                 for (int r = 0; r < RM; ++r) {
                     const int p = lane * R + r;
+                    const double xval = r + 1 == R ? Bs : __fma_rn(al[r], prev, bl[r]);
+                    xp[r] = p < nf ? xval : 0.0;
                     if (p < nf) {
-                        const double xval = r + 1 == R ? Bs : __fma_rn(al[r], prev, bl[r]);
                         const int j = v * nf + (backward ? nf - 1 - p : p);
                         if (SM)
                             asm volatile("st.shared.f64 [%0], %1;" ::"r"(xs + 8u * j), "d"(xval) : "memory");
