@@ -77,7 +77,7 @@ constexpr int kClScratch = 1024 + 160;
 /// Longest grid line of a line Gauss-Seidel sweep (32 lanes x 8 rows).
 constexpr int kLineMax = 256;
 /// Shortest grid line swept by lines (shorter levels: block sweeps).
-constexpr int kLineMin = 48;
+constexpr int kLineMin = 24;
 
 /// One p-multigrid hierarchy (PMultigridHierarchy, pmultigrid.hpp:215-324)
 /// plus the spatial solver settings of its ThetaStepper (theta.hpp:66-75).
