@@ -56,12 +56,18 @@ typedef struct {
     int exact;
 } phi_pmg_options;
 
-/* SpatialSolverConfig, theta.hpp:66-75 (p-multigrid kind) */
+/* SpatialSolverKind, theta.hpp:64 */
+enum { PHI_SOLVER_PMG = 0, PHI_SOLVER_CG = 1 };
+
+/* SpatialSolverConfig, theta.hpp:66-75.  kind PHI_SOLVER_CG: Jacobi-
+ * preconditioned CG on the left-hand operator (solvers.hpp:21-75,
+ * theta.hpp:121-125); pmg and fixed_cycles are then unused. */
 typedef struct {
     double rel_tol; /* 1e-12 */
     int max_iter;   /* 400 */
     int fixed_cycles;
     phi_pmg_options pmg;
+    int kind; /* PHI_SOLVER_PMG (default) or PHI_SOLVER_CG */
 } phi_solver_config;
 
 /* MgritConfig, mgrit.hpp:17-31 (workers replaced by the device batch) */

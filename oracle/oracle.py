@@ -113,6 +113,9 @@ def ref_lib():
         L.ref_mgrit_create.restype = _vp
         L.ref_mgrit_create.argtypes = [_i, _i, _d, _d, _i, _d, _i, _d, _i, _vp, _i, _i, _i, _d,
                                        _i, _i, _i, _d, _i]
+        L.ref_mgrit_create_kind.restype = _vp
+        L.ref_mgrit_create_kind.argtypes = [_i, _i, _d, _d, _i, _d, _i, _d, _i, _vp, _i, _i, _i,
+                                            _d, _i, _i, _i, _i, _d, _i]
         L.ref_mgrit_free.argtypes = [_vp]
         L.ref_mgrit_levels.argtypes = [_vp, _vp, _vp]
         L.ref_mgrit_solve.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]
@@ -259,12 +262,14 @@ class RefMgrit:
     def __init__(self, degree, mesh_exponent, nt, *, kappa=1.0, t_final=0.1, theta=1.0,
                  source_kind=SOURCE_CONSTANT, source_param=1.0, init_kind=INIT_ZERO,
                  init_coeffs=None, cycle=CYCLE_V, relax=RELAX_FCF, m=2, halt_tol=1e-10,
-                 max_iter=50, coarse_floor=8, workers=1, rel_tol=1e-12, sp_max_iter=400):
+                 max_iter=50, coarse_floor=8, workers=1, rel_tol=1e-12, sp_max_iter=400,
+                 spatial_kind=0):
         L = ref_lib()
         self._coeffs = None if init_coeffs is None else np.ascontiguousarray(init_coeffs, np.float64)
-        self.h = L.ref_mgrit_create(degree, mesh_exponent, kappa, t_final, nt, theta, source_kind,
-                                    source_param, init_kind, _p(self._coeffs), cycle, relax, m,
-                                    halt_tol, max_iter, coarse_floor, workers, rel_tol, sp_max_iter)
+        self.h = L.ref_mgrit_create_kind(degree, mesh_exponent, kappa, t_final, nt, theta,
+                                         source_kind, source_param, init_kind, _p(self._coeffs),
+                                         cycle, relax, m, halt_tol, max_iter, coarse_floor, workers,
+                                         spatial_kind, rel_tol, sp_max_iter)
         if not self.h:
             raise RuntimeError(_ref_err())
         self.nt = nt
@@ -360,6 +365,8 @@ def oc_lib():
         L.oc_solve.argtypes = [_vp, _vp, _vp, _d, _i, _i, _i, _vp, _vp, _vp, _vp, _i]
         L.oc_stepper_create.restype = _vp
         L.oc_stepper_create.argtypes = [_vp, _d, _d, _d, _d, _i, _i]
+        L.oc_stepper_create_kind.restype = _vp
+        L.oc_stepper_create_kind.argtypes = [_vp, _d, _d, _d, _i, _d, _i, _i]
         L.oc_stepper_free.argtypes = [_vp]
         L.oc_stepper_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
         L.oc_sequential_integrate.argtypes = [_vp, _d, _d, _i, _d, _vp, _vp, _i, _d, _i, _vp, _vp,
@@ -367,6 +374,9 @@ def oc_lib():
         L.oc_mgrit_create.restype = _vp
         L.oc_mgrit_create.argtypes = [_vp, _d, _d, _i, _d, _vp, _vp, _i, _i, _i, _i, _d, _i, _i,
                                       _d, _i]
+        L.oc_mgrit_create_kind.restype = _vp
+        L.oc_mgrit_create_kind.argtypes = [_vp, _d, _d, _i, _d, _vp, _vp, _i, _i, _i, _i, _d, _i,
+                                           _i, _i, _d, _i]
         L.oc_mgrit_free.argtypes = [_vp]
         L.oc_mgrit_levels.argtypes = [_vp, _vp, _vp]
         L.oc_mgrit_solve.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i]
@@ -503,13 +513,13 @@ class OcHier:
 
 
 class OcStepper:
-    """Restated ThetaStepper (theta.hpp:92-146), p-multigrid kind."""
+    """Restated ThetaStepper (theta.hpp:92-146); kind 0 p-multigrid, 1 Jacobi CG."""
 
     def __init__(self, disc: OcDisc, kappa, dt, theta, rel_tol=1e-12, max_iter=400,
-                 fixed_cycles=0):
+                 fixed_cycles=0, kind=0):
         self.disc = disc
-        self.h = oc_lib().oc_stepper_create(disc.h, kappa, dt, theta, rel_tol, max_iter,
-                                            fixed_cycles)
+        self.h = oc_lib().oc_stepper_create_kind(disc.h, kappa, dt, theta, kind, rel_tol, max_iter,
+                                                 fixed_cycles)
         if not self.h:
             raise RuntimeError(_oc_err())
 
@@ -548,15 +558,17 @@ class OcMgrit:
 
     def __init__(self, disc: OcDisc, nt, *, kappa=1.0, t_final=0.1, theta=1.0, u0=None,
                  loads=None, load_steady=False, cycle=CYCLE_V, relax=RELAX_FCF, m=2,
-                 halt_tol=1e-10, max_iter=50, coarse_floor=8, rel_tol=1e-12, sp_max_iter=400):
+                 halt_tol=1e-10, max_iter=50, coarse_floor=8, rel_tol=1e-12, sp_max_iter=400,
+                 spatial_kind=0):
         self.disc = disc
         self.nt = nt
         self.max_iter = max_iter
         self._u0 = None if u0 is None else np.ascontiguousarray(u0, np.float64)
         self._loads = None if loads is None else np.ascontiguousarray(loads, np.float64)
-        self.h = oc_lib().oc_mgrit_create(disc.h, kappa, t_final, nt, theta, _p(self._u0),
-                                          _p(self._loads), int(load_steady), cycle, relax, m,
-                                          halt_tol, max_iter, coarse_floor, rel_tol, sp_max_iter)
+        self.h = oc_lib().oc_mgrit_create_kind(disc.h, kappa, t_final, nt, theta, _p(self._u0),
+                                               _p(self._loads), int(load_steady), cycle, relax, m,
+                                               halt_tol, max_iter, coarse_floor, spatial_kind,
+                                               rel_tol, sp_max_iter)
         if not self.h:
             raise RuntimeError(_oc_err())
 

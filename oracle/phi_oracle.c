@@ -660,22 +660,37 @@ int oc_solve(const oc_hier* h, const double* b, double* x, double rel_tol, int m
 struct oc_stepper {
     const oc_disc* d;
     mat a_plus, a_minus;
-    oc_hier* pmg;
+    int kind;      /* SpatialSolverKind (theta.hpp:64): 0 pmg, 1 cg */
+    oc_hier* pmg;  /* pmg kind */
+    double* diag;  /* cg kind: diagonal_of(a_plus) (sparse.hpp:180-184) */
     double rel_tol;
     int max_iter, fixed_cycles;
 };
 
-/* theta.hpp:94-103 (pmg solver kind) */
-oc_stepper* oc_stepper_create(const oc_disc* d, double kappa, double dt, double theta,
-                              double rel_tol, int max_iter, int fixed_cycles) {
+/* theta.hpp:94-103 */
+oc_stepper* oc_stepper_create_kind(const oc_disc* d, double kappa, double dt, double theta,
+                                   int kind, double rel_tol, int max_iter, int fixed_cycles) {
+    if (kind != 0 && kind != 1) {
+        set_err("unknown spatial solver kind");
+        return NULL;
+    }
     oc_stepper* s = (oc_stepper*)calloc(1, sizeof(oc_stepper));
     s->d = d;
+    s->kind = kind;
     sparse_add(1.0, &d->mass_p, kappa * dt * theta, &d->stiff_p, &s->a_plus);
     sparse_add(1.0, &d->mass_p, -kappa * dt * (1.0 - theta), &d->stiff_p, &s->a_minus);
-    s->pmg = oc_hier_create(d, kappa * dt * theta, 1, 1, 2, 2, 1e-13, 0);
-    if (!s->pmg) {
-        oc_stepper_free(s);
-        return NULL;
+    if (kind == 0) {
+        s->pmg = oc_hier_create(d, kappa * dt * theta, 1, 1, 2, 2, 1e-13, 0);
+        if (!s->pmg) {
+            oc_stepper_free(s);
+            return NULL;
+        }
+    } else {
+        const int n = s->a_plus.n_rows;
+        s->diag = (double*)calloc((size_t)n, sizeof(double));
+        for (int i = 0; i < n; ++i)
+            for (int e = s->a_plus.ro[i]; e < s->a_plus.ro[i + 1]; ++e)
+                if (s->a_plus.ci[e] == i) s->diag[i] = s->a_plus.v[e];
     }
     s->rel_tol = rel_tol;
     s->max_iter = max_iter;
@@ -683,20 +698,94 @@ oc_stepper* oc_stepper_create(const oc_disc* d, double kappa, double dt, double 
     return s;
 }
 
+oc_stepper* oc_stepper_create(const oc_disc* d, double kappa, double dt, double theta,
+                              double rel_tol, int max_iter, int fixed_cycles) {
+    return oc_stepper_create_kind(d, kappa, dt, theta, 0, rel_tol, max_iter, fixed_cycles);
+}
+
 void oc_stepper_free(oc_stepper* s) {
     if (!s) return;
     mat_free(&s->a_plus);
     mat_free(&s->a_minus);
     oc_hier_free(s->pmg);
+    free(s->diag);
     free(s);
 }
 
-/* theta.hpp:111-126 -- solve_lhs with the pmg kind */
+/* solvers.hpp:21-75 -- Jacobi-preconditioned CG; x holds x0 (zeros when the
+ * reference's x0 is empty).  Returns 0, or 3 on breakdown (p^T A p <= 0). */
+static int cg_solve(const mat* am, const double* b, double* x, double rel_tol, int max_iter,
+                    const double* diag, int* iters, int* converged) {
+    const int n = am->n_rows;
+    const oc_csr a = view(am);
+    *iters = 0;
+    *converged = 0;
+    const double bnorm = sqrt(dot(b, b, n));
+    if (bnorm == 0.0) {
+        for (int i = 0; i < n; ++i) x[i] = 0.0;
+        *converged = 1;
+        return 0;
+    }
+    double* r = (double*)malloc(sizeof(double) * (size_t)n * 4);
+    double *z = r + n, *p = r + 2 * (size_t)n, *q = r + 3 * (size_t)n;
+    oc_spmv(&a, x, q);
+    for (int i = 0; i < n; ++i) r[i] = b[i] - q[i];  /* subtract(b, spmv(a, x)) */
+    double rnorm = sqrt(dot(r, r, n));
+    int rc = 0;
+    if (rnorm <= rel_tol * bnorm) {
+        *converged = 1;
+        goto done;
+    }
+    for (int i = 0; i < n; ++i) z[i] = r[i] / diag[i];
+    for (int i = 0; i < n; ++i) p[i] = z[i];
+    double rz = dot(r, z, n);
+    for (int it = 1; it <= max_iter; ++it) {
+        oc_spmv(&a, p, q);
+        const double pq = dot(p, q, n);
+        if (pq <= 0.0) {
+            set_err("cg_solve: breakdown, matrix not SPD");
+            rc = 3;
+            goto done;
+        }
+        const double alpha = rz / pq;
+        for (int i = 0; i < n; ++i) x[i] += alpha * p[i];
+        for (int i = 0; i < n; ++i) r[i] += -alpha * q[i];
+        rnorm = sqrt(dot(r, r, n));
+        *iters = it;
+        if (rnorm <= rel_tol * bnorm) {
+            *converged = 1;
+            goto done;
+        }
+        for (int i = 0; i < n; ++i) z[i] = r[i] / diag[i];
+        const double rz_new = dot(r, z, n);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    }
+done:
+    free(r);
+    return rc;
+}
+
+/* theta.hpp:111-126 -- solve_lhs */
 static int solve_lhs(const oc_stepper* s, const double* rhs, const double* guess, double* out,
                      int* iters) {
     const int n = s->d->n_p;
     int conv = 0;
     double fr = 0.0;
+    if (s->kind == 1) {
+        if (guess)
+            memcpy(out, guess, sizeof(double) * (size_t)n);
+        else
+            memset(out, 0, sizeof(double) * (size_t)n);
+        const int rc = cg_solve(&s->a_plus, rhs, out, s->rel_tol, s->max_iter, s->diag, iters, &conv);
+        if (rc) return rc;
+        if (!conv) {
+            set_err("spatial solve did not converge (cg)");
+            return 2;
+        }
+        return 0;
+    }
     if (guess) memcpy(out, guess, sizeof(double) * (size_t)n);
     int rc = oc_solve(s->pmg, rhs, out, s->rel_tol, s->max_iter, s->fixed_cycles, guess == NULL,
                       iters, &conv, &fr, NULL, 0);
@@ -784,6 +873,15 @@ oc_mgrit* oc_mgrit_create(const oc_disc* d, double kappa, double t_final, int nt
                           const double* u0, const double* loads, int load_steady, int cycle,
                           int relax, int m, double halt_tol, int max_iter, int coarse_floor,
                           double rel_tol, int sp_max_iter) {
+    return oc_mgrit_create_kind(d, kappa, t_final, nt, theta, u0, loads, load_steady, cycle, relax,
+                                m, halt_tol, max_iter, coarse_floor, 0, rel_tol, sp_max_iter);
+}
+
+oc_mgrit* oc_mgrit_create_kind(const oc_disc* d, double kappa, double t_final, int nt,
+                               double theta, const double* u0, const double* loads,
+                               int load_steady, int cycle, int relax, int m, double halt_tol,
+                               int max_iter, int coarse_floor, int spatial_kind, double rel_tol,
+                               int sp_max_iter) {
     if (m < 2) {
         set_err("MgritConfig: m must be >= 2");
         return NULL;
@@ -826,7 +924,7 @@ oc_mgrit* oc_mgrit_create(const oc_disc* d, double kappa, double t_final, int nt
         level_t* lv = &g->lev[l];
         lv->steps = steps[l];
         lv->dt = dt0 * (nt / steps[l]);
-        lv->stepper = oc_stepper_create(d, kappa, lv->dt, theta, rel_tol, sp_max_iter, 0);
+        lv->stepper = oc_stepper_create_kind(d, kappa, lv->dt, theta, spatial_kind, rel_tol, sp_max_iter, 0);
         if (!lv->stepper) {
             oc_mgrit_free(g);
             return NULL;

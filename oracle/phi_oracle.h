@@ -72,6 +72,10 @@ int oc_solve(const oc_hier* h, const double* b, double* x, double rel_tol, int m
 /* ---- ThetaStepper (theta.hpp:92-146) ------------------------------------- */
 oc_stepper* oc_stepper_create(const oc_disc* d, double kappa, double dt, double theta,
                               double rel_tol, int max_iter, int fixed_cycles);
+/* the same with SpatialSolverKind (theta.hpp:64): 0 pmg, 1 cg (Jacobi-preconditioned,
+ * solvers.hpp:21-75) */
+oc_stepper* oc_stepper_create_kind(const oc_disc* d, double kappa, double dt, double theta,
+                                   int kind, double rel_tol, int max_iter, int fixed_cycles);
 void oc_stepper_free(oc_stepper*);
 /* u_next = Phi(u_prev) + load (load may be NULL); guess may be NULL (empty) */
 int oc_stepper_step(const oc_stepper* s, const double* u_prev, const double* load,
@@ -89,6 +93,11 @@ oc_mgrit* oc_mgrit_create(const oc_disc* d, double kappa, double t_final, int nt
                           const double* u0, const double* loads, int load_steady, int cycle,
                           int relax, int m, double halt_tol, int max_iter, int coarse_floor,
                           double rel_tol, int sp_max_iter);
+oc_mgrit* oc_mgrit_create_kind(const oc_disc* d, double kappa, double t_final, int nt,
+                               double theta, const double* u0, const double* loads,
+                               int load_steady, int cycle, int relax, int m, double halt_tol,
+                               int max_iter, int coarse_floor, int spatial_kind, double rel_tol,
+                               int sp_max_iter);
 void oc_mgrit_free(oc_mgrit*);
 int oc_mgrit_levels(const oc_mgrit* g, int* steps, double* dts);
 int oc_mgrit_solve(oc_mgrit* g, int* iterations, int* converged, double* g_norm, double* final_rel,

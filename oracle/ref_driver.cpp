@@ -306,11 +306,12 @@ int ref_coarse_solve(void* p, const double* b, double* x, int n) {
 
 // Spline evaluation of free coefficients at (x, y) -> used to build golden
 // initial conditions consistently with the reference's basis.
-void* ref_mgrit_create(int degree, int mesh_exponent, double kappa, double t_final, int nt,
-                       double theta, int source_kind, double source_param, int init_kind,
-                       const double* init_coeffs, int cycle, int relax, int m, double halt_tol,
-                       int max_iter, int coarse_floor, int workers, double rel_tol,
-                       int sp_max_iter) {
+// spatial_kind: SpatialSolverKind (theta.hpp:64), 0 pmg, 1 cg
+void* ref_mgrit_create_kind(int degree, int mesh_exponent, double kappa, double t_final, int nt,
+                            double theta, int source_kind, double source_param, int init_kind,
+                            const double* init_coeffs, int cycle, int relax, int m,
+                            double halt_tol, int max_iter, int coarse_floor, int workers,
+                            int spatial_kind, double rel_tol, int sp_max_iter) {
     try {
         auto* g = new RefMgrit;
         ThreadPool pool(workers > 0 ? workers : 1);
@@ -331,6 +332,7 @@ void* ref_mgrit_create(int degree, int mesh_exponent, double kappa, double t_fin
         g->cfg.max_iter = max_iter;
         g->cfg.coarse_floor = coarse_floor;
         g->cfg.workers = workers > 0 ? workers : 1;
+        g->scfg.kind = spatial_kind == 1 ? SpatialSolverKind::cg : SpatialSolverKind::pmg;
         g->scfg.rel_tol = rel_tol;
         g->scfg.max_iter = sp_max_iter;
         g->solver = std::make_unique<MgritSolver>(g->d, g->ps, g->cfg, g->scfg);
@@ -339,6 +341,16 @@ void* ref_mgrit_create(int degree, int mesh_exponent, double kappa, double t_fin
         fail(e);
         return nullptr;
     }
+}
+
+void* ref_mgrit_create(int degree, int mesh_exponent, double kappa, double t_final, int nt,
+                       double theta, int source_kind, double source_param, int init_kind,
+                       const double* init_coeffs, int cycle, int relax, int m, double halt_tol,
+                       int max_iter, int coarse_floor, int workers, double rel_tol,
+                       int sp_max_iter) {
+    return ref_mgrit_create_kind(degree, mesh_exponent, kappa, t_final, nt, theta, source_kind,
+                                 source_param, init_kind, init_coeffs, cycle, relax, m, halt_tol,
+                                 max_iter, coarse_floor, workers, 0, rel_tol, sp_max_iter);
 }
 
 void ref_mgrit_free(void* p) { delete static_cast<RefMgrit*>(p); }

@@ -66,6 +66,7 @@ HierOptions to_opts(const phi_pmg_options* o) {
 SolverConfig to_cfg(const phi_solver_config* c) {
     SolverConfig s;
     if (c) {
+        s.kind = c->kind;
         s.rel_tol = c->rel_tol;
         s.max_iter = c->max_iter;
         s.fixed_cycles = c->fixed_cycles;
@@ -156,6 +157,7 @@ extern "C" {
 const char* phi_last_error(void) { return g_err.c_str(); }
 
 void phi_default_solver_config(phi_solver_config* c) {
+    c->kind = PHI_SOLVER_PMG;
     c->rel_tol = 1e-12;
     c->max_iter = 400;
     c->fixed_cycles = 0;
@@ -437,7 +439,7 @@ static void stepper_check(phi_stepper* s, const std::string& prefix) {
     const auto e = s->err.download(s->s);
     if (e[0]) {
         const double rel = s->err_rel.download(s->s)[0];
-        throw NotConverged(prefix + "spatial solve did not converge (p-multigrid), residual " + std::to_string(rel));
+        throw NotConverged(prefix + spatial_failure(s->st->cfg.kind, rel));
     }
 }
 
@@ -519,8 +521,8 @@ int phi_sequential_integrate(phi_stepper* s, int nt, const double* u0, const dou
         const auto e = s->err.download(s->s);
         if (e[0]) {
             const double rel = s->err_rel.download(s->s)[0];
-            throw NotConverged("sequential_integrate: step " + std::to_string(e[1]) +
-                               ": spatial solve did not converge (p-multigrid), residual " + std::to_string(rel));
+            throw NotConverged("sequential_integrate: step " + std::to_string(e[1]) + ": " +
+                               spatial_failure(s->st->cfg.kind, rel));
         }
     });
 }

@@ -105,6 +105,10 @@ struct DevHier {
     int max_iter;
     int fixed_cycles;
     int exact;  // 1: the reference's sequential summation order; 0: reassociated sums
+    // SpatialSolverKind (theta.hpp:64): 0 p-multigrid, 1 Jacobi-preconditioned CG
+    // (solvers.hpp:21-75; then only n_p, A and diag are set, n_h = 0)
+    int kind;
+    const double* diag;  // cg kind: diagonal_of(A) (sparse.hpp:180-184), the centre plane of A
 };
 
 /// Shared-memory placement of the latency-critical vectors of one CTA (offsets

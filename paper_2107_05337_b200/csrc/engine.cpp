@@ -208,14 +208,15 @@ DevBlk Hier::BlkDev::view() const {
     return b;
 }
 
-Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_, cudaStream_t s)
-    : disc(std::move(disc_)), c(c_), opt(opt_) {
+Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_, cudaStream_t s, bool cg_only_)
+    : disc(std::move(disc_)), c(c_), opt(opt_), cg_only(cg_only_) {
     const Disc& d = *disc;
     A.ru = A.rv = A.cu = A.cv = d.nf_p;
     A.lo = d.M.lo;
     A.hi = d.M.hi;
     A.vals.alloc(A.size());
     launch_axpby(d.M.vals.get(), c, d.K.vals.get(), A.vals.get(), A.size(), s);
+    if (cg_only) return;
     const HostCsr ah = stencil_to_csr(A);
     ilut_factor(ah, opt.ilut_tau, opt.ilut_fill, L_host, U_host);
     // exact mode: level-scheduled streams (the reference's summation order);
@@ -292,6 +293,17 @@ DevHier Hier::view(const SolverConfig& cfg) const {
     const Disc& d = *disc;
     if ((int)d.h.size() > kMaxH) throw InvalidArgument("too many h-levels");
     DevHier H{};
+    if (cg_only) {  // CG kind: the operator and its diagonal (the centre plane)
+        H.n_p = d.n_p;
+        H.A = A.view();
+        const int w = A.hi - A.lo + 1;
+        H.diag = A.vals.get() + (size_t)((w * w - 1) / 2) * d.n_p;
+        H.kind = 1;
+        H.rel_tol = cfg.rel_tol;
+        H.max_iter = cfg.max_iter;
+        H.exact = opt.exact;
+        return H;
+    }
     H.n_p = d.n_p;
     H.n_1 = d.n_1;
     H.n_h = (int)d.h.size();
@@ -356,10 +368,17 @@ void Workspace::ensure(const DevHier& H) {
 // ---------------------------------------------------------------------------
 // Stepper
 // ---------------------------------------------------------------------------
+std::string spatial_failure(int kind, double rel) {
+    if (kind == 1)
+        return rel < 0.0 ? "cg_solve: breakdown, matrix not SPD" : "spatial solve did not converge (cg)";
+    return "spatial solve did not converge (p-multigrid), residual " + std::to_string(rel);
+}
+
 Stepper::Stepper(std::shared_ptr<const Disc> disc_, double kappa_, double dt_, double theta_,
                  const SolverConfig& cfg_, cudaStream_t s)
     : disc(std::move(disc_)), kappa(kappa_), dt(dt_), theta(theta_), cfg(cfg_) {
-    hier = std::make_unique<Hier>(disc, kappa * dt * theta, cfg.pmg, s);
+    if (cfg.kind != 0 && cfg.kind != 1) throw InvalidArgument("unknown spatial solver kind");
+    hier = std::make_unique<Hier>(disc, kappa * dt * theta, cfg.pmg, s, cfg.kind == 1);
     const Disc& d = *disc;
     Aminus.ru = Aminus.rv = Aminus.cu = Aminus.cv = d.nf_p;
     Aminus.lo = d.M.lo;
@@ -546,8 +565,8 @@ void Mgrit::check_errors() {
     const auto e = err.download(stream);
     if (e[0]) {
         const double rel = err_rel.download(stream)[0];
-        throw NotConverged("MGRIT level " + std::to_string(e[2]) + ", time step " + std::to_string(e[1]) +
-                           ": spatial solve did not converge (p-multigrid), residual " + std::to_string(rel));
+        throw NotConverged("MGRIT level " + std::to_string(e[2]) + ", time step " + std::to_string(e[1]) + ": " +
+                           spatial_failure(scfg.kind, rel));
     }
 }
 

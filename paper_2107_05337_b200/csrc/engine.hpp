@@ -73,7 +73,8 @@ struct HierOptions {  // PMultigridOptions (pmultigrid.hpp:161-168)
     int dense_cluster_max = 1024;  // ... in cluster mode (the product is split over the cluster's SMs)
 };
 
-struct SolverConfig {  // SpatialSolverConfig (theta.hpp:66-75), pmg kind
+struct SolverConfig {  // SpatialSolverConfig (theta.hpp:66-75)
+    int kind = 0;  // SpatialSolverKind (theta.hpp:64): 0 pmg, 1 cg (Jacobi-preconditioned)
     double rel_tol = 1e-12;
     int max_iter = 400;
     int fixed_cycles = 0;
@@ -91,9 +92,13 @@ struct Workspace {
 /// PMultigridHierarchy(disc, c, opt) (pmultigrid.hpp:215-324) on device.
 class Hier {
 public:
-    Hier(std::shared_ptr<const Disc> disc, double c, const HierOptions& opt, cudaStream_t s = nullptr);
+    /// cg_only: the CG kind's left-hand operator alone (A = M + c K; no ILUT,
+    /// no h-levels -- the reference builds no hierarchy then, theta.hpp:99-102)
+    Hier(std::shared_ptr<const Disc> disc, double c, const HierOptions& opt, cudaStream_t s = nullptr,
+         bool cg_only = false);
     std::shared_ptr<const Disc> disc;
     double c = 0.0;
+    bool cg_only = false;
     HierOptions opt;
     StencilBuf A;                       // M + c K
     std::vector<StencilBuf> a_h;        // per h-level
@@ -134,6 +139,10 @@ public:
     DevHier view(const SolverConfig& cfg) const;
     HostCsr a_h_csr(int l) const;
 };
+
+/// Message of a failed spatial solve (theta.hpp:116-118, 123-124; a negative
+/// residual marks a CG breakdown, solvers.hpp:59).
+std::string spatial_failure(int kind, double rel);
 
 /// ThetaStepper (theta.hpp:92-146): Phi(u) = (M + k dt th K)^-1 ((M - k dt (1-th) K) u + load).
 class Stepper {

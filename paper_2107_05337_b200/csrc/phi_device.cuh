@@ -196,6 +196,7 @@ struct Ws {
     double* hxc[kMaxH];
     double* hrc[kMaxH];
     double *b, *x, *r, *zg;  // global
+    double *cgp, *cgq;       // global: the CG kind's search direction and its product
     double* z;               // in-place triangular-solve vector (n_p + 1 slots)
     double* dot;             // shared scratch for ordered dots
     int z_off, ring_off, slot_bytes, prod_off;  // g_smem offsets (-1: global)
@@ -214,6 +215,8 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     w.x = base + np;
     w.r = base + 2 * np;
     w.zg = base + 3 * np;
+    w.cgp = base + 4 * np;  // the CG kind's plan keeps z in shared memory or unused
+    w.cgq = base + 5 * np;
     w.z = P.z_off >= 0 ? smem + P.z_off : base + 4 * np;
     w.dot = smem + P.dot_off;
     w.z_off = P.z_off;
@@ -235,6 +238,7 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
         g += 3 * (size_t)nl + 1;
     }
     w.zc = cl_main(w.z);
+    if (H.n_h == 0) return w;  // CG kind: no hierarchy
     w.hb0c = cl_main(w.hb[0]);
     w.hx0c = cl_main(w.hx[0]);
     for (int l = 0; l < H.n_h; ++l) {
@@ -1560,6 +1564,66 @@ __device__ double rel_residual(const DevHier& H, const Ws& w, double bnorm, doub
     return sqrt(d) / bnorm;
 }
 
+// The CG kind's solve of one Phi (theta.hpp:121-125): Jacobi-preconditioned CG
+// on A from the guess in w.x (solvers.hpp:21-75), b = w.b, |b| = bnorm > 0.
+// The vectors live in the global workspace; with a cluster every phase is
+// split by row over its CTAs (each CTA forms the dot products over the whole
+// vectors in the same order, so all agree).  exact: the reference's operator
+// rows and index-ordered dots.  rel < 0 on breakdown (p^T A p <= 0).
+template <int DEG>
+__device__ __noinline__ void cg_point(const DevHier& H, const Ws& w, double bnorm, double* sh, int& iters, int& conv,
+                                      double& rel) {
+    const int n = H.n_p;
+    const int part = cl_rank(), parts = cl_size();
+    const bool ex = H.exact != 0;
+    const double* __restrict__ diag = H.diag;
+    double *x = w.x, *r = w.r, *z = w.zg, *p = w.cgp, *q = w.cgq;
+    stencil_apply<kOutResid, Widths<DEG>::A>(H.A, x, r, w.b, ex, part, parts);  // r = b - A x
+    cl_sync();
+    double rnorm = sqrt(cta_ordered_dot(r, r, n, w.dot, sh, ex));
+    rel = rnorm / bnorm;
+    if (rnorm <= H.rel_tol * bnorm) {
+        conv = 1;
+        return;
+    }
+    for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
+        const double zi = r[i] / diag[i];
+        z[i] = zi;
+        p[i] = zi;
+    }
+    cl_sync();
+    double rz = cta_ordered_dot(r, z, n, w.dot, sh, ex);
+    for (int it = 1; it <= H.max_iter; ++it) {
+        stencil_apply<kOutSet, Widths<DEG>::A>(H.A, p, q, nullptr, ex, part, parts);
+        cl_sync();
+        const double pq = cta_ordered_dot(p, q, n, w.dot, sh, ex);
+        if (pq <= 0.0) {  // breakdown: not SPD
+            rel = -1.0;
+            return;
+        }
+        const double alpha = rz / pq;
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
+            x[i] += alpha * p[i];
+            r[i] += -alpha * q[i];
+        }
+        cl_sync();
+        rnorm = sqrt(cta_ordered_dot(r, r, n, w.dot, sh, ex));
+        iters = it;
+        rel = rnorm / bnorm;
+        if (rnorm <= H.rel_tol * bnorm) {
+            conv = 1;
+            return;
+        }
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) z[i] = r[i] / diag[i];
+        cl_sync();
+        const double rz_new = cta_ordered_dot(r, z, n, w.dot, sh, ex);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) p[i] = z[i] + beta * p[i];
+        cl_sync();
+    }
+}
+
 // One Phi application: build b, solve (pmultigrid.hpp:271-307), epilogue.
 template <int DEG>
 __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, const WaveArgs& a, const Ws& w, int task,
@@ -1607,6 +1671,8 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
         cta_fill(w.x, 0.0, n, part, parts);  // zero rhs -> zero solution, not the guess
         conv = 1;
         cl_sync();
+    } else if (H.kind == 1) {
+        cg_point<DEG>(H, w, bnorm, sh, iters, conv, rel);
     } else if (H.fixed_cycles > 0) {
         for (int c = 0; c < H.fixed_cycles; ++c) vcycle<DEG>(H, w);
         iters = H.fixed_cycles;

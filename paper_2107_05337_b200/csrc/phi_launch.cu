@@ -87,6 +87,11 @@ SmemPlan phi_smem_plan(const DevHier& H) {
     P.ring_off = 0;
     P.dot_off = 0;
     for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
+    if (H.kind == 1) {  // CG kind: the ordered-dot scratch only (vectors in global memory)
+        P.prod_off = P.z_off = P.cl_scr_off = -1;
+        P.total = kDotChunk;
+        return P;
+    }
     size_t tri, gs_tri;
     if (H.exact) {
         int slot = std::max(H.L.max_unit_bytes, H.U.max_unit_bytes);

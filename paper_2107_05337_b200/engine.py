@@ -54,9 +54,12 @@ class PmgOptions(C.Structure):
                 ("nu_post", C.c_int), ("gs_pre", C.c_int), ("gs_post", C.c_int), ("exact", C.c_int)]
 
 
+SOLVER_PMG, SOLVER_CG = 0, 1  # SpatialSolverKind (theta.hpp:64)
+
+
 class SolverConfig(C.Structure):
     _fields_ = [("rel_tol", C.c_double), ("max_iter", C.c_int), ("fixed_cycles", C.c_int),
-                ("pmg", PmgOptions)]
+                ("pmg", PmgOptions), ("kind", C.c_int)]
 
 
 class MgritConfig(C.Structure):
@@ -169,6 +172,7 @@ def dev_tuning(tri_warps=16, gs_warps=16, sleep_ns=0) -> None:
 
 
 def default_solver_config(**kw) -> SolverConfig:
+    """SpatialSolverConfig (theta.hpp:66-75); kind=SOLVER_CG selects the Jacobi CG."""
     c = SolverConfig()
     lib().phi_default_solver_config(C.byref(c))
     for k, v in kw.items():

@@ -20,6 +20,7 @@ Fixtures
   mgrit_c1.npz    BASELINE.json config 1 (p=2, h=2^-4, Nt=100, two-level m=4, FCF,
                   f=0, u0=sin sin): MgritSolver::solve() (mgrit.hpp:93-118) result,
                   residual history, projected u0 and the trajectory.
+  mgrit_cg.npz    as mgrit_src.npz with the CG spatial solver (theta.hpp:121-125)
   mgrit_src.npz   the config-2 shape at small size (p=3, h=2^-4, Nt=32, m=8, transient
                   2 pi^2 e^-t sin sin source, spline u0 from seeded U[-1,1] coefficients):
                   result, u0, the level-0 load terms and the trajectory.
@@ -112,23 +113,37 @@ def mgrit_fixture(p, k, nt, **kw) -> dict:
     return out
 
 
-def main() -> None:
+def fixtures() -> dict:
+    """name -> builder of each committed fixture."""
+    coeffs = np.random.default_rng(12345).uniform(-1.0, 1.0, (2 ** 4 + 3 - 2) ** 2)
+    return {
+        "ops_p2k3.npz": ops_fixture,
+        "mgrit_c1.npz": lambda: mgrit_fixture(2, 4, 100, cycle=O.CYCLE_TWO_LEVEL, m=4,
+                                              source_param=0.0, init_kind=O.INIT_SIN),
+        "mgrit_src.npz": lambda: dict(coeffs=coeffs, **mgrit_fixture(
+            3, 4, 32, cycle=O.CYCLE_TWO_LEVEL, m=8, source_kind=O.SOURCE_SIN_EXP,
+            source_param=2 * np.pi ** 2, init_kind=O.INIT_COEFFS, init_coeffs=coeffs)),
+        # the CG spatial-solver kind (SpatialSolverKind::cg, theta.hpp:64, 121-125)
+        "mgrit_cg.npz": lambda: dict(coeffs=coeffs, **mgrit_fixture(
+            3, 4, 32, cycle=O.CYCLE_TWO_LEVEL, m=8, source_kind=O.SOURCE_SIN_EXP,
+            source_param=2 * np.pi ** 2, init_kind=O.INIT_COEFFS, init_coeffs=coeffs,
+            spatial_kind=1)),
+    }
+
+
+def main(only=None) -> None:
     if not O.ref_available():
         raise SystemExit("oracle/_ref missing: run `make -C oracle ref` (needs /root/reference)")
-    np.savez_compressed(os.path.join(HERE, "ops_p2k3.npz"), **ops_fixture())
-    np.savez_compressed(os.path.join(HERE, "mgrit_c1.npz"),
-                        **mgrit_fixture(2, 4, 100, cycle=O.CYCLE_TWO_LEVEL, m=4, source_param=0.0,
-                                        init_kind=O.INIT_SIN))
-    coeffs = np.random.default_rng(12345).uniform(-1.0, 1.0, (2 ** 4 + 3 - 2) ** 2)
-    np.savez_compressed(os.path.join(HERE, "mgrit_src.npz"),
-                        coeffs=coeffs,
-                        **mgrit_fixture(3, 4, 32, cycle=O.CYCLE_TWO_LEVEL, m=8,
-                                        source_kind=O.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2,
-                                        init_kind=O.INIT_COEFFS, init_coeffs=coeffs))
+    for name, make in fixtures().items():
+        if only and name not in only:
+            continue
+        np.savez_compressed(os.path.join(HERE, name), **make())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)), "bytes")
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+
+    main(sys.argv[1:] or None)

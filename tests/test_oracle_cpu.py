@@ -185,6 +185,7 @@ def test_restatement_matches_reference_building_blocks():
 @pytest.mark.parametrize("name,kw", [
     ("mgrit_c1.npz", dict(cycle=O.CYCLE_TWO_LEVEL, m=4)),
     ("mgrit_src.npz", dict(cycle=O.CYCLE_TWO_LEVEL, m=8)),
+    ("mgrit_cg.npz", dict(cycle=O.CYCLE_TWO_LEVEL, m=8, spatial_kind=1)),
 ])
 def test_restatement_matches_reference_mgrit(name, kw):
     g = _gold(name)
