@@ -57,8 +57,9 @@ def init_coeffs(cfg, rank=0):
 
 
 def workload_name(name, cfg):
+    spatial = "Jacobi CG" if cfg.get("spatial_kind") else "p-MG V(1,1) ILUT"
     return (f"config{name[1]}: MGRIT p={cfg['p']} h=2^-{cfg['k']} Nt={cfg['nt']} m={cfg['m']} "
-            f"{'two-level' if cfg['cycle'] == 2 else 'V-cycle'} FCF, p-MG V(1,1) ILUT, fp64")
+            f"{'two-level' if cfg['cycle'] == 2 else 'V-cycle'} FCF, {spatial}, fp64")
 
 
 def peaks():
@@ -160,7 +161,8 @@ def ref_solver(cfg, workers):
     from oracle import oracle as O
     return O.RefMgrit(cfg["p"], cfg["k"], cfg["nt"], source_kind=cfg["source_kind"],
                       source_param=cfg["source_param"], init_kind=cfg["init_kind"],
-                      init_coeffs=init_coeffs(cfg), cycle=cfg["cycle"], m=cfg["m"], workers=workers)
+                      init_coeffs=init_coeffs(cfg), cycle=cfg["cycle"], m=cfg["m"], workers=workers,
+                      spatial_kind=cfg.get("spatial_kind", 0))
 
 
 def cpu_baseline(cfg):
@@ -325,8 +327,10 @@ def run_phi(args, cfg, name):
     n, nt = n_free(cfg), cfg["nt"]
     coeffs = init_coeffs(cfg)
     disc = P.SpatialDiscretization.build(cfg["p"], cfg["k"])
+    from paper_2107_05337_b200.engine import default_solver_config
     sol = P.MgritSolver(disc, nt, source_kind=cfg["source_kind"], source_param=cfg["source_param"],
-                        init_kind=cfg["init_kind"], init_coeffs=coeffs, cycle=cfg["cycle"], m=cfg["m"])
+                        init_kind=cfg["init_kind"], init_coeffs=coeffs, cycle=cfg["cycle"], m=cfg["m"],
+                        solver=default_solver_config(kind=cfg.get("spatial_kind", 0)))
     if world > 1:  # one problem, level 0 sharded over the ranks
         from paper_2107_05337_b200 import timeshard as TS
         dev = torch.device("cuda", local)
@@ -417,14 +421,17 @@ def run_phi(args, cfg, name):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(name)  # DRAM bytes of one captured wave launch
+            key = name + ("_cg" if cfg.get("spatial_kind") else "")
+            traffic = json.load(open(tpath)).get(key)  # DRAM bytes of one captured wave launch
         except Exception:
             traffic = None
     roofline = {"kernel": "phi_wave_kernel (fused batched Phi solve)", "bound": "hbm", "achieved": achieved,
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "waves": n_waves, "kernel_ms_per_step": wave_ms,
                 "algorithmic_bytes_per_step": wave_bytes,
-                "note": "latency-bound: ILUT level sets and Gauss-Seidel wavefronts are dependent chains"}
+                "note": ("latency-bound: ILUT level sets and Gauss-Seidel wavefronts are dependent chains"
+                         if not cfg.get("spatial_kind") else
+                         "CG: one SpMV and three dot products per iteration, L2-resident operator")}
 
     launches = int(allreduce_sum(float(launches), world))  # all ranks' kernels
     line = {"metric": "MGRIT time-to-tol, DOF*timesteps/s", "value": value, "unit": "DOF*timesteps/s",
@@ -433,7 +440,7 @@ def run_phi(args, cfg, name):
             "data": "synthetic (seeded U[-1,1] spline coefficients, analytic source)",
             "config": {"workload": workload_name(name, cfg), "n_free": n, "Nt": nt,
                        "mgrit_iterations": res.iterations, "spatial_solves": res.total_spatial_solves,
-                       "mean_pmg_cycles": res.mean_spatial_iterations,
+                       "mean_spatial_iterations": res.mean_spatial_iterations,
                        "parallelism": ("single GPU" if world == 1 else
                                        f"MGRIT level 0 time-sharded over {world} GPUs (NCCL halo + coarse rhs)"),
                        "summation": "reassociated (default; within north-star tolerance)",
@@ -459,8 +466,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partial", action="store_true",
                     help="initialize + one cycle, extrapolated (large configs)")
+    ap.add_argument("--solver", default="pmg", choices=["pmg", "cg"],
+                    help="spatial solver of Phi (SpatialSolverKind, theta.hpp:64); the headline is pmg")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    cfg["spatial_kind"] = 1 if args.solver == "cg" else 0
     if args.config == "c5":
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "config 5 is a GPU kernel microbenchmark"}))

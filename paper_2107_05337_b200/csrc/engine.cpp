@@ -824,6 +824,13 @@ int Mgrit::wave_report(double* ms, double* bytes) {
         const Stepper& S = *levels[recs[k].level].stepper;
         const Hier& H = *S.hier;
         const double nnzA = (double)stencil_nnz(H.A.view());
+        const double cmax = st[3 * k], csum = st[3 * k + 1], pts = st[3 * k + 2];
+        if (H.cg_only) {  // CG kind: A once per iteration (shared by the batch), 18 n per iteration and RHS
+            const double mat = nnzA /* A- */ + (1 + cmax) * nnzA;
+            const double vec = pts * (5 * n + 3 * n) + pts * 5 * n + csum * 18 * n;
+            *bytes += 8.0 * (mat + vec);
+            continue;
+        }
         double vmat = 3 * nnzA + 2.0 * (H.L_host.nnz() + H.U_host.nnz()) + 2.0 * stencil_nnz(d.T.view());
         double vvec = 18 * n + 3 * n + (n + n1) + (n1 + 2 * n);
         const int nh = (int)d.h.size();
@@ -834,7 +841,6 @@ int Mgrit::wave_report(double* ms, double* bytes) {
             vvec += visits * (4 * 3 * nl + 3 * nl + (nl + nc) + nc + (nc + 2 * nl));
         }
         vmat += std::ldexp(1.0, nh - 1) * (double)H.coarse.n * H.coarse.n;
-        const double cmax = st[3 * k], csum = st[3 * k + 1], pts = st[3 * k + 2];
         if (std::getenv("PHI_WAVE_DEBUG"))
             std::fprintf(stderr, "wave %zu level %d: %.3f ms, points %d, cycles sum %d max %d\n", k, recs[k].level,
                          t, (int)pts, (int)csum, (int)cmax);
