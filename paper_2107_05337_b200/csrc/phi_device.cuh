@@ -1959,7 +1959,31 @@ void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs
     static int cl = -1;
     if (cl < 0) {
         cl = kPhiCluster;
-        if (const char* e = std::getenv("PHI_CLUSTER")) cl = std::atoi(e);
+        if (const char* e = std::getenv("PHI_CLUSTER")) {
+            cl = std::atoi(e);
+        } else {
+            // kPhiClusterWide CTAs (a non-portable size) when the device can
+            // co-schedule such a cluster at the largest shared-memory plan
+            PHI_CUDA(cudaFuncSetAttribute(phi_wave_kernel<DEG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            PHI_CUDA(cudaFuncSetAttribute(phi_wave_kernel<DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kPhiSmemBudgetBytes));
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3((unsigned)kPhiClusterWide);
+            q.blockDim = dim3(NT);
+            q.dynamicSmemBytes = kPhiSmemBudgetBytes;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = (unsigned)kPhiClusterWide;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, phi_wave_kernel<DEG>, &q) == cudaSuccess && ncl >= 1)
+                cl = kPhiClusterWide;
+            else
+                (void)cudaGetLastError();
+        }
     }
     int n_sm = 0, dev = 0;
     PHI_CUDA(cudaGetDevice(&dev));

@@ -16,7 +16,8 @@ constexpr int kPhiThreads = 256;
 // (one CTA per SM; 227 KB is the sm_100 per-block maximum).
 constexpr size_t kPhiSmemBudgetBytes = 212 * 1024;
 /// CTAs per cluster for waves of few right-hand sides (reassociated mode).
-constexpr int kPhiCluster = 8;
+constexpr int kPhiCluster = 8;       // CTAs per single-RHS cluster (portable size)
+constexpr int kPhiClusterWide = 16;  // ... when the device can co-schedule this many (non-portable)
 
 size_t phi_ws_doubles(const DevHier& H);
 SmemPlan phi_smem_plan(const DevHier& H);

@@ -26,7 +26,8 @@ for _ in range(5):
     st.step(u2)
 print(f"step wall {1e3 * (time.perf_counter() - t0) / 5:.3f} ms (zero guess)", flush=True)
 if len(sys.argv) > 4:
-    E.dev_tuning(8, 8, -1)
+    mask = int(sys.argv[5]) if len(sys.argv) > 5 else 0  # developer mask (c_tune.xmask)
+    E.dev_tuning(-mask if mask else 8, 8, -1)
     st.step(u2)
     buf = np.zeros(49152, np.int64)
     E.lib().phi_dev_trace(buf.ctypes.data_as(C.c_void_p), buf.size)
