@@ -99,3 +99,38 @@ def test_cg_not_converged_message():
     u = np.random.default_rng(5).standard_normal((1, d.n_free))
     with pytest.raises(Exception, match=r"spatial solve did not converge \(cg\)"):
         st.step(u, None, None)
+
+
+def test_cg_theta_half_and_zero_rhs_bitwise():
+    # theta = 0.5: the right-hand operator M - k dt/2 K is non-trivial; a zero
+    # right-hand side returns zero without iterating (solvers.hpp:28-32)
+    d = E.SpatialDiscretization.build(2, 5)
+    dt = 2e-3
+    st = E.ThetaStepper(d, 1.0, dt, 0.5, _cfg(True))
+    ost = O.OcStepper(O.OcDisc(d.operators()), 1.0, dt, 0.5, kind=1)
+    rng = np.random.default_rng(37)
+    u = rng.standard_normal((2, d.n_free))
+    u[1] = 0.0
+    guess = rng.standard_normal((2, d.n_free))
+    got = st.step(u, None, guess)
+    for i in range(2):
+        ref, _ = ost.step(u[i], None, guess[i])
+        assert np.array_equal(got[i], ref)
+    assert not np.any(got[1])
+
+
+def test_cg_sequential_integrate_bitwise():
+    d = E.SpatialDiscretization.build(2, 4)
+    nt, dt = 16, 0.1 / 16
+    st = E.ThetaStepper(d, 1.0, dt, 1.0, _cfg(True))
+    od = O.OcDisc(d.operators())
+    u0 = np.random.default_rng(41).uniform(-1, 1, d.n_free)
+    got, solves, its = st.sequential_integrate(nt, u0, None)
+    ost = O.OcStepper(od, 1.0, dt, 1.0, kind=1)
+    u = u0.copy()
+    total = 0
+    for k in range(nt):
+        u, it = ost.step(u, None, u)
+        total += it
+        assert np.array_equal(got[k + 1], u)
+    assert solves == nt and its == total
