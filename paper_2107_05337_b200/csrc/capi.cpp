@@ -371,7 +371,10 @@ int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, doub
         }
         DevBuf<double> b(len), x(len), flush;
         PHI_CUDA(cudaMemcpyAsync(b.get(), hb.data(), sizeof(double) * len, cudaMemcpyHostToDevice, h->s));
-        if (flush_l2) flush.alloc((size_t)32 << 20);  // 256 MB > L2
+        if (flush_l2) {  // 256 MB > L2, zeroed once; each repetition reads it (clean lines, no write-backs)
+            flush.alloc((size_t)32 << 20);
+            PHI_CUDA(cudaMemsetAsync(flush.get(), 0, sizeof(double) * ((size_t)32 << 20), h->s));
+        }
         SolverConfig cfg;
         const DevHier H = h->h->view(cfg);
         if (which == 1) h->ws.ensure(H);
@@ -380,7 +383,7 @@ int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, doub
         PHI_CUDA(cudaEventCreate(&e1));
         double total = 0.0;
         for (int r = -1; r < reps; ++r) {  // r = -1: warm-up
-            if (flush_l2) PHI_CUDA(cudaMemsetAsync(flush.get(), r & 0xff, sizeof(double) * ((size_t)32 << 20), h->s));
+            if (flush_l2) launch_l2_flush_read(flush.get(), (size_t)32 << 20, x.get(), h->s);
             if (which == 1) PHI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * len, h->s));  // x0 = 0
             PHI_CUDA(cudaEventRecord(e0, h->s));
             if (which == 0)

@@ -63,6 +63,8 @@ void launch_restrict_first(const double* fg, const double* fu, double* cg, doubl
                            cudaStream_t s);
 void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s);
 void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s);
+/// Reads n doubles (a multiple of 4, > L2): flushes L2 leaving clean lines.
+void launch_l2_flush_read(const double* buf, size_t n, double* sink, cudaStream_t s);
 void launch_copy(double* dst, const double* src, size_t n, cudaStream_t s);
 
 // ---- device assembly (assembly.cu) ---------------------------------------

@@ -56,6 +56,18 @@ __global__ void resid0_kernel(const double* g, const double* u, double* sq, int 
     (void)sh;
 }
 
+// Reads a buffer larger than L2 (an L2 flush that leaves only clean lines,
+// so the timed kernel does not pay for write-backs); the sum is stored only
+// under a condition that never holds for finite data.
+__global__ void l2_flush_read_kernel(const double2* __restrict__ buf, size_t n2, double* sink) {
+    double s = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
+        const double2 v = __ldg(buf + i);
+        s += v.x + v.y;
+    }
+    if (s != s) sink[0] = s;  // NaN only
+}
+
 __global__ void copy_kernel(double* dst, const double* src, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
@@ -239,6 +251,11 @@ void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream
 
 void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s) {
     resid0_kernel<<<1, 256, 0, s>>>(g, u, sq, n);
+    PHI_CUDA(cudaGetLastError());
+}
+
+void launch_l2_flush_read(const double* buf, size_t n, double* sink, cudaStream_t s) {
+    l2_flush_read_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const double2*>(buf), n / 2, sink);
     PHI_CUDA(cudaGetLastError());
 }
 

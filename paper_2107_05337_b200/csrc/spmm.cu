@@ -48,42 +48,35 @@ __global__ void tile_kernel(const DevStencil A, double* __restrict__ At) {
     }
 }
 
-// SpMV: a CTA owns one tile (lane = row); warp w sums the stencil rows
-// dv = w, w + 8, ... of it, every load of those rows issued at once; the 8
-// partial sums are reduced through shared memory.
+// SpMV: a CTA owns one tile (lane = row); warp w sums the stencil entries
+// e = w, w + 8, w + 16, ... of it (an even share of the W^2 entries per warp:
+// no warp waits for another at the reduction), every load issued at once;
+// the 8 partial sums are reduced through shared memory.
 template <int W>
 __global__ void __launch_bounds__(256) spmv_kernel(const DevStencil A, const double* __restrict__ At,
                                                    const double* __restrict__ x, double* __restrict__ y) {
+    constexpr int E = W * W, PE = (E + 7) / 8;  // entries, entries per warp (at most)
     __shared__ double part[8][32];
     const int n = A.ru * A.rv;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i = min(blockIdx.x * 32 + lane, n - 1);
     const int iv = i / A.ru, iu = i - iv * A.ru;
-    const double* at = At + (size_t)blockIdx.x * W * W * 32 + lane;
-    constexpr int ND = (W + 7) / 8;  // stencil rows per warp
-    double pr[ND][W];
+    const double* at = At + (size_t)blockIdx.x * E * 32 + lane;
+    double pr[PE];
 #pragma unroll
-    for (int j = 0; j < ND; ++j) {
-        const int dv = w + 8 * j;
-#pragma unroll
-        for (int du = 0; du < W; ++du) pr[j][du] = 0.0;
-        if (dv < W) {
-            const int r = iv + A.lo + dv;
-            const bool okr = r >= 0 && r < A.cv;
-            const double* xr = x + (size_t)min(max(r, 0), A.cv - 1) * A.cu;
-#pragma unroll
-            for (int du = 0; du < W; ++du) {
-                const int c = iu + A.lo + du;
-                const double v = __ldg(at + (size_t)(dv * W + du) * 32);
-                const double xv = __ldg(xr + min(max(c, 0), A.cu - 1));
-                pr[j][du] = (okr && c >= 0 && c < A.cu) ? v * xv : 0.0;
-            }
+    for (int k = 0; k < PE; ++k) {
+        const int e = w + 8 * k;
+        pr[k] = 0.0;
+        if (k + 1 < PE || e < E) {
+            const int dv = e / W, du = e - dv * W;
+            const int r = iv + A.lo + dv, c = iu + A.lo + du;
+            const bool ok = r >= 0 && r < A.cv && c >= 0 && c < A.cu;
+            const double v = __ldg(at + (size_t)e * 32);
+            const double xv = __ldg(x + (size_t)min(max(r, 0), A.cv - 1) * A.cu + min(max(c, 0), A.cu - 1));
+            pr[k] = ok ? v * xv : 0.0;
         }
     }
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < ND; ++j) s = s + TreeS<W>::sum(pr[j]);
-    part[w][lane] = s;
+    part[w][lane] = TreeS<PE>::sum(pr);
     __syncthreads();
     if (w == 0 && blockIdx.x * 32 + lane < n) {
         double q[8];
@@ -93,21 +86,24 @@ __global__ void __launch_bounds__(256) spmv_kernel(const DevStencil A, const dou
     }
 }
 
-// SpMM: a CTA owns one tile of 32 rows, warp w its rows 4w .. 4w+3, lane l
-// the right-hand-side pair (2l, 2l+1) (nrhs = 2 x lanes in use).  Per stencil
+// SpMM: a CTA owns 32 / (nrhs / 2) tiles of 32 rows (one per lane group of
+// nrhs / 2 lanes: 4 at nrhs = 16, 1 at 64), warp w rows 4w .. 4w+3 of each,
+// lane l of a group the right-hand-side pair (2l, 2l+1).  Per stencil
 // row the warp loads the x values its rows touch once (16-byte loads,
 // coalesced across the lanes) and reuses them for all products of its rows;
 // each operator value is one broadcast load from the contiguous tile.
-template <int W>
-__global__ void __launch_bounds__(256) spmm_kernel(const DevStencil A, const double* __restrict__ At,
-                                                   const double* __restrict__ X, double* __restrict__ Y, int nrhs) {
+template <int W, int NRHS>
+__global__ void __launch_bounds__(256, 2) spmm_kernel(const DevStencil A, const double* __restrict__ At,
+                                                   const double* __restrict__ X, double* __restrict__ Y) {
     constexpr int kRW = 4;  // rows per warp
+    constexpr int nrhs = NRHS, nl = NRHS / 2, groups = 32 / nl;  // lanes per group, groups per warp
     const int n = A.ru * A.rv;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nl = nrhs / 2, lg = min(lane, nl - 1);
-    const int i0 = blockIdx.x * 32 + w * kRW;  // first row of this warp
+    const int grp = lane / nl, lg = lane - grp * nl;
+    const int tile = blockIdx.x * groups + grp;
+    const int i0 = tile * 32 + w * kRW;  // first row of this lane's group
     if (i0 >= n) return;
-    const double* at = At + (size_t)blockIdx.x * W * W * 32 + w * kRW;
+    const double* at = At + (size_t)tile * W * W * 32 + w * kRW;
     double2 acc[kRW];
 #pragma unroll
     for (int rr = 0; rr < kRW; ++rr) acc[rr] = make_double2(0.0, 0.0);
@@ -130,15 +126,18 @@ __global__ void __launch_bounds__(256) spmm_kernel(const DevStencil A, const dou
             }
 #pragma unroll
             for (int rr = 0; rr < kRW; ++rr) {
-                double px[W], py[W];
+                // fused multiply-adds into two chains per component (reassociated
+                // mode only; entries outside the grid carry a zero coefficient)
+                double2 c0 = make_double2(0.0, 0.0), c1 = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int du = 0; du < W; ++du) {
-                    const double a = __ldg(at + (size_t)(dv * W + du) * 32 + rr);
-                    px[du] = okc[rr + du] ? a * xs[rr + du].x : 0.0;
-                    py[du] = okc[rr + du] ? a * xs[rr + du].y : 0.0;
+                    const double a = okc[rr + du] ? __ldg(at + (size_t)(dv * W + du) * 32 + rr) : 0.0;
+                    double2& c = (du & 1) ? c1 : c0;
+                    c.x = __fma_rn(a, xs[rr + du].x, c.x);
+                    c.y = __fma_rn(a, xs[rr + du].y, c.y);
                 }
-                acc[rr].x = acc[rr].x + TreeS<W>::sum(px);
-                acc[rr].y = acc[rr].y + TreeS<W>::sum(py);
+                acc[rr].x = acc[rr].x + (c0.x + c1.x);
+                acc[rr].y = acc[rr].y + (c0.y + c1.y);
             }
         }
     } else {  // rows across a line end (or past n): row by row
@@ -166,10 +165,9 @@ __global__ void __launch_bounds__(256) spmm_kernel(const DevStencil A, const dou
             }
         }
     }
-    if (lane < nl)
 #pragma unroll
-        for (int rr = 0; rr < kRW; ++rr)
-            if (i0 + rr < n) *reinterpret_cast<double2*>(Y + (size_t)(i0 + rr) * nrhs + 2 * lane) = acc[rr];
+    for (int rr = 0; rr < kRW; ++rr)
+        if (i0 + rr < n) *reinterpret_cast<double2*>(Y + (size_t)(i0 + rr) * nrhs + 2 * lg) = acc[rr];
 }
 
 template <int W>
@@ -177,8 +175,12 @@ void launch_w(const DevStencil& A, const double* At, const double* X, double* Y,
     const int n = A.ru * A.rv;
     if (nrhs == 1)
         spmv_kernel<W><<<(n + 31) / 32, 256, 0, s>>>(A, At, X, Y);
+    else if (nrhs == 16)
+        spmm_kernel<W, 16><<<((n + 31) / 32 + 3) / 4, 256, 0, s>>>(A, At, X, Y);
+    else if (nrhs == 32)
+        spmm_kernel<W, 32><<<((n + 31) / 32 + 1) / 2, 256, 0, s>>>(A, At, X, Y);
     else
-        spmm_kernel<W><<<(n + 31) / 32, 256, 0, s>>>(A, At, X, Y, nrhs);
+        spmm_kernel<W, 64><<<(n + 31) / 32, 256, 0, s>>>(A, At, X, Y);
     PHI_CUDA(cudaGetLastError());
 }
 
