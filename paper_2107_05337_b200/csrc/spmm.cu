@@ -53,7 +53,7 @@ __global__ void tile_kernel(const DevStencil A, double* __restrict__ At) {
 // no warp waits for another at the reduction), every load issued at once;
 // the 8 partial sums are reduced through shared memory.
 template <int W>
-__global__ void __launch_bounds__(256) spmv_kernel(const DevStencil A, const double* __restrict__ At,
+__global__ void __launch_bounds__(256, W <= 7 ? 8 : 6) spmv_kernel(const DevStencil A, const double* __restrict__ At,
                                                    const double* __restrict__ x, double* __restrict__ y) {
     constexpr int E = W * W, PE = (E + 7) / 8;  // entries, entries per warp (at most)
     __shared__ double part[8][32];
@@ -62,21 +62,25 @@ __global__ void __launch_bounds__(256) spmv_kernel(const DevStencil A, const dou
     const int i = min(blockIdx.x * 32 + lane, n - 1);
     const int iv = i / A.ru, iu = i - iv * A.ru;
     const double* at = At + (size_t)blockIdx.x * E * 32 + lane;
-    double pr[PE];
+    // fused multiply-adds in two chains (entries outside the grid carry a
+    // zero coefficient), so few registers hold products: more CTAs per SM
+    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int k = 0; k < PE; ++k) {
         const int e = w + 8 * k;
-        pr[k] = 0.0;
         if (k + 1 < PE || e < E) {
             const int dv = e / W, du = e - dv * W;
             const int r = iv + A.lo + dv, c = iu + A.lo + du;
             const bool ok = r >= 0 && r < A.cv && c >= 0 && c < A.cu;
             const double v = __ldg(at + (size_t)e * 32);
             const double xv = __ldg(x + (size_t)min(max(r, 0), A.cv - 1) * A.cu + min(max(c, 0), A.cu - 1));
-            pr[k] = ok ? v * xv : 0.0;
+            if (k & 1)
+                s1 = __fma_rn(ok ? v : 0.0, xv, s1);
+            else
+                s0 = __fma_rn(ok ? v : 0.0, xv, s0);
         }
     }
-    part[w][lane] = TreeS<PE>::sum(pr);
+    part[w][lane] = s0 + s1;
     __syncthreads();
     if (w == 0 && blockIdx.x * 32 + lane < n) {
         double q[8];
