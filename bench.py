@@ -226,6 +226,14 @@ def run_reference(args, cfg, name):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def c5_traffic():
+    """DRAM bytes of the captured p=5 SpMV launch (profiles/traffic.json), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("c5")
+    except Exception:
+        return None
+
+
 def run_c5(args, cfg):
     """BASELINE config 5: A x for B in {1, 16, 64} right-hand sides (SpMV / SpMM
     of A = M + 1e-4 K, p = 2..5, h = 2^-8) and one V(1,1) cycle from x0 = 0,
@@ -262,7 +270,7 @@ def run_c5(args, cfg):
             "config": {"workload": "config5: A x and one V(1,1) on A = M + 1e-4 K, p=2..5, h=2^-8, B in {1,16,64}",
                        "l2": "flushed between repetitions (256 MB read: clean lines, no write-backs in the timed kernel)"},
             "roofline": {"kernel": "spmv_kernel (p=5, B=1)", "bound": "hbm", "achieved": spmm5["GBs"], "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": spmm5["frac"], "traffic": None},
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": spmm5["frac"], "traffic": c5_traffic()},
             "table": rows}
     print(json.dumps(line), flush=True)
 
