@@ -195,6 +195,10 @@ int phi_mgrit_initialize_state(phi_mgrit* g);               /* initialize() minu
 int phi_mgrit_gnorm_terms(phi_mgrit* g, double* terms);
 /* steps_level + 1 per-point squared residuals (mgrit.hpp:200-214) */
 int phi_mgrit_residual_terms(phi_mgrit* g, int level, double* terms);
+/* per-solve p-MG cycle counts of the residual wave of `level` at the current
+ * state (the Phi solves residual_norm performs, mgrit.hpp:197-214); iters:
+ * steps_level + 1 host ints, [0] = 0.  The state is not modified. */
+int phi_mgrit_residual_iters(phi_mgrit* g, int level, int* iters);
 /* op 0 F-relaxation, 1 F+C relaxation, 2 restrict residual to level+1,
  * 3 inject the coarse correction into the C-points, 4 full cycle from level */
 int phi_mgrit_phase(phi_mgrit* g, int level, int op);

@@ -124,6 +124,11 @@ def ref_lib():
         L.ref_mgrit_initial.argtypes = [_vp, _vp]
         L.ref_load_terms.argtypes = [_vp, _vp]
         L.ref_sequential_integrate.argtypes = [_vp, _vp, _vp, _vp]
+        L.ref_mgrit_initialize.argtypes = [_vp, _vp]
+        L.ref_mgrit_cycle.argtypes = [_vp, _i]
+        L.ref_mgrit_residual_norm.argtypes = [_vp, _i, _vp]
+        L.ref_mgrit_points.argtypes = [_vp, _i, _i, _i, _i, _vp]
+        L.ref_mgrit_residual_iters.argtypes = [_vp, _i, _i, _vp]
         _ref = L
     return _ref
 
@@ -319,6 +324,36 @@ class RefMgrit:
         out = np.zeros((self.nt, self.n))
         has = ref_lib().ref_load_terms(self.h, _p(out))
         return out if has else None
+
+    # ---- one phase at a time (mgrit.hpp:76-91, 185, 197-214)
+    def initialize(self):
+        g = _d()
+        if ref_lib().ref_mgrit_initialize(self.h, C.byref(g)):
+            raise RuntimeError(_ref_err())
+        return g.value
+
+    def mgrit_cycle(self, level=0):
+        if ref_lib().ref_mgrit_cycle(self.h, level):
+            raise RuntimeError(_ref_err())
+
+    def residual_norm(self, level=0):
+        v = _d()
+        if ref_lib().ref_mgrit_residual_norm(self.h, level, C.byref(v)):
+            raise RuntimeError(_ref_err())
+        return v.value
+
+    def points(self, level, which, k0, count):
+        out = np.zeros((count, self.n))
+        ref_lib().ref_mgrit_points(self.h, level, which, k0, count, _p(out))
+        return out
+
+    def residual_iters(self, level=0, workers=None):
+        """Per-solve p-MG cycle counts of the residual wave at the current state."""
+        steps = self.levels()[0][level]
+        out = np.zeros(steps + 1, np.int32)
+        if ref_lib().ref_mgrit_residual_iters(self.h, level, workers or (os.cpu_count() or 1), _p(out)):
+            raise RuntimeError(_ref_err())
+        return out
 
     def sequential(self):
         out = np.zeros((self.nt + 1, self.n))

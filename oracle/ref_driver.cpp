@@ -18,6 +18,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "miga/mgrit.hpp"
@@ -450,6 +451,85 @@ int ref_sequential_integrate(void* p, double* out, long long* solves, long long*
             std::memcpy(out + k * n, traj[k].data(), sizeof(double) * n);
         *solves = st.solves.load();
         *iters = st.iterations.load();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// initialize() / mgrit_cycle(l) / residual_norm(l) one at a time (mgrit.hpp:76-91,
+// 185, 197-214), so a test can stop at any iteration and compare state.
+int ref_mgrit_initialize(void* p, double* g_norm) {
+    try {
+        auto& g = *static_cast<RefMgrit*>(p);
+        g.solver->initialize();
+        *g_norm = g.solver->g_norm();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_mgrit_cycle(void* p, int level) {
+    try {
+        static_cast<RefMgrit*>(p)->solver->mgrit_cycle(level);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_mgrit_residual_norm(void* p, int level, double* out) {
+    try {
+        *out = static_cast<RefMgrit*>(p)->solver->residual_norm(level);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Copy `count` point vectors k0.. of level l's u (which 0) or g (1).
+int ref_mgrit_points(void* p, int level, int which, int k0, int count, double* out) {
+    auto& g = *static_cast<RefMgrit*>(p);
+    const auto& lev = g.solver->level(level);
+    const int n = g.d->dofmap_p.n_free;
+    const auto& arr = which == 0 ? lev.u : lev.g;
+    for (int k = 0; k < count; ++k) std::memcpy(out + (size_t)k * n, arr.at(k0 + k).data(), sizeof(double) * n);
+    return 0;
+}
+
+// Per-solve p-multigrid iteration counts of the residual wave of level l at
+// the solver's current state: for every point k = 1..steps the Phi solve that
+// residual_norm(l) performs (mgrit.hpp:197-214 -> step_value 261-269:
+// stepper->step(u[k-1], load(k), guess u[k])), each with its own SolveStats
+// (theta.hpp:77-85), on `workers` threads.  iters: steps + 1 entries, [0] = 0.
+// The state is not modified.
+int ref_mgrit_residual_iters(void* p, int level, int workers, int* iters) {
+    try {
+        auto& g = *static_cast<RefMgrit*>(p);
+        const auto& lev = g.solver->level(level);
+        const int steps = lev.steps;
+        iters[0] = 0;
+        std::vector<std::string> errs(workers > 0 ? workers : 1);
+        auto run = [&](int w, int nw) {
+            try {
+                for (int k = 1 + w; k <= steps; k += nw) {
+                    SolveStats st;
+                    static const Vector kEmpty;
+                    const Vector& load = level == 0 ? lev.loads.term(k) : kEmpty;
+                    (void)lev.stepper->step(lev.u[k - 1], load, lev.u[k], &st);
+                    iters[k] = static_cast<int>(st.iterations.load());
+                }
+            } catch (const std::exception& e) {
+                errs[w] = e.what();
+            }
+        };
+        const int nw = workers > 0 ? workers : 1;
+        std::vector<std::thread> th;
+        for (int w = 0; w < nw; ++w) th.emplace_back(run, w, nw);
+        for (auto& t : th) t.join();
+        for (const auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -17,7 +17,8 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_lib")
+# developer trace builds go to their own directory (PHI_TRACE=1 -> _lib_trace)
+OUT_DIR = os.path.join(HERE, "_lib_trace" if os.environ.get("PHI_TRACE") == "1" else "_lib")
 LIB = os.path.join(OUT_DIR, "libphi_engine.so")
 ROOT = os.path.dirname(HERE)
 

@@ -642,6 +642,13 @@ int phi_mgrit_residual_terms(phi_mgrit* g, int level, double* terms) {
     return guarded([&] { g->g->residual_terms(level, terms); });
 }
 
+int phi_mgrit_residual_iters(phi_mgrit* g, int level, int* iters) {
+    return guarded([&] {
+        if (level < 0 || level >= g->g->n_levels()) throw InvalidArgument("MGRIT level out of range");
+        g->g->residual_iters(level, iters);
+    });
+}
+
 int phi_mgrit_phase(phi_mgrit* g, int level, int op) {
     return guarded([&] { g->g->phase(level, op); });
 }
@@ -659,7 +666,13 @@ int phi_mgrit_set_init_coeffs(phi_mgrit* g, const double* coeffs) {
 }
 
 int phi_mgrit_profile(phi_mgrit* g, int enable) {
-    return guarded([&] { g->g->profile = enable != 0; });
+    return guarded([&] {
+        g->g->profile = enable != 0;
+        if (g->g->profile && g->g->wstats.size() == 0) {
+            g->g->wstats.alloc(3 * 8192);
+            g->g->wstats.zero(g->g->stream);
+        }
+    });
 }
 
 int phi_mgrit_wave_report(phi_mgrit* g, double* ms, double* bytes) {

@@ -34,6 +34,7 @@ constexpr int kTriSlots = 8;
 /// hand-off ring.
 constexpr int kBlkMaxSlots = 8;
 constexpr int kBlkHand = 4;
+constexpr int kBlkMinSlots = 3;  // workers wait for unit g once block g - 3 is done
 /// Warps that take turns on the blocks of a fast (reassociated) sweep.
 constexpr int kSweepWarps = 6;
 /// Bytes per triangular-factor block (TriPlan chunking) and the product
@@ -54,6 +55,8 @@ struct DevTri {
 /// block of 32 rows in solve order; `table` holds (offset / 16, bytes).
 struct DevBlk {
     int n, n_blocks, parts, mf0, lookahead, max_unit_bytes;
+    int win;   // rolling-window layout (BlkStream::win), 0: absolute columns
+    int desc;  // rows in descending order (upper factor, backward sweep)
     const unsigned char* stream;  // 16-byte aligned
     const int4* table;  // per block: offset / 16, bytes, fresh slots, 0
 };
@@ -124,6 +127,7 @@ struct SmemPlan {
     int z_off;             // in-place triangular-solve vector (n_p + 1)
     int lvl_off[kMaxH];    // per h-level: b, x, r (3 n_l)
     int cl_scr_off;        // cluster dense-apply scratch (kClScratch doubles) free during the W-cycle, -1: none
+    int win_off;           // rolling window of the ILUT substitutions (win + 2 doubles), -1: none
     int total;             // doubles
 };
 

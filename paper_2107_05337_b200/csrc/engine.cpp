@@ -192,6 +192,29 @@ void upload_blk(const BlkStream& b, Hier::BlkDev& d, cudaStream_t s) {
     d.mf0 = b.mf0;
     d.lookahead = b.lookahead;
     d.max_unit_bytes = b.max_unit_bytes;
+    d.win = b.win;
+    d.desc = b.desc;
+}
+
+// Block-recurrence streams of the two ILUT substitutions.  When the vector z
+// does not fit in shared memory next to a ring of kBlkMinSlots units, the
+// streams use the rolling-window layout (setup_host.hpp), which keeps only a
+// band-wide window of z on chip.
+void build_ilut_streams(const HostCsr& L, const HostCsr& U, int n, BlkStream& lb, BlkStream& ub) {
+    lb = blk_lower(L);
+    ub = blk_upper(U);
+    auto slot = [](const BlkStream& a, const BlkStream& b) {
+        return (size_t)(std::max(a.max_unit_bytes, b.max_unit_bytes) + 127) / 128 * 128;
+    };
+    const size_t zb = ((size_t)n + 2) * 8;
+    if (zb < kPhiSmemBudgetBytes && (kPhiSmemBudgetBytes - zb) / slot(lb, ub) >= (size_t)kBlkMinSlots) return;
+    const int wz = blk_window_for(ilut_span(L, U));
+    if (!wz) return;
+    BlkStream lw = blk_lower(L, wz), uw = blk_upper(U, wz);
+    const size_t wb = ((size_t)wz + 2) * 8;
+    if ((kPhiSmemBudgetBytes - wb) / slot(lw, uw) < (size_t)kBlkMinSlots) return;
+    lb = std::move(lw);
+    ub = std::move(uw);
 }
 }  // namespace
 
@@ -203,6 +226,8 @@ DevBlk Hier::BlkDev::view() const {
     b.mf0 = mf0;
     b.lookahead = lookahead;
     b.max_unit_bytes = max_unit_bytes;
+    b.win = win;
+    b.desc = desc;
     b.stream = stream.get();
     b.table = reinterpret_cast<const int4*>(table.get());
     return b;
@@ -227,8 +252,10 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
         upload_tri(Lp, false, Ld, s);
         upload_tri(Up, false, Ud, s);
     } else {
-        upload_blk(blk_lower(L_host), Lbd, s);
-        upload_blk(blk_upper(U_host), Ubd, s);
+        BlkStream lb, ub;
+        build_ilut_streams(L_host, U_host, d.n_p, lb, ub);
+        upload_blk(lb, Lbd, s);
+        upload_blk(ub, Ubd, s);
     }
     for (const auto& hl : d.h) {
         StencilBuf a;
@@ -546,6 +573,7 @@ void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, 
     a.err_rel = err_rel.get();
     a.level = l;
     a.x0_empty = mode == kModeSolve ? 1 : 0;  // g-norm solves start from zero (mgrit.hpp:301)
+    a.iters_out = iters_dev;
     const bool rec = profile && recs.size() * 3 < wstats.size();
     if (rec) {
         WaveRec r{};
@@ -662,6 +690,24 @@ void Mgrit::residual_terms(int l, double* host) {
     PHI_CUDA(cudaMemcpyAsync(host, sq.get(), sizeof(double) * (lv.steps + 1), cudaMemcpyDeviceToHost, stream));
     PHI_CUDA(cudaStreamSynchronize(stream));
     check_errors();
+}
+
+void Mgrit::residual_iters(int l, int* host) {
+    Level& lv = levels[l];
+    const int lo = range_lo(l);
+    DevBuf<int> it((size_t)lv.steps + 1);
+    it.zero(stream);
+    iters_dev = it.get() + lo * cfg.m + 1;  // task 0 of the residual wave is point lo m + 1
+    std::vector<double> scratch(lv.steps + 1);
+    try {
+        residual_terms(l, scratch.data());
+    } catch (...) {
+        iters_dev = nullptr;
+        throw;
+    }
+    iters_dev = nullptr;
+    const std::vector<int> h = it.download(stream);
+    std::copy(h.begin(), h.end(), host);
 }
 
 double Mgrit::compute_g_norm() {

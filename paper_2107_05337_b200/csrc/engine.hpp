@@ -115,7 +115,7 @@ public:
     struct BlkDev {
         DevBuf<unsigned char> stream;
         DevBuf<int> table;
-        int n = 0, n_blocks = 0, parts = 1, mf0 = 0, lookahead = 0, max_unit_bytes = 0;
+        int n = 0, n_blocks = 0, parts = 1, mf0 = 0, lookahead = 0, max_unit_bytes = 0, win = 0, desc = 0;
         DevBlk view() const;
     } Lbd, Ubd;
     std::vector<BlkDev> gsb_dev;  // per h-level (but the coarsest): forward, backward
@@ -207,6 +207,8 @@ public:
     void initialize_state();                     // initialize() without the g-norm
     void gnorm_terms(double* host);              // steps_0 + 1 terms: [0] = |g_0|^2
     void residual_terms(int l, double* host);    // steps_l + 1 terms
+    /// per-solve p-MG cycle counts of the residual wave (steps_l + 1 entries, [0] = 0)
+    void residual_iters(int l, int* host);
     void phase(int l, int op);                   // see phi_mgrit_phase
     void points(int l, int which, int k0, int count, double* ptr, bool device, bool set);
     void stats(long long* out4) const;           // level-0 solves, iters; coarser solves, iters
@@ -236,6 +238,7 @@ public:
     DevBuf<double> u0;
     double g_norm = 0.0;
     long long launches = 0;  // kernels launched by the solve (bench evidence)
+    int* iters_dev = nullptr;  // per-task iteration counts of the next waves (nullable)
 
     // Optional per-launch profile of the Phi waves (CUDA events on the engine
     // stream + device counters of p-MG cycles), for the bench's roofline.

@@ -85,6 +85,11 @@ __device__ __forceinline__ int vlds_s32(unsigned a) {
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ int vlds_u16(unsigned a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return (int)v;
+}
 __device__ __forceinline__ int lds_s32(unsigned a) {
     int v;
     asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -202,6 +207,7 @@ struct Ws {
     int z_off, ring_off, slot_bytes, prod_off;  // g_smem offsets (-1: global)
     int n_slots, gs_slot_bytes, gs_n_slots;     // block-sweep rings (SmemPlan)
     int cl_scr_off;                             // cluster dense-apply scratch (SmemPlan), -1: none
+    int win_off;                                // rolling window of the ILUT substitutions (SmemPlan), -1: none
     int lvl_off[kMaxH];  // g_smem offset of level l's vectors (b, x, r), -1: global
     double* hb[kMaxH];
     double* hx[kMaxH];
@@ -227,6 +233,7 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
     w.gs_slot_bytes = P.gs_slot_bytes;
     w.gs_n_slots = P.gs_n_slots;
     w.cl_scr_off = P.cl_scr_off;
+    w.win_off = P.win_off;
     double* g = base + 6 * np;
     for (int l = 0; l < H.n_h; ++l) {
         const int nl = H.h[l].n;
@@ -763,9 +770,13 @@ __device__ __forceinline__ void hand_wait(int id) { asm volatile("bar.sync %0, 6
 __device__ __forceinline__ void hand_signal(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 constexpr int kHandBar = 1;  // ids 1 .. kBlkSolvers
 
-template <bool XSM, bool RSM>
+// WIN (rolling-window streams, BlkStream::win): x_off is the window, the
+// stream's columns are window slots (16-bit for the old entries), solved
+// values go to the window slot row & (win - 1) and through to global xg.
+template <bool XSM, bool RSM, bool WIN>
 __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg, int x_off, const double* rg,
                                          int r_off, int ring_off, int slot_bytes, int n_slots) {
+    static_assert(!WIN || (XSM && !RSM), "the window is the shared x; the right-hand side is global");
     BlkSync& sy = g_blk;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nb = T.n_blocks, P = T.parts, total = count * nb;
@@ -781,16 +792,34 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
         // ---- solver warps 0 .. NS-1 take blocks g = w, w + NS, ...  The parts'
         // count implies the block's unit has landed (each worker waited).
         const unsigned tb = sh_addr(sy.tb[w]);
-        const int xn = T.n;  // the zero slot x[n]
+        const int xn = WIN ? T.win : T.n;  // the zero slot x[n] (window: slot win)
         int slot = w % n_slots, k = w % nb;
         int4 info = w < total ? __ldg(table + k) : make_int4(0, 0, 0, 0);  // (off16, bytes, mf, 0)
         int4 refill_next = make_int4(0, 0, 0, 0);
         if (lane == 0 && w + n_slots < total) refill_next = __ldg(table + (k + n_slots) % nb);
+        // rows are taken in solve order: lane l of block k solves position 32 k + l
+        auto row_of = [&](int kb) {
+            const int pos = kb * kBlkRows + lane;
+            return pos < T.n ? (T.desc ? T.n - 1 - pos : pos) : -1;
+        };
+        // a global right-hand side is prefetched one turn ahead (its rows are
+        // not written before their own block), off the chain
+        double rhs_next = 0.0;
+        if constexpr (!RSM) {
+            const int r0 = row_of(k);
+            if (w < total && r0 >= 0) rhs_next = *reinterpret_cast<const volatile double*>(rg + r0);
+        }
         for (int g = w; g < total; g += NS) {
             const int mf = info.z;
             int kn2 = k + NS;  // this solver's next block
             while (kn2 >= nb) kn2 -= nb;
             if (g + NS < total) info = __ldg(table + kn2);
+            double rhs_pref = 0.0;
+            if constexpr (!RSM) {
+                rhs_pref = rhs_next;
+                const int rn = row_of(kn2);
+                if (g + NS < total && rn >= 0) rhs_next = *reinterpret_cast<const volatile double*>(rg + rn);
+            }
             // the unit that refills this block's slot after the block: its
             // table entry was loaded one turn earlier (no L2 latency here)
             const int4 refill = refill_next;
@@ -809,9 +838,9 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             // data dependence on the wait: none of these loads moves above it
             const unsigned u = ring + slot * slot_bytes + (unsigned)(seen > 0 ? 0 : 1);
             // ---- independent of block g-1: row, rhs, inverse, mid slots
-            const int row = vlds_s32(u + 16u + 4u * lane);
-            double rhs = 0.0;
-            if (row >= 0) rhs = RSM ? vlds_f64(rs + 8u * row) : *reinterpret_cast<const volatile double*>(rg + row);
+            const int row = RSM ? vlds_s32(u + 16u + 4u * lane) : row_of(k);
+            double rhs = rhs_pref;
+            if (RSM && row >= 0) rhs = vlds_f64(rs + 8u * row);
             double iv[32];
 #pragma unroll
             for (int p2 = 0; p2 < 16; ++p2) lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
@@ -871,7 +900,14 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 }
             }
             const double z = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-            if (row >= 0) xst<XSM>(xg, xs, row, z);
+            if constexpr (WIN) {
+                if (row >= 0) {
+                    xst<true>(xg, xs, row & (T.win - 1), z);
+                    xg[row] = z;  // write-through: read by the next phases after the sweep
+                }
+            } else if (row >= 0) {
+                xst<XSM>(xg, xs, row, z);
+            }
             if constexpr (!XSM) __threadfence_block();  // global x: order the stores before the hand-off
             __syncwarp();
             if (lane == 0) st_volatile_s32(prog, g);  // monotone: block g+1 starts after the hand-off
@@ -909,15 +945,20 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             if (tr) tr[8] = clock64();
             const unsigned u = ring + slot * slot_bytes;
             const int mo = vlds_s32(u), mf = vlds_s32(u + 12u);
-            const unsigned oc = u + kBlkFreshOff + 512u * mf + 384u * mo * q + 4u * lane;
-            const unsigned ov = oc + 128u * mo + 4u * lane;
+            // part q: columns int32[mo][32] (window: uint16), then values double[mo][32]
+            constexpr unsigned CB = WIN ? 2u : 4u;
+            const unsigned pb = u + kBlkFreshOff + 512u * mf + (32u * CB + 256u) * mo * q;
+            const unsigned oc = pb + CB * lane;
+            const unsigned ov = pb + 32u * CB * mo + 8u * lane;
+            const int xpad = WIN ? T.win : T.n;
+            auto ldc = [&](int e) { return WIN ? vlds_u16(oc + 32u * CB * e) : vlds_s32(oc + 32u * CB * e); };
             double a0 = 0.0, a1 = 0.0;
             if (mo <= 8) {  // the common case: every load issued before the wait
                 int c[8];
                 double v[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    c[e] = e < mo ? vlds_s32(oc + 128u * e) : T.n;
+                    c[e] = e < mo ? ldc(e) : xpad;
                     v[e] = e < mo ? vlds_f64(ov + 256u * e) : 0.0;
                 }
                 if (tr) tr[9] = clock64();
@@ -933,7 +974,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 wait_ge(prog, need);
                 if (tr) tr[10] = clock64();
                 for (int e = 0; e < mo; e += 2) {
-                    const int c0 = vlds_s32(oc + 128u * e), c1 = e + 1 < mo ? vlds_s32(oc + 128u * (e + 1)) : T.n;
+                    const int c0 = ldc(e), c1 = e + 1 < mo ? ldc(e + 1) : xpad;
                     const double v0 = vlds_f64(ov + 256u * e), v1 = e + 1 < mo ? vlds_f64(ov + 256u * (e + 1)) : 0.0;
                     a0 = __fma_rn(v0, xld<XSM>(xg, xs, c0), a0);
                     a1 = __fma_rn(v1, xld<XSM>(xg, xs, c1), a1);
@@ -960,7 +1001,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
 // `count` sweeps over T: prime, the solver / worker split, closing barrier,
 // phase bookkeeping.  Called by the whole CTA (blk_init ran at kernel start).
 __device__ __forceinline__ void blk_sweep(const DevBlk& T, int count, double* xg, int x_off, const double* rg,
-                                          int r_off, int ring_off, int slot_bytes, int n_slots) {
+                                          int r_off, int ring_off, int slot_bytes, int n_slots, int win_off = -1) {
     BlkSync& sy = g_blk;
     const int nb = T.n_blocks, total = count * nb;
     if (total == 0) return;
@@ -968,9 +1009,11 @@ __device__ __forceinline__ void blk_sweep(const DevBlk& T, int count, double* xg
     // phases: order those writes before the TMA (async-proxy) writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    const bool win = T.win > 0 && win_off >= 0;
     if (threadIdx.x == 0) {
         const unsigned bar = sh_addr(sy.bar);
         sy.prog = -1;
+        if (win) g_smem[win_off + T.win] = 0.0;  // the window's zero slot (padding)
         const unsigned ring = sh_addr(g_smem + ring_off);
         for (int g = 0; g < n_slots && g < total; ++g) {
             const int4 e = __ldg(T.table + g % nb);
@@ -978,12 +1021,14 @@ __device__ __forceinline__ void blk_sweep(const DevBlk& T, int count, double* xg
         }
     }
     __syncthreads();
-    if (x_off >= 0 && r_off >= 0)
-        blk_sweep_t<true, true>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
+    if (win)
+        blk_sweep_t<true, false, true>(T, count, xg, win_off, rg, -1, ring_off, slot_bytes, n_slots);
+    else if (x_off >= 0 && r_off >= 0)
+        blk_sweep_t<true, true, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
     else if (x_off >= 0)
-        blk_sweep_t<true, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
+        blk_sweep_t<true, false, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
     else
-        blk_sweep_t<false, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
+        blk_sweep_t<false, false, false>(T, count, xg, x_off, rg, r_off, ring_off, slot_bytes, n_slots);
     __syncthreads();
     if (threadIdx.x == 0)  // units delivered per slot
         for (int g = 0; g < n_slots; ++g) sy.phase[g] += g < total ? (total - 1 - g) / n_slots + 1 : 0;
@@ -1031,8 +1076,8 @@ __device__ __forceinline__ void ilut_solve(const DevTri& L, const DevTri& U, dou
 // Reassociated mode: both substitutions as block recurrences, then x += z.
 __device__ __forceinline__ void ilut_solve_blk(const DevBlk& L, const DevBlk& U, double* zg, int z_off, double* xadd,
                                                const Ws& w) {
-    blk_sweep(L, 1, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
-    blk_sweep(U, 1, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots);
+    blk_sweep(L, 1, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots, w.win_off);
+    blk_sweep(U, 1, zg, z_off, zg, z_off, w.ring_off, w.slot_bytes, w.n_slots, w.win_off);
     if (xadd) {
         const double* z = z_off >= 0 ? g_smem + z_off : zg;
         for (int i = threadIdx.x; i < L.n; i += NT) xadd[i] = xadd[i] + z[i];

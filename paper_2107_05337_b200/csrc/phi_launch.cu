@@ -98,6 +98,7 @@ SmemPlan phi_smem_plan(const DevHier& H) {
     const size_t budget = kPhiSmemBudgetBytes / 8;  // doubles
     P.ring_off = 0;
     P.dot_off = 0;
+    P.win_off = -1;
     for (int l = 0; l < kMaxH; ++l) P.lvl_off[l] = -1;
     if (H.kind == 1) {  // CG kind: the ordered-dot scratch only (vectors in global memory)
         P.prod_off = P.z_off = P.cl_scr_off = -1;
@@ -124,10 +125,12 @@ SmemPlan phi_smem_plan(const DevHier& H) {
             gslot = std::max(gslot, std::max(H.h[l].gsb_fwd.max_unit_bytes, H.h[l].gsb_bwd.max_unit_bytes));
         P.slot_bytes = (slot + 127) / 128 * 128;
         P.gs_slot_bytes = (gslot + 127) / 128 * 128;
-        const int min_slots = 3;  // workers wait for unit g once block g - 3 is done
-        // the ILUT ring leaves room for z when it can
-        const size_t zb = ((size_t)H.n_p + 2) * 8;
+        const int min_slots = kBlkMinSlots;
+        // the ILUT ring leaves room for z (or, rolling-window streams, for the window) when it can
+        const int win = std::max(H.Lb.win, H.Ub.win);
+        const size_t zb = win ? ((size_t)win + 2) * 8 : ((size_t)H.n_p + 2) * 8;
         int ns = (int)std::min<size_t>(kBlkMaxSlots, (kPhiSmemBudgetBytes - std::min(zb, kPhiSmemBudgetBytes)) / P.slot_bytes);
+        if (win && ns < min_slots) throw InvalidArgument("rolling-window ILUT streams exceed shared memory");
         if (ns < min_slots) ns = (int)std::min<size_t>(kBlkMaxSlots, kPhiSmemBudgetBytes / P.slot_bytes);
         if (ns < min_slots) throw InvalidArgument("triangular-factor blocks exceed shared memory");
         P.n_slots = ns;
@@ -136,7 +139,11 @@ SmemPlan phi_smem_plan(const DevHier& H) {
         gs_tri = (size_t)P.gs_n_slots * P.gs_slot_bytes / 8;
     }
     size_t top = std::max(tri, gs_tri);
-    if (tri + (size_t)H.n_p + 2 <= budget) {
+    if (!H.exact && std::max(H.Lb.win, H.Ub.win) > 0) {  // z global, its window after the ring
+        P.z_off = -1;
+        P.win_off = (int)tri;
+        top = std::max(top, tri + std::max(H.Lb.win, H.Ub.win) + 2);
+    } else if (tri + (size_t)H.n_p + 2 <= budget) {
         P.z_off = (int)tri;
         top = std::max(top, tri + H.n_p + 2);
     } else {
@@ -162,8 +169,8 @@ SmemPlan phi_smem_plan(const DevHier& H) {
         P.cl_scr_off = -1;
     P.total = (int)std::max(top, (size_t)kDotChunk);
     if (std::getenv("PHI_PLAN_DEBUG"))
-        std::fprintf(stderr, "smem plan: slot %d B x %d, gs slot %d B x %d, prod @%d, z @%d, levels @%d.., total %d doubles\n",
-                     P.slot_bytes, P.n_slots, P.gs_slot_bytes, P.gs_n_slots, P.prod_off, P.z_off, P.lvl_off[0], P.total);
+        std::fprintf(stderr, "smem plan: slot %d B x %d, gs slot %d B x %d, prod @%d, z @%d, window @%d, levels @%d.., total %d doubles\n",
+                     P.slot_bytes, P.n_slots, P.gs_slot_bytes, P.gs_n_slots, P.prod_off, P.z_off, P.win_off, P.lvl_off[0], P.total);
     return P;
 }
 

@@ -702,10 +702,15 @@ struct BlkRowsView {
     std::function<double(int)> diag;
 };
 
-BlkStream make_blk_stream(const BlkRowsView& rv) {
+BlkStream make_blk_stream(const BlkRowsView& rv, int win) {
     const int n = rv.n;
     BlkStream bs;
     bs.n = n;
+    bs.win = win;
+    bs.desc = rv.descending ? 1 : 0;
+    // column as stored: absolute, or its window slot (padding: n, or the zero slot)
+    auto stored = [&](int c) { return win ? (c & (win - 1)) : c; };
+    const int pad = win ? win : n;
     bs.n_blocks = (n + kBlkRows - 1) / kBlkRows;
     auto pos_of = [&](int i) { return rv.descending ? n - 1 - i : i; };
     auto row_at = [&](int pos) { return rv.descending ? n - 1 - pos : pos; };
@@ -770,7 +775,8 @@ BlkStream make_blk_stream(const BlkRowsView& rv) {
                 for (int m = j; m < l; ++m) acc -= b.B[l][m] * inv[m][j];
                 inv[l][j] = acc / b.B[l][l];
             }
-        const size_t bytes = kBlkFreshOff + 512 * mf + static_cast<size_t>(P) * 384 * mo;
+        const size_t part_bytes = (win ? 320 : 384) * mo;
+        const size_t bytes = kBlkFreshOff + 512 * mf + static_cast<size_t>(P) * part_bytes;
         std::vector<unsigned char> img(bytes, 0);
         const int hdr[4] = {static_cast<int>(mo), 0, static_cast<int>(bytes), static_cast<int>(mf)};
         std::memcpy(img.data(), hdr, sizeof hdr);
@@ -784,22 +790,31 @@ BlkStream make_blk_stream(const BlkRowsView& rv) {
         unsigned char* fr = img.data() + kBlkFreshOff;
         for (size_t q = 0; q < mf; ++q)
             for (int l = 0; l < kBlkRows; ++l) {
-                int col = n;
+                int col = pad;
                 double v = 0.0;
                 if (q < b.frsh[l].size()) {
-                    col = b.frsh[l][q].first;
+                    col = stored(b.frsh[l][q].first);
                     v = b.frsh[l][q].second;
                 }
                 std::memcpy(fr + (q * kBlkRows + l) * 16, &col, 4);
                 std::memcpy(fr + (q * kBlkRows + l) * 16 + 8, &v, 8);
             }
         for (int p = 0; p < P; ++p) {
-            int* oc = reinterpret_cast<int*>(img.data() + kBlkFreshOff + 512 * mf + static_cast<size_t>(p) * 384 * mo);
-            double* ov = reinterpret_cast<double*>(oc + kBlkRows * mo);
-            for (size_t s2 = 0; s2 < kBlkRows * mo; ++s2) oc[s2] = n;  // neutral padding (x[n] = +0.0)
+            unsigned char* pb = img.data() + kBlkFreshOff + 512 * mf + static_cast<size_t>(p) * part_bytes;
+            const size_t cb = (win ? 2 : 4) * kBlkRows * mo;  // column bytes of the part
+            double* ov = reinterpret_cast<double*>(pb + cb);
+            auto put_col = [&](size_t slot, int c) {
+                if (win) {
+                    const unsigned short c16 = static_cast<unsigned short>(c);
+                    std::memcpy(pb + 2 * slot, &c16, 2);
+                } else {
+                    std::memcpy(pb + 4 * slot, &c, 4);
+                }
+            };
+            for (size_t s2 = 0; s2 < kBlkRows * mo; ++s2) put_col(s2, pad);  // neutral padding (zero slot)
             for (int l = 0; l < kBlkRows; ++l)
                 for (size_t e = p, q = 0; e < b.olde[l].size(); e += P, ++q) {
-                    oc[q * kBlkRows + l] = b.olde[l][e].first;
+                    put_col(q * kBlkRows + l, stored(b.olde[l][e].first));
                     ov[q * kBlkRows + l] = b.olde[l][e].second;
                 }
         }
@@ -822,7 +837,22 @@ BlkStream make_blk_stream(const BlkRowsView& rv) {
 
 }  // namespace
 
-BlkStream blk_lower(const HostCsr& m) {
+int ilut_span(const HostCsr& lower, const HostCsr& upper) {
+    int span = 0;
+    for (const HostCsr* f : {&lower, &upper})
+        for (int i = 0; i < f->n_rows; ++i)
+            for (int e = f->row_offsets[i]; e < f->row_offsets[i + 1]; ++e)
+                span = std::max(span, std::abs(i - f->col_indices[e]));
+    return span;
+}
+
+int blk_window_for(int span) {
+    int w = 64;
+    while (w < span + 64) w *= 2;
+    return w <= kBlkMaxWin ? w : 0;
+}
+
+BlkStream blk_lower(const HostCsr& m, int win) {
     BlkRowsView rv;
     rv.n = m.n_rows;
     rv.entries = [&m](int i, std::vector<int>& c, std::vector<double>& v) {
@@ -830,10 +860,10 @@ BlkStream blk_lower(const HostCsr& m) {
         v.assign(m.values.begin() + m.row_offsets[i], m.values.begin() + m.row_offsets[i + 1]);
     };
     rv.diag = [](int) { return 1.0; };
-    return make_blk_stream(rv);
+    return make_blk_stream(rv, win);
 }
 
-BlkStream blk_upper(const HostCsr& m) {
+BlkStream blk_upper(const HostCsr& m, int win) {
     BlkRowsView rv;
     rv.n = m.n_rows;
     rv.descending = true;
@@ -842,7 +872,7 @@ BlkStream blk_upper(const HostCsr& m) {
         v.assign(m.values.begin() + m.row_offsets[i] + 1, m.values.begin() + m.row_offsets[i + 1]);
     };
     rv.diag = [&m](int i) { return m.values[m.row_offsets[i]]; };
-    return make_blk_stream(rv);
+    return make_blk_stream(rv, win);
 }
 
 BlkStream blk_gauss_seidel(const HostCsr& a, bool backward) {
@@ -863,7 +893,7 @@ BlkStream blk_gauss_seidel(const HostCsr& a, bool backward) {
             if (a.col_indices[e] == i) return a.values[e];
         throw std::runtime_error("gauss_seidel_sweep: zero diagonal entry");
     };
-    return make_blk_stream(rv);
+    return make_blk_stream(rv, 0);
 }
 
 }  // namespace phi

@@ -163,11 +163,28 @@ struct BlkStream {
     std::vector<unsigned char> stream;
     std::vector<int> table;  // 4 per block: offset / 16, bytes, fresh slots, 0
     int n = 0, n_blocks = 0, parts = 1, mf0 = 0, lookahead = 0, max_unit_bytes = 0;
+    int win = 0;   // rolling-window layout (below), 0: absolute columns
+    int desc = 0;  // solve order descending: block k, lane l solves row n - 1 - (32 k + l)
 };
+/// Rolling-window layout (win = WZ, a power of two; ILUT substitutions whose
+/// vector does not fit in shared memory).  The factors are banded: every
+/// column a row reads was solved at most `span` rows earlier in solve order
+/// (ilut_span).  With WZ > span + 32 the device keeps only the last WZ solved
+/// values in a shared-memory ring (slot j & (WZ - 1)) and writes the solution
+/// through to global memory.  Columns in the stream are then window slots
+/// (col & (WZ - 1); padding: the zero slot WZ) and the old entries are packed
+/// with 16-bit columns: per part q, cols uint16[mo][32], vals double[mo][32]
+/// at kBlkFreshOff + 512 mf + q * 320 mo.
+constexpr int kBlkMaxWin = 4096;
+/// Largest distance in solve order between a row and a column it reads, over
+/// both factors (the band of the IgA ILUT factors).
+int ilut_span(const HostCsr& lower, const HostCsr& upper);
+/// Window size for a span: the power of two >= span + 64 (0 if above kBlkMaxWin).
+int blk_window_for(int span);
 /// Unit lower ILUT factor (strictly lower entries stored), ascending.
-BlkStream blk_lower(const HostCsr& lower);
+BlkStream blk_lower(const HostCsr& lower, int win = 0);
 /// Upper ILUT factor (diagonal first in each row), descending.
-BlkStream blk_upper(const HostCsr& upper);
+BlkStream blk_upper(const HostCsr& upper, int win = 0);
 /// Lexicographic Gauss-Seidel sweep on A (solvers.hpp:80-99).
 BlkStream blk_gauss_seidel(const HostCsr& a, bool backward);
 

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libphi_engine.so")
+LIB_PATH = os.path.join(HERE, "_lib_trace" if os.environ.get("PHI_TRACE") == "1" else "_lib", "libphi_engine.so")
 
 PHI_OK, PHI_ERR_INVALID, PHI_ERR_NOT_CONVERGED, PHI_ERR_CUDA, PHI_ERR_RUNTIME = range(5)
 SOURCE_CONSTANT, SOURCE_SIN_EXP, SOURCE_SIN = 0, 1, 2
@@ -37,7 +37,7 @@ EXPORTED = [
     "phi_mgrit_launches", "phi_mgrit_set_init_coeffs", "phi_mgrit_profile", "phi_mgrit_wave_report",
     "phi_dev_tuning", "phi_dev_trace", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
     "phi_mgrit_gnorm_terms", "phi_mgrit_residual_terms", "phi_mgrit_phase", "phi_mgrit_points",
-    "phi_mgrit_stats",
+    "phi_mgrit_stats", "phi_mgrit_residual_iters",
 ]
 
 
@@ -137,6 +137,7 @@ def lib():
         L.phi_mgrit_initialize_state.argtypes = [_vp]
         L.phi_mgrit_gnorm_terms.argtypes = [_vp, _vp]
         L.phi_mgrit_residual_terms.argtypes = [_vp, _i, _vp]
+        L.phi_mgrit_residual_iters.argtypes = [_vp, _i, _vp]
         L.phi_mgrit_phase.argtypes = [_vp, _i, _i]
         L.phi_mgrit_points.argtypes = [_vp, _i, _i, _i, _i, _vp, _i, _i]
         L.phi_mgrit_stats.argtypes = [_vp, _vp]
@@ -470,6 +471,12 @@ class MgritSolver:
     def residual_terms(self, level: int = 0) -> np.ndarray:
         out = np.zeros(self.levels()[0][level] + 1)
         _check(lib().phi_mgrit_residual_terms(self.h, level, _p(out)))
+        return out
+
+    def residual_iters(self, level: int = 0) -> np.ndarray:
+        """Per-solve p-MG cycle counts of the residual wave at the current state."""
+        out = np.zeros(self.levels()[0][level] + 1, np.int32)
+        _check(lib().phi_mgrit_residual_iters(self.h, level, _p(out)))
         return out
 
     def phase(self, level: int, op: int) -> None:
