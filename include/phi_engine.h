@@ -218,6 +218,12 @@ int phi_mgrit_set_init_coeffs(phi_mgrit* g, const double* coeffs);
  * the summed kernel time (ms) and algorithmic bytes (DESIGN.md byte model) */
 int phi_mgrit_profile(phi_mgrit* g, int enable);
 int phi_mgrit_wave_report(phi_mgrit* g, double* ms, double* bytes);
+/* per MGRIT level (cap entries) of the last profiled solve: summed wave time
+ * (ms), Phi solves, p-MG cycles, and the dependent steps of one single-RHS
+ * V-cycle of that level's hierarchy (the latency model); call before
+ * phi_mgrit_wave_report, which releases the records */
+int phi_mgrit_wave_levels(phi_mgrit* g, double* ms, long long* points, long long* cycles, long long* chain_steps,
+                          int cap);
 
 /* Developer knob (not part of the reference API): warps used by the sync-free
  * triangular solves / Gauss-Seidel sweeps and the readiness-poll back-off. */

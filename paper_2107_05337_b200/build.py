@@ -32,7 +32,7 @@ if os.environ.get("PHI_TRACE") == "1":  # developer timing stamps (tools/probe_*
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-unused-function",
              f"-I{CUDA_INC}"]
 
-CU = ["phi_launch.cu", "assembly.cu", "spmm.cu"]
+CU = ["phi_launch.cu", "assembly.cu", "spmm.cu", "ilut.cu"]
 DEGREES = range(1, 9)  # phi_deg.cu is compiled once per spline degree (-DPHI_DEG=d)
 CPP = ["setup_host.cpp", "engine.cpp", "capi.cpp"]
 HEADERS = ["common.hpp", "device_types.cuh", "phi_kernels.cuh", "phi_device.cuh", "setup_host.hpp", "engine.hpp"]

@@ -675,6 +675,15 @@ int phi_mgrit_profile(phi_mgrit* g, int enable) {
     });
 }
 
+int phi_mgrit_wave_levels(phi_mgrit* g, double* ms, long long* points, long long* cycles, long long* chain_steps,
+                          int cap) {
+    return guarded([&] {
+        g->g->wave_levels(ms, points, cycles, cap);
+        for (int l = 0; l < cap; ++l)
+            chain_steps[l] = l < g->g->n_levels() ? g->g->levels[l].stepper->hier->chain_steps() : 0;
+    });
+}
+
 int phi_mgrit_wave_report(phi_mgrit* g, double* ms, double* bytes) {
     int n = 0;
     const int rc = guarded([&] { n = g->g->wave_report(ms, bytes); });

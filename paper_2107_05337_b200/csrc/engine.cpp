@@ -242,8 +242,7 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
     A.vals.alloc(A.size());
     launch_axpby(d.M.vals.get(), c, d.K.vals.get(), A.vals.get(), A.size(), s);
     if (cg_only) return;
-    const HostCsr ah = stencil_to_csr(A);
-    ilut_factor(ah, opt.ilut_tau, opt.ilut_fill, L_host, U_host);
+    device_ilut(A.view(), opt.ilut_tau, opt.ilut_fill, L_host, U_host, s);
     // exact mode: level-scheduled streams (the reference's summation order);
     // reassociated mode: block recurrences
     if (opt.exact) {
@@ -315,6 +314,22 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
 }
 
 HostCsr Hier::a_h_csr(int l) const { return stencil_to_csr(a_h.at(l)); }
+
+long long Hier::chain_steps() const {
+    if (cg_only || opt.exact) return 0;
+    const Disc& d = *disc;
+    long long s = (long long)(opt.nu_pre + opt.nu_post) * (Lbd.n_blocks + Ubd.n_blocks);
+    const int nh = (int)d.h.size();
+    const int dl = dense_level_cl >= 0 ? dense_level_cl : (dense_level >= 0 ? dense_level : nh - 1);
+    for (int l = 0; l < dl && l + 1 < nh; ++l) {
+        const long long visits = 1LL << l;
+        const bool line = d.h[l].nf <= kLineMax && d.h[l].nf >= kLineMin;
+        const long long per_sweep = line ? d.h[l].nf : gsb_dev[2 * l].n_blocks;
+        s += visits * (opt.gs_pre + opt.gs_post) * per_sweep;
+    }
+    s += 1LL << dl;  // dense (or LU) applications of the coarse subtree
+    return s;
+}
 
 DevHier Hier::view(const SolverConfig& cfg) const {
     const Disc& d = *disc;
@@ -851,6 +866,25 @@ long long stencil_nnz(const DevStencil& A) {
     return s;
 }
 }  // namespace
+
+void Mgrit::wave_levels(double* ms, long long* points, long long* cycles, int cap) {
+    for (int l = 0; l < cap; ++l) {
+        ms[l] = 0.0;
+        points[l] = cycles[l] = 0;
+    }
+    if (recs.empty()) return;
+    std::vector<int> st(3 * recs.size());
+    PHI_CUDA(cudaMemcpy(st.data(), wstats.get(), sizeof(int) * st.size(), cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < recs.size(); ++k) {
+        const int l = recs[k].level;
+        if (l >= cap) continue;
+        float t = 0.f;
+        PHI_CUDA(cudaEventElapsedTime(&t, recs[k].start, recs[k].stop));
+        ms[l] += t;
+        cycles[l] += st[3 * k + 1];
+        points[l] += st[3 * k + 2];
+    }
+}
 
 // Algorithmic bytes: 8 B per stored nonzero of the reference
 // operators read once per wave-phase (the batch shares them) plus 8 B per

@@ -138,6 +138,11 @@ public:
 
     DevHier view(const SolverConfig& cfg) const;
     HostCsr a_h_csr(int l) const;
+    /// Dependent steps on the critical path of one single-right-hand-side
+    /// V-cycle (reassociated mode, cluster W-cycle): ILUT blocks of the
+    /// smoothings, Gauss-Seidel lines / blocks of the W-cycle sweeps, one
+    /// step per dense coarse application -- the latency model of bench.py.
+    long long chain_steps() const;
 };
 
 /// Message of a failed spatial solve (theta.hpp:116-118, 123-124; a negative
@@ -252,6 +257,10 @@ public:
     /// Sum of wave kernel times (ms) and of their algorithmic bytes (DESIGN.md
     /// section 5 byte model) over the last solve(); returns the wave count.
     int wave_report(double* ms, double* bytes);
+    /// Per MGRIT level of the last profiled solve: summed wave time (ms),
+    /// Phi solves and p-MG cycles.  Must be called before wave_report (which
+    /// releases the records).
+    void wave_levels(double* ms, long long* points, long long* cycles, int cap);
     void set_init_coeffs(const double* host);
 
 private:

@@ -67,6 +67,12 @@ void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStre
 void launch_l2_flush_read(const double* buf, size_t n, double* sink, cudaStream_t s);
 void launch_copy(double* dst, const double* src, size_t n, cudaStream_t s);
 
+// ---- device ILUT (ilut.cu) ------------------------------------------------
+/// Dual-threshold ILUT of a square stencil operator on the device, bit-identical
+/// to ilut_factor (ilut.hpp:29-143); factors returned as host CSR (L strictly
+/// lower, U with its diagonal first).  Throws on a zero pivot.
+void device_ilut(const DevStencil& A, double tau, int fill_limit, HostCsr& lower, HostCsr& upper, cudaStream_t s);
+
 // ---- device assembly (assembly.cu) ---------------------------------------
 /// 1D tables on the device for one direction (see Tables1D).
 struct DevTables1D {

@@ -213,111 +213,6 @@ HostCsr transpose(const HostCsr& a) {
     return t;
 }
 
-void ilut_factor(const HostCsr& a, double tau, int fill_limit, HostCsr& lower, HostCsr& upper) {
-    const int n = a.n_rows;
-    if (a.n_rows != a.n_cols) throw InvalidArgument("ilut_factor: matrix not square");
-    if (fill_limit <= 0) fill_limit = (a.nnz() + n - 1) / std::max(n, 1);
-    lower = HostCsr{};
-    upper = HostCsr{};
-    lower.n_rows = lower.n_cols = upper.n_rows = upper.n_cols = n;
-    lower.col_indices.reserve(a.nnz());
-    lower.values.reserve(a.nnz());
-    upper.col_indices.reserve(a.nnz() + n);
-    upper.values.reserve(a.nnz() + n);
-
-    std::vector<double> w(n, 0.0);
-    std::vector<char> active(n, 0);
-    std::vector<int> touched;
-    std::priority_queue<int, std::vector<int>, std::greater<int>> pending;
-    struct Ent {
-        int col;
-        double val;
-    };
-    std::vector<Ent> lpart, upart;
-    // strict total order: larger magnitude first, then smaller column
-    auto larger = [](const Ent& x, const Ent& y) {
-        const double ax = std::abs(x.val), ay = std::abs(y.val);
-        if (ax != ay) return ax > ay;
-        return x.col < y.col;
-    };
-    auto keep = [&](std::vector<Ent>& part) {
-        if (static_cast<int>(part.size()) > fill_limit) {
-            std::partial_sort(part.begin(), part.begin() + fill_limit, part.end(), larger);
-            part.resize(fill_limit);
-        }
-        std::sort(part.begin(), part.end(), [](const Ent& x, const Ent& y) { return x.col < y.col; });
-    };
-
-    for (int i = 0; i < n; ++i) {
-        double row_norm_sq = 0.0;
-        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) {
-            const int j = a.col_indices[e];
-            const double v = a.values[e];
-            row_norm_sq += v * v;
-            w[j] = v;
-            if (!active[j]) {
-                active[j] = 1;
-                touched.push_back(j);
-                if (j < i) pending.push(j);
-            }
-        }
-        const double drop = tau * std::sqrt(row_norm_sq);
-        while (!pending.empty()) {
-            const int k = pending.top();
-            pending.pop();
-            const int urow = upper.row_offsets[k];
-            const double beta = w[k] / upper.values[urow];
-            if (std::abs(beta) < drop) {
-                w[k] = 0.0;
-                continue;
-            }
-            w[k] = beta;
-            for (int e = urow + 1; e < upper.row_offsets[k + 1]; ++e) {
-                const int j = upper.col_indices[e];
-                if (!active[j]) {
-                    active[j] = 1;
-                    touched.push_back(j);
-                    w[j] = 0.0;
-                    if (j < i) pending.push(j);
-                }
-                w[j] -= beta * upper.values[e];
-            }
-        }
-        lpart.clear();
-        upart.clear();
-        double diag = 0.0;
-        bool diag_present = false;
-        for (int j : touched) {
-            const double v = w[j];
-            w[j] = 0.0;
-            active[j] = 0;
-            if (j == i) {
-                diag = v;
-                diag_present = true;
-            } else if (v != 0.0 && std::abs(v) >= drop) {
-                (j < i ? lpart : upart).push_back({j, v});
-            }
-        }
-        touched.clear();
-        if (!diag_present || diag == 0.0)
-            throw std::runtime_error("ilut_factor: zero pivot in row " + std::to_string(i));
-        keep(lpart);
-        keep(upart);
-        for (const auto& e : lpart) {
-            lower.col_indices.push_back(e.col);
-            lower.values.push_back(e.val);
-        }
-        lower.row_offsets.push_back(lower.nnz());
-        upper.col_indices.push_back(i);
-        upper.values.push_back(diag);
-        for (const auto& e : upart) {
-            upper.col_indices.push_back(e.col);
-            upper.values.push_back(e.val);
-        }
-        upper.row_offsets.push_back(upper.nnz());
-    }
-}
-
 DenseLUHost dense_lu_factor(const HostCsr& a) {
     if (a.n_rows != a.n_cols) throw InvalidArgument("DenseLU: matrix not square");
     DenseLUHost f;

@@ -50,9 +50,6 @@ LowTables build_low_tables(const Knots& low, const Tables1D& high);
 HostCsr p1_embedding_free(int n_elements_fine);
 HostCsr transpose(const HostCsr& a);
 
-/// Dual-threshold ILUT (restates ilut.hpp:29-143).  Throws on a zero pivot.
-void ilut_factor(const HostCsr& a, double tau, int fill_limit, HostCsr& lower, HostCsr& upper);
-
 /// Dense LU with partial pivoting (restates solvers.hpp:102-172).
 struct DenseLUHost {
     int n = 0;

@@ -37,7 +37,7 @@ EXPORTED = [
     "phi_mgrit_launches", "phi_mgrit_set_init_coeffs", "phi_mgrit_profile", "phi_mgrit_wave_report",
     "phi_dev_tuning", "phi_dev_trace", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
     "phi_mgrit_gnorm_terms", "phi_mgrit_residual_terms", "phi_mgrit_phase", "phi_mgrit_points",
-    "phi_mgrit_stats", "phi_mgrit_residual_iters",
+    "phi_mgrit_stats", "phi_mgrit_residual_iters", "phi_mgrit_wave_levels",
 ]
 
 
@@ -138,6 +138,7 @@ def lib():
         L.phi_mgrit_gnorm_terms.argtypes = [_vp, _vp]
         L.phi_mgrit_residual_terms.argtypes = [_vp, _i, _vp]
         L.phi_mgrit_residual_iters.argtypes = [_vp, _i, _vp]
+        L.phi_mgrit_wave_levels.argtypes = [_vp, _vp, _vp, _vp, _vp, _i]
         L.phi_mgrit_phase.argtypes = [_vp, _i, _i]
         L.phi_mgrit_points.argtypes = [_vp, _i, _i, _i, _i, _vp, _i, _i]
         L.phi_mgrit_stats.argtypes = [_vp, _vp]
@@ -496,6 +497,16 @@ class MgritSolver:
 
     def set_profile(self, enable: bool) -> None:
         _check(lib().phi_mgrit_profile(self.h, int(enable)))
+
+    def wave_levels(self, cap: int = 8):
+        """Per level of the last profiled solve(): (ms, Phi solves, p-MG cycles,
+        dependent steps of one single-RHS V-cycle).  Call before wave_report()."""
+        ms = np.zeros(cap)
+        pts, cyc, steps = (np.zeros(cap, np.int64) for _ in range(3))
+        _check(lib().phi_mgrit_wave_levels(self.h, _p(ms), _p(pts), _p(cyc), _p(steps), cap))
+        L = len(self.levels()[0])
+        return [dict(level=l, ms=float(ms[l]), solves=int(pts[l]), cycles=int(cyc[l]), chain_steps=int(steps[l]))
+                for l in range(L)]
 
     def wave_report(self):
         """(waves, kernel ms, algorithmic bytes) of the last profiled solve()."""
