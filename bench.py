@@ -5,19 +5,29 @@ One "step" = one full ``MgritSolver::solve()`` (mgrit.hpp:93-118): IC
 projection, g-norm solves and MGRIT iterations to the 1e-10 halting
 tolerance -- the reference's own timing window (bench.hpp:146-149).  The
 metric is DOF*timesteps/s = n_free * Nt / time-to-tol, whole job over all
-ranks.  Default workload: BASELINE config 2 (p=3, h=2^-6, Nt=1000, two-level
-m=8, transient 2 pi^2 e^-t sin sin source, seeded U[-1,1] spline initial
-coefficients), fp64.
+ranks.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl phi|reference]
+Default workload: BASELINE config 3 (p=4, h=2^-7, Nt=2500, m=4 -- the
+reference builds two levels, 2500/625 -- seeded U[-1,1] spline initial
+coefficients, f=0), fp64.  Config 4 is the largest config that fits one GPU,
+but it is not the default: one C4 solve takes minutes on the B200 and the
+reference's own C4 setup alone takes ~25 min on the host (10,001 load
+assemblies), so neither arm's 25-step run fits the driver's window; a
+single-solve C4 line is committed under profiles/ instead
+(`bench.py --config c4 --steps 1 --warmup 0`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl phi|reference]
 
 For N > 1 (torchrun, one rank per GPU) the ONE space-time problem is solved
-by the time-sharded MGRIT driver (paper_2107_05337_b200/timeshard.py): each
+time-sharded inside the engine (csrc/timeshard.cpp, phi_mgrit_set_comm): each
 rank owns a block of the level-0 coarse intervals, halos and the coarse
-right-hand side travel over NCCL, the coarse cycle is replicated -- strong
+right-hand sides travel over NCCL, the coarse cycle is replicated -- strong
 scaling, identical results for any N.  The reference arm (--impl reference)
 runs the unmodified reference (oracle/_ref, compiled from /root/reference)
-with all host threads on rank 0; other ranks exit without work.
+with all host threads on rank 0; other ranks exit without work.  Configs too
+long for the host (C3, C4) are timed on a bounded sample per step:
+initialize() + one MGRIT cycle + its residual, extrapolated to the
+reference's iteration count (8 at C3).
 """
 from __future__ import annotations
 
@@ -40,9 +50,24 @@ CONFIGS = {
     "c2": dict(p=3, k=6, nt=1000, m=8, cycle=2, source_kind=1, source_param=2 * np.pi ** 2, init_kind=2),
     "c3": dict(p=4, k=7, nt=2500, m=4, cycle=0, source_kind=0, source_param=0.0, init_kind=2),
     "c4": dict(p=5, k=8, nt=10000, m=8, cycle=0, source_kind=1, source_param=2 * np.pi ** 2, init_kind=0),
+    # the divisible multilevel variants of C3 / C4 (hard part 2): the
+    # reference's build_levels (mgrit.hpp:217-244) gives 3 levels 2560/640/160 with
+    # coarse_floor 41, and 4 levels 10240/1280/160/20 with the default floor
+    "c3ml": dict(p=4, k=7, nt=2560, m=4, cycle=0, source_kind=0, source_param=0.0, init_kind=2, coarse_floor=41),
+    "c4ml": dict(p=5, k=8, nt=10240, m=8, cycle=0, source_kind=1, source_param=2 * np.pi ** 2, init_kind=0),
     # BASELINE.json configs[4]: kernel microbenchmark (SpMV/SpMM and one V(1,1)), p = 2..5, h = 2^-8
     "c5": dict(p=5, k=8, c=1e-4),
 }
+DEFAULT_CONFIG = "c3"
+# the reference's MGRIT iteration count where its full solve is too long for
+# the host (SURVEY.md section 6 probes; the engine converges in the same count)
+REF_ITERS = {"c3": 8, "c4": 8, "c3ml": 8, "c4ml": 8}
+# configs whose reference setup alone is too long for a bench run on the host
+HOST_TOO_LONG = {k: ("not run: the reference's setup at h=2^-8, p=5 builds a 10,001-point transient load "
+                     "schedule on the host (~25 min, SURVEY.md section 6) and one solve takes ~1.5-2.6 h on "
+                     "8 cores; parity at this operator shape is pinned by tests/test_gpu_baseline_parity.py")
+                 for k in ("c4", "c4ml")}
+FULL_REF_WORK = 5_000_000  # n_free * Nt up to which the reference runs full solves
 SEED = 12345
 
 
@@ -58,8 +83,33 @@ def init_coeffs(cfg, rank=0):
 
 def workload_name(name, cfg):
     spatial = "Jacobi CG" if cfg.get("spatial_kind") else "p-MG V(1,1) ILUT"
-    return (f"config{name[1]}: MGRIT p={cfg['p']} h=2^-{cfg['k']} Nt={cfg['nt']} m={cfg['m']} "
+    tag = f"config{name[1]}" + (" multilevel variant" if name.endswith("ml") else "")
+    return (f"{tag}: MGRIT p={cfg['p']} h=2^-{cfg['k']} Nt={cfg['nt']} m={cfg['m']} "
             f"{'two-level' if cfg['cycle'] == 2 else 'V-cycle'} FCF, {spatial}, fp64")
+
+
+def level_steps(cfg):
+    """The reference's time-grid hierarchy (build_levels, mgrit.hpp:217-244)."""
+    m, steps = cfg["m"], [cfg["nt"]]
+    while steps[-1] % m == 0 and steps[-1] >= m:
+        nxt = steps[-1] // m
+        if len(steps) > 1 and nxt + 1 <= cfg.get("coarse_floor", 8):
+            break
+        steps.append(nxt)
+        if cfg["cycle"] == 2:
+            break
+    return steps
+
+
+def shared_config(name, cfg):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": workload_name(name, cfg), "n_free": n_free(cfg), "Nt": cfg["nt"], "m": cfg["m"],
+            "levels": level_steps(cfg),
+            "l2": "flushed between timed steps (256 MB read); operators and state are re-read from HBM"}
+
+
+def full_reference(cfg):
+    return cfg["nt"] * n_free(cfg) <= FULL_REF_WORK
 
 
 def peaks():
@@ -162,29 +212,70 @@ def ref_solver(cfg, workers):
     return O.RefMgrit(cfg["p"], cfg["k"], cfg["nt"], source_kind=cfg["source_kind"],
                       source_param=cfg["source_param"], init_kind=cfg["init_kind"],
                       init_coeffs=init_coeffs(cfg), cycle=cfg["cycle"], m=cfg["m"], workers=workers,
-                      spatial_kind=cfg.get("spatial_kind", 0))
+                      coarse_floor=cfg.get("coarse_floor", 8), spatial_kind=cfg.get("spatial_kind", 0))
 
 
-def cpu_baseline(cfg):
-    """Reference MGRIT solve() on the box's host cores, bounded sample."""
+def ref_step(rm, cfg, name):
+    """One reference step: a full solve() where the host finishes it in
+    seconds, else initialize() + 1 cycle + residual extrapolated to the
+    reference's iteration count.  Returns (seconds, sample text, details)."""
+    if full_reference(cfg):
+        r = rm.solve()
+        return r["wall"], f"full MGRIT solve() ({r['iterations']} iterations)", r
+    t_init, t_cyc, hist = rm.partial(1)
+    iters = REF_ITERS.get(name, 8)
+    return (t_init + iters * t_cyc,
+            f"initialize() {t_init:.2f} s + 1 MGRIT cycle with its residual {t_cyc:.2f} s, "
+            f"extrapolated to the reference's {iters} iterations", {"hist": hist})
+
+
+def cpu_baseline_and_parity(cfg, name, sol, res_eng):
+    """The reference on the box's host cores (cpu_baseline) and, on the same
+    run, the parity of the benchmarked engine mode against it.  Full-solve
+    configs compare the whole solve; the others compare the state after one
+    MGRIT iteration from initialize(), with per-solve p-MG counts of the
+    residual wave."""
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     if not O.ref_available():
-        return {"value": None, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
-                "sample": "unavailable: oracle/_ref not built"}
+        return ({"value": None, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+                 "sample": "unavailable: oracle/_ref not built"}, None)
     n, nt = n_free(cfg), cfg["nt"]
+    if name in HOST_TOO_LONG:
+        return ({"value": None, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+                 "sample": HOST_TOO_LONG[name]}, None)
     rm = ref_solver(cfg, cores)
-    if nt * n <= 5_000_000:
-        r = rm.solve()
-        wall = r["wall"]
-        sample = f"full MGRIT solve() ({r['iterations']} iterations), workers={cores}"
-    else:  # too long for the CPU: init + one cycle, extrapolated by the iteration count
-        t_init, t_cyc, _ = rm.partial(1)
-        iters = 8
-        wall = t_init + iters * t_cyc
-        sample = f"initialize() + 1 MGRIT cycle, extrapolated to {iters} iterations, workers={cores}"
-    return {"value": n * nt / wall, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
-            "sample": sample, "seconds": wall}
+    wall, sample, det = ref_step(rm, cfg, name)
+    base = {"value": n * nt / wall, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+            "sample": sample + f", workers={cores}", "seconds": wall}
+
+    def rel(a, b):
+        return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+    if full_reference(cfg):
+        par = {"compared": "full solve() on identical inputs",
+               "mgrit_iterations": [res_eng.iterations, det["iterations"]],
+               "spatial_solves": [res_eng.total_spatial_solves, det["total_spatial_solves"]],
+               "mean_spatial_iterations": [res_eng.mean_spatial_iterations, det["mean_spatial_iterations"]],
+               "final_relative_residual": [res_eng.final_relative_residual, det["final_relative_residual"]],
+               "rel_l2_vs_ref": rel(sol.trajectory(), rm.trajectory())}
+    else:
+        g = sol.initialize()
+        sol.mgrit_cycle(0)
+        it_e = sol.residual_iters(0)
+        r_e = sol.residual_norm(0) / (g if g > 0 else 1.0)
+        it_r = rm.residual_iters(0, cores)
+        d = np.abs(it_e.astype(np.int64) - it_r.astype(np.int64))
+        ue = sol.trajectory()
+        ur = np.concatenate([rm.points(0, 0, k0, min(500, nt + 1 - k0)) for k0 in range(0, nt + 1, 500)])
+        par = {"compared": "state after initialize() + 1 MGRIT iteration, identical inputs",
+               "relative_residual_after_1": [r_e, float(det["hist"][0])],
+               "rel_l2_vs_ref": rel(ue, ur),
+               "per_solve_pmg_cycles": {"solves": int(nt), "max_abs_diff": int(d.max()),
+                                        "differing": int((d > 0).sum())},
+               "mgrit_iterations_full_solve": [res_eng.iterations, REF_ITERS.get(name)]}
+    par["bar"] = "iteration counts +-1, space-time rel L2 <= 1e-8 (north star)"
+    return base, par
 
 
 def run_reference(args, cfg, name):
@@ -193,34 +284,32 @@ def run_reference(args, cfg, name):
         return
     cores = os.cpu_count() or 1
     from oracle import oracle as O
-    base = {"metric": "MGRIT time-to-tol, DOF*timesteps/s", "unit": "DOF*timesteps/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
-            "impl": "reference", "dtype": "f64", "data": "synthetic (seeded)",
-            "config": {"workload": workload_name(name, cfg), "parallelism": f"{cores} CPU threads"},
-            "vs_baseline": None}
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmiga_ref.so not built"}))
         return
     n, nt = n_free(cfg), cfg["nt"]
+    if name in HOST_TOO_LONG:
+        print(json.dumps({"impl": "reference", "unavailable": HOST_TOO_LONG[name]}))
+        return
     rm = ref_solver(cfg, cores)
     for _ in range(args.warmup):
-        rm.partial(1)  # warm caches / thread pool; bounded
-    times = []
-    full = nt * n <= 5_000_000
+        rm.initialize()  # warm the thread pool and caches; bounded
+    times, sample = [], ""
     for _ in range(args.steps):
-        if full:
-            times.append(rm.solve()["wall"])
-        else:
-            ti, tc, _ = rm.partial(1)
-            times.append(ti + 8 * tc)
+        t, sample, _ = ref_step(rm, cfg, name)
+        times.append(t)
     t = float(np.mean(times))
     v = n * nt / t
-    base.update({"value": v, "ms_per_step": t * 1e3,
-                 "cpu_baseline": {"value": v, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
-                                  "sample": "full MGRIT solve()" if full else
-                                  "initialize() + 1 cycle, extrapolated to 8 iterations"},
-                 "e2e": {"value": v, "unit": "DOF*timesteps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
-    print(json.dumps(base), flush=True)
+    line = {"metric": "MGRIT time-to-tol, DOF*timesteps/s", "value": v, "unit": "DOF*timesteps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong", "impl": "reference", "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] spline coefficients, analytic source)",
+            "config": shared_config(name, cfg), "vs_baseline": None,
+            "run": {"parallelism": f"{cores} CPU threads (MgritConfig::workers)", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "DOF*timesteps/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "DOF*timesteps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -338,16 +427,13 @@ def run_phi(args, cfg, name):
     from paper_2107_05337_b200.engine import default_solver_config
     sol = P.MgritSolver(disc, nt, source_kind=cfg["source_kind"], source_param=cfg["source_param"],
                         init_kind=cfg["init_kind"], init_coeffs=coeffs, cycle=cfg["cycle"], m=cfg["m"],
+                        coarse_floor=cfg.get("coarse_floor", 8),
                         solver=default_solver_config(kind=cfg.get("spatial_kind", 0)))
-    if world > 1:  # one problem, level 0 sharded over the ranks
+    if world > 1:  # one problem, level 0 sharded over the ranks inside the engine (C++ + NCCL)
         from paper_2107_05337_b200 import timeshard as TS
-        dev = torch.device("cuda", local)
-        drv = TS.TimeShardedMgrit(TS.EngineExecutor(sol, dev), TS.TorchComm(dev), cycle=sol.cycle,
-                                  relax=sol.relax, halt_tol=sol.halt_tol, max_iter=sol.max_iter)
-        solve_fn = drv.solve
-    else:
-        drv = None
-        solve_fn = sol.solve
+        comm = TS.nccl_comm_from_torch()
+        sol.set_comm(comm)
+    solve_fn = sol.solve
 
     def timed(fn):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -375,10 +461,9 @@ def run_phi(args, cfg, name):
     for _ in range(args.steps):
         flush_buf.sum()
         torch.cuda.synchronize()
-        l0 = sol.launches()
         t, res = timed(solve_fn)
         times.append(t)
-        launches += sol.launches() - (0 if drv is None else l0)  # solve() resets the counter
+        launches += sol.launches()  # solve() resets the counter
     clk = clocks.stop()
     barrier(world)
     t_step = allreduce_max(float(np.mean(times)), world)
@@ -388,7 +473,6 @@ def run_phi(args, cfg, name):
     e2e_steps = max(1, min(args.steps, 2))
     pinned_in = torch.empty(n, dtype=torch.float64).pin_memory() if coeffs is not None else None
     pinned_out = torch.empty((nt + 1) * n, dtype=torch.float64).pin_memory()
-    out_np = pinned_out.numpy().reshape(nt + 1, n)
     from paper_2107_05337_b200.engine import _check, _p
     import ctypes as C
 
@@ -397,12 +481,8 @@ def run_phi(args, cfg, name):
             pinned_in.numpy()[:] = coeffs
             sol._coeffs = pinned_in.numpy()
             _check(lib().phi_mgrit_set_init_coeffs(sol.h, C.c_void_p(pinned_in.data_ptr())))
-        if drv is None:
-            r = sol.solve()
-            _check(lib().phi_mgrit_trajectory(sol.h, C.c_void_p(pinned_out.data_ptr())))
-        else:
-            r = drv.solve()
-            out_np[:] = drv.trajectory()
+        r = sol.solve()
+        _check(lib().phi_mgrit_trajectory(sol.h, C.c_void_p(pinned_out.data_ptr())))  # gathers when sharded
         return r
 
     barrier(world)
@@ -418,10 +498,8 @@ def run_phi(args, cfg, name):
 
     # ---- roofline of the dominant kernel (phi_wave_kernel), profiled solve
     sol.set_profile(True)
-    if drv is None:
-        sol.solve()
-    else:
-        drv.solve()
+    sol.solve()
+    per_level = sol.wave_levels()
     n_waves, wave_ms, wave_bytes = sol.wave_report()
     sol.set_profile(False)
     peak, peak_kind = peaks()
@@ -434,11 +512,30 @@ def run_phi(args, cfg, name):
             traffic = json.load(open(tpath)).get(key)  # DRAM bytes of one captured wave launch
         except Exception:
             traffic = None
+    # Latency model of the same kernel: the solve is a chain of dependent
+    # steps (ILUT blocks, Gauss-Seidel lines), so its bound is cycles per
+    # dependent step, not bandwidth.  The coarsest level runs one right-hand
+    # side at a time (the serial march, mgrit.hpp:188-194): its time per
+    # p-MG cycle over the steps of one V-cycle's chain.
+    coarse = per_level[-1]
+    f_mhz = clk.get("sm_mhz") or 1965.0
+    latency = None
+    if coarse["cycles"] > 0 and coarse["chain_steps"] > 0:
+        ms_cycle = coarse["ms"] / coarse["cycles"]
+        latency = {"level": coarse["level"], "serial_phi_solves": coarse["solves"],
+                   "pmg_cycles": coarse["cycles"], "ms_per_pmg_cycle": ms_cycle,
+                   "dependent_steps_per_vcycle": coarse["chain_steps"],
+                   "cycles_per_dependent_step": ms_cycle * 1e-3 * f_mhz * 1e6 / coarse["chain_steps"],
+                   "share_of_kernel_time": coarse["ms"] / wave_ms if wave_ms > 0 else None,
+                   "note": "per-cycle time includes the residual checks and the right-hand-side product"}
     roofline = {"kernel": "phi_wave_kernel (fused batched Phi solve)", "bound": "hbm", "achieved": achieved,
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "waves": n_waves, "kernel_ms_per_step": wave_ms,
                 "algorithmic_bytes_per_step": wave_bytes,
-                "note": ("latency-bound: ILUT level sets and Gauss-Seidel wavefronts are dependent chains"
+                "per_level": per_level, "latency": latency,
+                "note": ("latency-bound, not bandwidth-bound: the serial coarse march runs ILUT block "
+                         "recurrences and Gauss-Seidel line scans as dependent chains; 'latency' gives "
+                         "the cycles per dependent step that explain the time"
                          if not cfg.get("spatial_kind") else
                          "CG: one SpMV and three dot products per iteration, L2-resident operator")}
 
@@ -447,17 +544,16 @@ def run_phi(args, cfg, name):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded U[-1,1] spline coefficients, analytic source)",
-            "config": {"workload": workload_name(name, cfg), "n_free": n, "Nt": nt,
-                       "mgrit_iterations": res.iterations, "spatial_solves": res.total_spatial_solves,
-                       "mean_spatial_iterations": res.mean_spatial_iterations,
-                       "parallelism": ("single GPU" if world == 1 else
-                                       f"MGRIT level 0 time-sharded over {world} GPUs (NCCL halo + coarse rhs)"),
-                       "summation": "reassociated (default; within north-star tolerance)",
-                       "l2": "flushed between timed steps (256 MB read); the operators (a few MB) are re-read "
-                             "from HBM by the first solve phase and stay L2-resident within one solve()"},
+            "config": shared_config(name, cfg),
+            "run": {"mgrit_iterations": res.iterations, "spatial_solves": res.total_spatial_solves,
+                    "mean_spatial_iterations": res.mean_spatial_iterations,
+                    "parallelism": ("single GPU" if world == 1 else
+                                    f"MGRIT level 0 time-sharded over {world} GPUs in the engine (NCCL halo "
+                                    f"shifts + allgathered coarse rhs; coarse cycle replicated)"),
+                    "summation": "reassociated (default; within north-star tolerance)"},
             "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg)
+        line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(cfg, name, sol, res)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -470,7 +566,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", 1)))
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="phi", choices=["phi", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partial", action="store_true",

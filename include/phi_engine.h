@@ -200,7 +200,10 @@ int phi_mgrit_residual_terms(phi_mgrit* g, int level, double* terms);
  * steps_level + 1 host ints, [0] = 0.  The state is not modified. */
 int phi_mgrit_residual_iters(phi_mgrit* g, int level, int* iters);
 /* op 0 F-relaxation, 1 F+C relaxation, 2 restrict residual to level+1,
- * 3 inject the coarse correction into the C-points, 4 full cycle from level */
+ * 3 inject the coarse correction into the C-points, 4 full cycle from level
+ * (cycle_impl(level, cycle == F)), 5 the same without the F-schedule
+ * (cycle_impl(level, false), the coarse call of the F-schedule's second pass,
+ * mgrit.hpp:278-288) */
 int phi_mgrit_phase(phi_mgrit* g, int level, int op);
 /* copy `count` consecutive point vectors k0.. of level's u (which 0) or g (1)
  * to (set 0) or from (set 1) ptr, a host or device pointer */
@@ -224,6 +227,35 @@ int phi_mgrit_wave_report(phi_mgrit* g, double* ms, double* bytes);
  * phi_mgrit_wave_report, which releases the records */
 int phi_mgrit_wave_levels(phi_mgrit* g, double* ms, long long* points, long long* cycles, long long* chain_steps,
                           int cap);
+
+/* ---- time sharding over GPUs (csrc/timeshard.cpp) -------
+ * One rank per GPU owns a contiguous block of the level-0 coarse intervals;
+ * operators and coarser levels are replicated.  With a communicator attached,
+ * phi_mgrit_solve runs the sharded schedule in the engine: a halo shift of one
+ * n-vector before every relaxation sweep, an allgather of the owned coarse
+ * right-hand sides after the restriction, the coarse cycle replicated, and
+ * point-ordered reductions (allgather of the owned per-point terms) -- the
+ * same floating-point operations as one process, so the results are
+ * identical for any rank count.  phi_mgrit_trajectory then gathers the
+ * trajectory (collective: every rank calls it). */
+typedef struct phi_comm phi_comm;
+/* host-callback transport: host buffers; return 0 on success.
+ * shift: send `count` values to rank + 1 (send null on the last rank) and
+ * receive `count` from rank - 1 (recv null on rank 0);
+ * allgather: recv[r * count ..] = rank r's send, in rank order. */
+typedef struct {
+    void* ctx;
+    int (*shift)(void* ctx, const double* send, double* recv, long long count);
+    int (*allgather)(void* ctx, const double* send, double* recv, long long count);
+} phi_comm_ops;
+/* NCCL transport (ncclSend/ncclRecv, ncclAllGather on the engine stream):
+ * rank 0 creates the 128-byte id, the caller distributes it to every rank */
+int phi_comm_nccl_unique_id(unsigned char* id128);
+int phi_comm_create_nccl(const unsigned char* id128, int nranks, int rank, phi_comm** out);
+int phi_comm_create_ops(const phi_comm_ops* ops, int nranks, int rank, phi_comm** out);
+void phi_comm_free(phi_comm* c);
+/* attach (null: detach -- single process); the comm must outlive its use */
+int phi_mgrit_set_comm(phi_mgrit* g, phi_comm* c);
 
 /* Developer knob (not part of the reference API): warps used by the sync-free
  * triangular solves / Gauss-Seidel sweeps and the readiness-poll back-off. */

@@ -34,8 +34,9 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-u
 
 CU = ["phi_launch.cu", "assembly.cu", "spmm.cu", "ilut.cu"]
 DEGREES = range(1, 9)  # phi_deg.cu is compiled once per spline degree (-DPHI_DEG=d)
-CPP = ["setup_host.cpp", "engine.cpp", "capi.cpp"]
-HEADERS = ["common.hpp", "device_types.cuh", "phi_kernels.cuh", "phi_device.cuh", "setup_host.hpp", "engine.hpp"]
+CPP = ["setup_host.cpp", "engine.cpp", "capi.cpp", "timeshard.cpp"]
+HEADERS = ["common.hpp", "device_types.cuh", "phi_kernels.cuh", "phi_device.cuh", "setup_host.hpp", "engine.hpp",
+           "timeshard.hpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -94,7 +95,7 @@ def build(verbose: bool = False) -> str:
         for part in ex.map(compile_one, jobs):
             log += part
     if jobs or _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"], log)
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"], log)
     with open(os.path.join(OUT_DIR, "build.log"), "w") as f:
         f.write("\n".join(log))
     if verbose:

@@ -595,6 +595,7 @@ int phi_mgrit_solve(phi_mgrit* g, phi_mgrit_result* res, double* history, int hi
 
 int phi_mgrit_trajectory(const phi_mgrit* g, double* out) {
     return guarded([&] {
+        const_cast<phi_mgrit*>(g)->g->gather_trajectory();  // sharded: collective gather
         const auto& lv = g->g->levels[0];
         PHI_CUDA(cudaMemcpyAsync(out, lv.u.get(), sizeof(double) * lv.u.size(), cudaMemcpyDeviceToHost,
                                  g->g->stream));
@@ -695,5 +696,41 @@ int phi_dev_tuning(int tri_warps, int gs_warps, int sleep_ns) {
 }
 
 int phi_dev_trace(long long* out, int n) { return phi_read_trace(out, n); }
+
+struct phi_comm {
+    std::unique_ptr<Comm> c;
+};
+
+int phi_comm_nccl_unique_id(unsigned char* id128) {
+    return guarded([&] {
+        const NcclUniqueId id = nccl_unique_id();
+        std::memcpy(id128, id.internal, sizeof id.internal);
+    });
+}
+
+int phi_comm_create_nccl(const unsigned char* id128, int nranks, int rank, phi_comm** out) {
+    return guarded([&] {
+        NcclUniqueId id;
+        std::memcpy(id.internal, id128, sizeof id.internal);
+        auto* c = new phi_comm;
+        c->c = make_nccl_comm(id, nranks, rank);
+        *out = c;
+    });
+}
+
+int phi_comm_create_ops(const phi_comm_ops* ops, int nranks, int rank, phi_comm** out) {
+    return guarded([&] {
+        if (!ops) throw InvalidArgument("phi_comm_ops: null");
+        auto* c = new phi_comm;
+        c->c = make_ops_comm(CommOps{ops->ctx, ops->shift, ops->allgather}, nranks, rank);
+        *out = c;
+    });
+}
+
+void phi_comm_free(phi_comm* c) { delete c; }
+
+int phi_mgrit_set_comm(phi_mgrit* g, phi_comm* c) {
+    return guarded([&] { g->g->set_comm(c ? c->c.get() : nullptr); });
+}
 
 }  // extern "C"

@@ -821,6 +821,7 @@ void Mgrit::phase(int l, int op) {
             break;
         }
         case 4: cycle_impl(l, cfg.cycle == 1); break;
+        case 5: cycle_impl(l, false); break;  // the F-schedule's second pass below level l - 1
         default: throw InvalidArgument("unknown MGRIT phase");
     }
     PHI_CUDA(cudaStreamSynchronize(stream));
@@ -938,6 +939,7 @@ int Mgrit::wave_report(double* ms, double* bytes) {
 }
 
 MgritResultHost Mgrit::solve() {
+    if (comm) return solve_sharded();
     launches = 0;
     for (auto& r : recs) {
         cudaEventDestroy(r.start);

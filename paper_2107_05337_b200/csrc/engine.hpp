@@ -14,6 +14,7 @@
 #include "device_types.cuh"
 #include "phi_kernels.cuh"
 #include "setup_host.hpp"
+#include "timeshard.hpp"
 
 namespace phi {
 
@@ -219,6 +220,16 @@ public:
     void stats(long long* out4) const;           // level-0 solves, iters; coarser solves, iters
     int n_levels() const { return (int)levels.size(); }
 
+    // ---- time sharding in the C++ host (timeshard.cpp): with a communicator
+    // attached, solve() runs the sharded schedule itself (halo shifts,
+    // allgathered coarse right-hand sides, point-ordered reductions)
+    Comm* comm = nullptr;
+    bool traj_gathered = false;
+    void set_comm(Comm* c);
+    MgritResultHost solve_sharded();
+    /// level-0 trajectory of every rank's points on every rank (collective)
+    void gather_trajectory();
+
     struct Level {
         int steps = 0;
         double dt = 0.0;
@@ -279,6 +290,10 @@ private:
     void interpolate_and_correct(int l);
     void coarsest_solve(int l);
     void cycle_impl(int l, bool f_schedule);
+    void halo();
+    void combine_coarse_rhs();
+    void cycle0_sharded(bool f_schedule);
+    std::vector<std::pair<int, int>> owned_points(int l) const;
 };
 
 /// Sequential Phi-march on device (sequential_integrate, theta.hpp:216-237):

@@ -38,6 +38,7 @@ EXPORTED = [
     "phi_dev_tuning", "phi_dev_trace", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
     "phi_mgrit_gnorm_terms", "phi_mgrit_residual_terms", "phi_mgrit_phase", "phi_mgrit_points",
     "phi_mgrit_stats", "phi_mgrit_residual_iters", "phi_mgrit_wave_levels",
+    "phi_comm_nccl_unique_id", "phi_comm_create_nccl", "phi_comm_create_ops", "phi_comm_free", "phi_mgrit_set_comm",
 ]
 
 
@@ -139,6 +140,12 @@ def lib():
         L.phi_mgrit_residual_terms.argtypes = [_vp, _i, _vp]
         L.phi_mgrit_residual_iters.argtypes = [_vp, _i, _vp]
         L.phi_mgrit_wave_levels.argtypes = [_vp, _vp, _vp, _vp, _vp, _i]
+        L.phi_comm_nccl_unique_id.argtypes = [_vp]
+        L.phi_comm_create_nccl.argtypes = [_vp, _i, _i, _vp]
+        L.phi_comm_create_ops.argtypes = [_vp, _i, _i, _vp]
+        L.phi_comm_free.argtypes = [_vp]
+        L.phi_comm_free.restype = None
+        L.phi_mgrit_set_comm.argtypes = [_vp, _vp]
         L.phi_mgrit_phase.argtypes = [_vp, _i, _i]
         L.phi_mgrit_points.argtypes = [_vp, _i, _i, _i, _i, _vp, _i, _i]
         L.phi_mgrit_stats.argtypes = [_vp, _vp]
@@ -387,6 +394,70 @@ class MgritResult:
     residual_history: np.ndarray = field(repr=False)
 
 
+_SHIFT = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_longlong)
+_GATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_longlong)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("shift", _SHIFT), ("allgather", _GATHER)]
+
+
+class Comm:
+    """A rank of the time partition (phi_comm, include/phi_engine.h): attach
+    with MgritSolver.set_comm and solve() runs the sharded schedule in the
+    engine.  Comm.nccl(id, nranks, rank): NCCL over NVLink; Comm.ops(shift,
+    allgather, nranks, rank): host callbacks on numpy arrays."""
+
+    def __init__(self, handle, keep=None):
+        self.h = handle
+        self._keep = keep
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(lib().phi_comm_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, uid: bytes, nranks: int, rank: int) -> "Comm":
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        h = _vp()
+        _check(lib().phi_comm_create_nccl(buf, nranks, rank, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def ops(cls, shift, allgather, nranks: int, rank: int) -> "Comm":
+        """shift(send | None, count) -> recv | None; allgather(send) -> all
+        (numpy float64 arrays)."""
+        def _shift(_ctx, send, recv, count):
+            try:
+                s = np.ctypeslib.as_array(send, (count,)).copy() if send else None
+                r = shift(s, count)
+                if recv:
+                    np.ctypeslib.as_array(recv, (count,))[:] = r
+                return 0
+            except Exception:  # reported to the engine as a transport failure
+                return 1
+
+        def _gather(_ctx, send, recv, count):
+            try:
+                a = allgather(np.ctypeslib.as_array(send, (count,)).copy())
+                np.ctypeslib.as_array(recv, (count * nranks,))[:] = a
+                return 0
+            except Exception:
+                return 1
+
+        ops = CommOps(None, _SHIFT(_shift), _GATHER(_gather))
+        h = _vp()
+        _check(lib().phi_comm_create_ops(C.byref(ops), nranks, rank, C.byref(h)))
+        return cls(h, keep=ops)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.phi_comm_free(self.h)
+            self.h = None
+
+
 class MgritSolver:
     """MgritSolver(disc, ps, cfg, scfg) (mgrit.hpp:50-320); space-time state on device."""
 
@@ -473,6 +544,11 @@ class MgritSolver:
         out = np.zeros(self.levels()[0][level] + 1)
         _check(lib().phi_mgrit_residual_terms(self.h, level, _p(out)))
         return out
+
+    def set_comm(self, comm: "Comm | None") -> None:
+        """Shard level 0 over the communicator's ranks (None: one process)."""
+        self._comm = comm
+        _check(lib().phi_mgrit_set_comm(self.h, comm.h if comm is not None else None))
 
     def residual_iters(self, level: int = 0) -> np.ndarray:
         """Per-solve p-MG cycle counts of the residual wave at the current state."""

@@ -10,13 +10,14 @@ coarse intervals of level 0 (`partition`).  Per MGRIT iteration
                       halo exchange (one n-vector, rank r-1 -> r) precedes
                       every relaxation sweep;
   restriction         local (each coarse point j+1 is restricted from the
-                      owned interval j); the coarse right-hand sides are then
-                      combined by an elementwise allreduce-sum of arrays that
-                      are zero outside each rank's points -- exact, since every
-                      entry has exactly one nonzero contributor;
+                      owned interval j); every rank then gathers the other
+                      ranks' coarse right-hand sides (an allgather of the owned
+                      points only, padded to the largest share);
   coarse cycle        replicated on every rank (the serial coarse march is the
                       Amdahl term either way, and replication needs no
-                      scatter);
+                      scatter); under the F-schedule the second pass runs its
+                      coarse cycle without the schedule, as cycle_impl(l,
+                      false) does (mgrit.hpp:278-288);
   correction          injection of the coarse correction (replicated), then a
                       local F-relaxation;
   residual norm       per-point squared residuals of the owned points, summed
@@ -29,6 +30,13 @@ interface of the engine's C ABI (phi_mgrit_phase & co.); `EngineExecutor`
 wraps the CUDA engine.  With identical inputs the sharded solve performs the
 same floating-point operations as the single-process solve, so its results
 are identical for any rank count.
+
+The product path for N > 1 is the same schedule in the C++ host
+(csrc/timeshard.cpp, phi_mgrit_set_comm): `nccl_comm_from_torch` builds its
+NCCL communicator (the unique id travels over torch.distributed) and
+MgritSolver.solve() then runs sharded inside the engine.  TimeShardedMgrit
+below is the Python statement of that schedule over any phase-level
+executor; the CPU tests drive it with an executor over the oracle.
 """
 from __future__ import annotations
 
@@ -38,8 +46,20 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-OP_F, OP_FC, OP_RESTRICT, OP_INJECT, OP_CYCLE = range(5)
+# phase ops of phi_mgrit_phase; OP_CYCLE runs cycle_impl(l, cycle == F),
+# OP_CYCLE_NOF cycle_impl(l, false)
+OP_F, OP_FC, OP_RESTRICT, OP_INJECT, OP_CYCLE, OP_CYCLE_NOF = range(6)
 U, G = 0, 1
+
+
+def nccl_comm_from_torch(group=None):
+    """phi_comm over NCCL for this torch.distributed rank (one GPU per rank):
+    rank 0 creates the NCCL unique id and broadcasts it."""
+    from .engine import Comm
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    box = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return Comm.nccl(box[0], size, rank)
 
 
 def partition(n_intervals: int, n_ranks: int, rank: int) -> tuple[int, int]:
@@ -71,6 +91,15 @@ class TorchComm:
 
     def allreduce_sum(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        """Every rank's `t` (same size on all ranks), concatenated in rank order."""
+        out = torch.empty(self.size * t.numel(), dtype=t.dtype, device=t.device)
+        if hasattr(dist, "all_gather_into_tensor") and t.is_cuda:
+            dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+        else:
+            dist.all_gather(list(out.chunk(self.size)), t.contiguous(), group=self.group)
+        return out
 
 
 @dataclass
@@ -118,12 +147,18 @@ class TimeShardedMgrit:
             self.ex.set_points(0, U, self.j0 * self.m, recv)
 
     def combine_coarse_rhs(self) -> None:
-        """Coarse g at points j + 1 of the owned intervals, summed over ranks."""
-        n, J = self.n, self.J
-        full = torch.zeros((J + 1) * n, dtype=torch.float64, device=self.comm.device)
-        full[(self.j0 + 1) * n:(self.j1 + 1) * n] = self.ex.get_points(1, G, self.j0 + 1, self.j1 - self.j0)
-        self.comm.allreduce_sum(full)
-        self.ex.set_points(1, G, 1, full[n:])
+        """Coarse g at points j + 1 of every rank's intervals: an allgather of
+        the owned points (padded to the largest share), placed in rank order."""
+        n, J, R = self.n, self.J, self.comm.size
+        shares = [partition(J, R, r) for r in range(R)]
+        width = max(b - a for a, b in shares)
+        mine = torch.zeros(width * n, dtype=torch.float64, device=self.comm.device)
+        own = self.j1 - self.j0
+        if own:
+            mine[:own * n] = self.ex.get_points(1, G, self.j0 + 1, own)
+        parts = self.comm.allgather(mine).view(R, width * n)
+        full = torch.cat([parts[r, :(b - a) * n] for r, (a, b) in enumerate(shares)])
+        self.ex.set_points(1, G, 1, full)
         # restriction zeroes the coarse iterate at every restricted point
         self.ex.set_points(1, U, 1, torch.zeros(J * n, dtype=torch.float64, device=self.comm.device))
 
@@ -145,7 +180,7 @@ class TimeShardedMgrit:
         ex.phase(0, OP_F)
         ex.phase(0, OP_RESTRICT)
         self.combine_coarse_rhs()
-        ex.phase(1, OP_CYCLE)  # replicated coarse cycle
+        ex.phase(1, OP_CYCLE if f_schedule else OP_CYCLE_NOF)  # replicated coarse cycle
         ex.phase(0, OP_INJECT)
         self.halo()
         ex.phase(0, OP_F)

@@ -21,6 +21,9 @@ Fixtures
                   f=0, u0=sin sin): MgritSolver::solve() (mgrit.hpp:93-118) result,
                   residual history, projected u0 and the trajectory.
   mgrit_cg.npz    as mgrit_src.npz with the CG spatial solver (theta.hpp:121-125)
+  mgrit_fcycle.npz  F-cycle (cycle=F, FCF) over 4 levels (p=2, h=2^-3, Nt=64, m=2:
+                  64/32/16/8), transient source, spline u0: the F-schedule's second
+                  pass (mgrit.hpp:278-288) with a coarse cycle below it.
   mgrit_src.npz   the config-2 shape at small size (p=3, h=2^-4, Nt=32, m=8, transient
                   2 pi^2 e^-t sin sin source, spline u0 from seeded U[-1,1] coefficients):
                   result, u0, the level-0 load terms and the trajectory.
@@ -116,6 +119,7 @@ def mgrit_fixture(p, k, nt, **kw) -> dict:
 def fixtures() -> dict:
     """name -> builder of each committed fixture."""
     coeffs = np.random.default_rng(12345).uniform(-1.0, 1.0, (2 ** 4 + 3 - 2) ** 2)
+    coeffs3 = np.random.default_rng(12345).uniform(-1.0, 1.0, (2 ** 3 + 2 - 2) ** 2)
     return {
         "ops_p2k3.npz": ops_fixture,
         "mgrit_c1.npz": lambda: mgrit_fixture(2, 4, 100, cycle=O.CYCLE_TWO_LEVEL, m=4,
@@ -123,6 +127,9 @@ def fixtures() -> dict:
         "mgrit_src.npz": lambda: dict(coeffs=coeffs, **mgrit_fixture(
             3, 4, 32, cycle=O.CYCLE_TWO_LEVEL, m=8, source_kind=O.SOURCE_SIN_EXP,
             source_param=2 * np.pi ** 2, init_kind=O.INIT_COEFFS, init_coeffs=coeffs)),
+        "mgrit_fcycle.npz": lambda: dict(coeffs=coeffs3, **mgrit_fixture(
+            2, 3, 64, cycle=O.CYCLE_F, m=2, source_kind=O.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2,
+            init_kind=O.INIT_COEFFS, init_coeffs=coeffs3)),
         # the CG spatial-solver kind (SpatialSolverKind::cg, theta.hpp:64, 121-125)
         "mgrit_cg.npz": lambda: dict(coeffs=coeffs, **mgrit_fixture(
             3, 4, 32, cycle=O.CYCLE_TWO_LEVEL, m=8, source_kind=O.SOURCE_SIN_EXP,

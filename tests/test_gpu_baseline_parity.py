@@ -19,7 +19,11 @@ Cases:
   * config 3 (p=4, h=2^-7, Nt=2500, m=4): initialize + 2 MGRIT iterations;
   * config-4 shape (p=5, h=2^-8, m=8, transient source, u0 = 0) at Nt=48,
     in both summation modes -- the exact mode bit for bit;
-  * one V(1,1) cycle and full solves at h=2^-8 for p = 2..5 (config 5).
+  * one V(1,1) cycle and full solves at h=2^-8 for p = 2..5 (config 5);
+  * the multilevel variants: config 3 at Nt=2560 with
+    coarse_floor 41 (3 levels 2560/640/160), initialize + 2 iterations, and
+    the config-4 operator over 3 levels (Nt=128, m=4: 128/32/8) to
+    convergence, both modes.
 """
 import os
 
@@ -193,3 +197,70 @@ def test_config5_vcycle_and_solve_k8(p):
         assert abs(int(got["iterations"][i]) - ref["iterations"]) <= 1
         assert got["converged"][i]
         assert _rel(got["x"][i], ref["x"]) <= 1e-9
+
+
+@pytest.mark.slow
+def test_config3_multilevel_variant_two_iterations():
+    """C3 operator, Nt=2560, m=4, coarse_floor=41: the reference's three
+    levels 2560/640/160 (bench.py --config c3ml)."""
+    _need_ref()
+    p, k, nt = 4, 7, 2560
+    kw = dict(cycle=E.CYCLE_V, m=4, source_param=0.0, init_kind=E.INIT_COEFFS, init_coeffs=_coeffs(p, k),
+              coarse_floor=41)
+    eng, ref = _pair(p, k, nt, **kw)
+    assert eng.levels()[0] == [2560, 640, 160]
+    he, hr, worst, differ = _step_and_compare(eng, ref, 2)
+    assert np.all(np.abs(he - hr) <= 1e-6 * hr)
+    ur = np.concatenate([ref.points(0, 0, k0, min(512, nt + 1 - k0)) for k0 in range(0, nt + 1, 512)])
+    assert _rel(eng.trajectory(), ur) <= TOL_TRAJ
+
+
+@pytest.fixture(scope="module")
+def c4_multilevel():
+    """C4 operator and source over three levels (Nt=128, m=4: 128/32/8)."""
+    _need_ref()
+    p, k, nt = 5, 8, 128
+    kw = dict(cycle=E.CYCLE_V, m=4, source_kind=E.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2)
+    ref = O.RefMgrit(p, k, nt, workers=WORKERS, **kw)
+    assert ref.levels()[0] == [128, 32, 8]
+    rr = ref.solve()
+    return dict(p=p, k=k, nt=nt, kw=kw, ref=ref, res=rr, traj=ref.trajectory())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("exact", [True, False])
+def test_config4_multilevel_shape(c4_multilevel, exact):
+    c = c4_multilevel
+    eng = E.MgritSolver(E.SpatialDiscretization.build(c["p"], c["k"]), c["nt"], exact=exact, **c["kw"])
+    r = eng.solve()
+    if exact:
+        assert r.iterations == c["res"]["iterations"]
+        assert r.total_spatial_solves == c["res"]["total_spatial_solves"]
+        assert np.array_equal(r.residual_history, c["res"]["residual_history"])
+        assert np.array_equal(eng.trajectory(), c["traj"])
+    else:
+        assert abs(r.iterations - c["res"]["iterations"]) <= 1 and r.converged
+        assert r.total_spatial_solves == c["res"]["total_spatial_solves"]
+        assert abs(r.mean_spatial_iterations - c["res"]["mean_spatial_iterations"]) <= 0.02
+        assert _rel(eng.trajectory(), c["traj"]) <= TOL_TRAJ
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_fcycle_four_levels_golden(exact):
+    """F-cycle over four levels against the committed reference fixture
+    (tests/golden/mgrit_fcycle.npz): bitwise in exact mode."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "mgrit_fcycle.npz"))
+    p, k, nt = 2, 3, 64
+    eng = E.MgritSolver(E.SpatialDiscretization.build(p, k), nt, cycle=E.CYCLE_F, m=2,
+                        source_kind=E.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2, init_kind=E.INIT_COEFFS,
+                        init_coeffs=g["coeffs"], exact=exact)
+    assert eng.levels()[0] == [int(v) for v in g["levels_steps"]]
+    r = eng.solve()
+    if exact:
+        assert r.iterations == int(g["iterations"][0])
+        assert r.total_spatial_solves == int(g["solves"][0])
+        assert np.array_equal(r.residual_history, g["history"])
+        assert np.array_equal(eng.trajectory(), g["trajectory"])
+    else:
+        assert abs(r.iterations - int(g["iterations"][0])) <= 1
+        assert _rel(eng.trajectory(), g["trajectory"]) <= TOL_TRAJ

@@ -32,11 +32,13 @@ def group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exact", [True, False])
-def test_sharded_driver_equals_solve(group, exact):
+@pytest.mark.parametrize("exact,cycle,m", [(True, 2, 8), (False, 2, 8), (True, 1, 2), (False, 1, 2)])
+def test_sharded_driver_equals_solve(group, exact, cycle, m):
+    """cycle 1 (F) with m = 2: 64/32/16/8, four levels -- the F-schedule's
+    second pass runs its coarse cycle without the schedule (OP_CYCLE_NOF)."""
     p, k, nt = 3, 5, 64
     coeffs = np.random.default_rng(12345).uniform(-1, 1, (2 ** k + p - 2) ** 2)
-    kw = dict(cycle=E.CYCLE_TWO_LEVEL, m=8, source_kind=E.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2,
+    kw = dict(cycle=cycle, m=m, source_kind=E.SOURCE_SIN_EXP, source_param=2 * np.pi ** 2,
               init_kind=E.INIT_COEFFS, init_coeffs=coeffs, exact=exact)
     d = E.SpatialDiscretization.build(p, k)
     ref = E.MgritSolver(d, nt, **kw)

@@ -152,6 +152,8 @@ class OracleExecutor:
             self._restrict(l)
         elif op == TS.OP_INJECT:
             self._inject(l)
+        elif op == TS.OP_CYCLE_NOF:
+            self._cycle(l, False)
         else:
             self._cycle(l, self.cycle == 1)
 
@@ -179,15 +181,17 @@ def _ops(g):
             "h_embed": [csr(f"h_embed{l}") for l in range(nh - 1)]}
 
 
-def _worker(rank, world, port, name, m, out):
+def _worker(rank, world, port, name, m, out, cycle=2):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g = np.load(os.path.join(GOLD, name))
         nt = g["trajectory"].shape[0] - 1
-        ex = OracleExecutor(O.OcDisc(_ops(g)), nt, m, u0=g["u0"], loads=g["loads"] if "loads" in g.files else None)
-        drv = TS.TimeShardedMgrit(ex, TS.TorchComm(torch.device("cpu")), cycle=2, relax=1, halt_tol=1e-10,
+        ex = OracleExecutor(O.OcDisc(_ops(g)), nt, m, u0=g["u0"], loads=g["loads"] if "loads" in g.files else None,
+                            cycle=cycle)
+        assert ex.steps == [int(v) for v in g["levels_steps"]]
+        drv = TS.TimeShardedMgrit(ex, TS.TorchComm(torch.device("cpu")), cycle=cycle, relax=1, halt_tol=1e-10,
                                   max_iter=50)
         r = drv.solve()
         traj = drv.trajectory()
@@ -206,16 +210,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name,m", [("mgrit_src.npz", 8), ("mgrit_c1.npz", 4)])
-def test_time_sharded_matches_reference_world2(name, m):
+@pytest.mark.parametrize("name,m,cycle", [("mgrit_src.npz", 8, 2), ("mgrit_c1.npz", 4, 2),
+                                          ("mgrit_fcycle.npz", 2, 1)])
+def test_time_sharded_matches_reference_world2(name, m, cycle):
+    """mgrit_fcycle: the F-schedule over 4 levels -- the second pass's coarse
+    cycle must run without the schedule (OP_CYCLE_NOF), as in the reference."""
     if not os.path.exists(O.OC_SO):
         import subprocess
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, m, q)) for r in range(2) for port in [None]]
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, m, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, m, q, cycle)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
