@@ -35,6 +35,8 @@ extern "C" {
 #define PHI_INIT_ZERO 0        /* ProblemSpec::initial empty                       */
 #define PHI_INIT_SIN 1         /* sin(pi x) sin(pi y), L2-projected                */
 #define PHI_INIT_COEFFS 2      /* spline sum_i c_i phi_i (free dofs), L2-projected */
+#define PHI_INIT_VECTOR 3      /* init_coeffs IS the projected free-dof state u0 (a
+                                * caller that ran project_initial itself, theta.hpp:150-160) */
 
 typedef struct phi_disc phi_disc;
 typedef struct phi_hier phi_hier;
@@ -147,6 +149,10 @@ int phi_hier_spmm(phi_hier* h, const double* x, double* y, int nrhs, int device_
  * which 1: one V(nu_pre, nu_post) cycle (pmultigrid.hpp:256-267) from x0 = 0
  * on nrhs right-hand sides (one CTA each).  flush_l2: write 256 MB between reps. */
 int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, double* ms_out);
+/* Algorithmic bytes of one V(nu_pre, nu_post) cycle on nrhs right-hand sides
+ * (SURVEY.md 8(d) model: 8 B per stored operator nonzero per application and
+ * batch + 8 B per vector entry read or written per right-hand side) */
+int phi_hier_vcycle_bytes(const phi_hier* h, int nrhs, double* bytes);
 /* Building blocks for parity tests (single vector, host arrays):
  * op 0 y = A_p x; 1 z = ilut_apply(r); 2 r1 = restrict_to_linear(r);
  * 3 x += prolong_from_linear(e1) (x in/out); 4 x1 = hmg_wcycle(b1, x1);

@@ -349,6 +349,13 @@ int phi_hier_spmm(phi_hier* h, const double* x, double* y, int nrhs, int device_
     });
 }
 
+int phi_hier_vcycle_bytes(const phi_hier* h, int nrhs, double* bytes) {
+    return guarded([&] {
+        if (nrhs < 1) throw InvalidArgument("phi_hier_vcycle_bytes: nrhs must be positive");
+        *bytes = 8.0 * (h->h->vcycle_matrix_entries() + nrhs * h->h->vcycle_vector_entries());
+    });
+}
+
 int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, double* ms_out) {
     return guarded([&] {
         if (reps < 1 || nrhs < 1) throw InvalidArgument("phi_hier_time: reps and nrhs must be positive");
@@ -543,7 +550,7 @@ int phi_mgrit_create(const phi_disc* d, const phi_problem* ps, const phi_mgrit_c
         po.source_param = ps->source_param;
         po.init_kind = ps->init_kind;
         const int n = d->d->n_p;
-        if (ps->init_kind == PHI_INIT_COEFFS) {
+        if (ps->init_kind == PHI_INIT_COEFFS || ps->init_kind == PHI_INIT_VECTOR) {
             if (!ps->init_coeffs) throw InvalidArgument("init_coeffs missing");
             po.init_coeffs.assign(ps->init_coeffs, ps->init_coeffs + n);
         }

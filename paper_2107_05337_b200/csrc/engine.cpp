@@ -158,6 +158,18 @@ void Disc::assemble_load(int kind, double c0, double c1, const double* coeffs_de
                          coeffs_dev, out, s);
 }
 
+namespace {
+// nnz of a stencil operator's valid (in-grid) entries = reference CSR nnz
+long long stencil_nnz(const DevStencil& A) {
+    long long s = 0;
+    for (int iv = 0; iv < A.rv; ++iv) {
+        const int dv = std::min(A.hi, A.cv - 1 - iv) - std::max(A.lo, -iv) + 1;
+        for (int iu = 0; iu < A.ru; ++iu) s += (long long)dv * (std::min(A.hi, A.cu - 1 - iu) - std::max(A.lo, -iu) + 1);
+    }
+    return s;
+}
+}  // namespace
+
 // ---------------------------------------------------------------------------
 // Hier
 // ---------------------------------------------------------------------------
@@ -314,6 +326,35 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
 }
 
 HostCsr Hier::a_h_csr(int l) const { return stencil_to_csr(a_h.at(l)); }
+
+// Byte model of one V(nu_pre, nu_post) cycle, in
+// fp64 entries: every stored nonzero of the operators the cycle applies,
+// once per application and batch (A for the two smoothing residuals and the
+// residual before the restriction, L and U twice, T and T^T, the h-chain
+// with 2^l visits of level l: 4 sweeps + residual of A_l, E and E^T, the
+// dense coarse LU); and per right-hand side every vector entry read or
+// written.
+double Hier::vcycle_matrix_entries() const {
+    const Disc& d = *disc;
+    double vmat = 3.0 * stencil_nnz(A.view()) + 2.0 * (L_host.nnz() + U_host.nnz()) + 2.0 * stencil_nnz(d.T.view());
+    const int nh = (int)d.h.size();
+    for (int l = 0; l + 1 < nh; ++l)
+        vmat += std::ldexp(1.0, l) * (5.0 * stencil_nnz(a_h[l].view()) + 2.0 * d.h[l].E.nnz());
+    vmat += std::ldexp(1.0, nh - 1) * (double)coarse.n * coarse.n;
+    return vmat;
+}
+
+double Hier::vcycle_vector_entries() const {
+    const Disc& d = *disc;
+    const double n = d.n_p, n1 = d.n_1;
+    double vvec = 18 * n + 3 * n + (n + n1) + (n1 + 2 * n);
+    const int nh = (int)d.h.size();
+    for (int l = 0; l + 1 < nh; ++l) {
+        const double nl = d.h[l].n, nc = d.h[l + 1].n;
+        vvec += std::ldexp(1.0, l) * (4 * 3 * nl + 3 * nl + (nl + nc) + nc + (nc + 2 * nl));
+    }
+    return vvec;
+}
 
 long long Hier::chain_steps() const {
     if (cg_only || opt.exact) return 0;
@@ -543,6 +584,12 @@ void Mgrit::project_initial() {
     const int n = disc->n_p;
     if (ps.init_kind == 0) {
         u0.zero(stream);
+        return;
+    }
+    if (ps.init_kind == 3) {  // the caller's projected initial state, as is
+        if ((int)ps.init_coeffs.size() != n) throw InvalidArgument("initial state: dimension mismatch");
+        u0.upload(ps.init_coeffs, stream);
+        PHI_CUDA(cudaStreamSynchronize(stream));
         return;
     }
     DevBuf<double> b(n), work(4 * (size_t)n), coeffs;
@@ -852,21 +899,12 @@ void Mgrit::stats(long long* out4) const {
 }
 
 void Mgrit::set_init_coeffs(const double* host) {
-    if (ps.init_kind != 2) throw InvalidArgument("set_init_coeffs: problem has no coefficient initial condition");
+    if (ps.init_kind != 2 && ps.init_kind != 3)
+        throw InvalidArgument("set_init_coeffs: problem has no coefficient initial condition");
     std::copy(host, host + disc->n_p, ps.init_coeffs.begin());
 }
 
-namespace {
-// nnz of a stencil operator's valid (in-grid) entries = reference CSR nnz
-long long stencil_nnz(const DevStencil& A) {
-    long long s = 0;
-    for (int iv = 0; iv < A.rv; ++iv) {
-        const int dv = std::min(A.hi, A.cv - 1 - iv) - std::max(A.lo, -iv) + 1;
-        for (int iu = 0; iu < A.ru; ++iu) s += (long long)dv * (std::min(A.hi, A.cu - 1 - iu) - std::max(A.lo, -iu) + 1);
-    }
-    return s;
-}
-}  // namespace
+
 
 void Mgrit::wave_levels(double* ms, long long* points, long long* cycles, int cap) {
     for (int l = 0; l < cap; ++l) {
@@ -912,16 +950,8 @@ int Mgrit::wave_report(double* ms, double* bytes) {
             *bytes += 8.0 * (mat + vec);
             continue;
         }
-        double vmat = 3 * nnzA + 2.0 * (H.L_host.nnz() + H.U_host.nnz()) + 2.0 * stencil_nnz(d.T.view());
-        double vvec = 18 * n + 3 * n + (n + n1) + (n1 + 2 * n);
-        const int nh = (int)d.h.size();
-        for (int l = 0; l + 1 < nh; ++l) {
-            const double visits = std::ldexp(1.0, l);
-            const double nl = d.h[l].n, nc = d.h[l + 1].n;
-            vmat += visits * (5.0 * stencil_nnz(H.a_h[l].view()) + 2.0 * d.h[l].E.nnz());
-            vvec += visits * (4 * 3 * nl + 3 * nl + (nl + nc) + nc + (nc + 2 * nl));
-        }
-        vmat += std::ldexp(1.0, nh - 1) * (double)H.coarse.n * H.coarse.n;
+        const double vmat = H.vcycle_matrix_entries(), vvec = H.vcycle_vector_entries();
+        (void)n1;
         if (std::getenv("PHI_WAVE_DEBUG"))
             std::fprintf(stderr, "wave %zu level %d: %.3f ms, points %d, cycles sum %d max %d\n", k, recs[k].level,
                          t, (int)pts, (int)csum, (int)cmax);

@@ -144,6 +144,10 @@ public:
     /// smoothings, Gauss-Seidel lines / blocks of the W-cycle sweeps, one
     /// step per dense coarse application -- the latency model of bench.py.
     long long chain_steps() const;
+    /// Byte model of one V-cycle: operator entries read per
+    /// batch, vector entries read or written per right-hand side.
+    double vcycle_matrix_entries() const;
+    double vcycle_vector_entries() const;
 };
 
 /// Message of a failed spatial solve (theta.hpp:116-118, 123-124; a negative

@@ -688,11 +688,12 @@ __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int 
 // The blocks stream through a shared-memory ring of n_slots units filled by
 // TMA bulk copies: the workers wait for a unit's mbarrier, the solver
 // refills the slot of block g (with block g + n_slots) once block g is done.
-// Hand-offs are plain shared-memory flags: `prog` (last block done) and
-// cnt[g % kBlkHand] (parts of block g summed, shared-memory atomics).  A
-// warp's shared-memory accesses are performed in order, and __syncwarp()
-// orders the lanes' data stores before the flag update of lane 0; a
-// global-memory vector is fenced (__threadfence_block) before its flag.
+// Hand-offs are shared-memory flags with release / acquire semantics at CTA
+// scope: `prog` (last block done, st.release after the block's values) and
+// cnt[g % kBlkHand] (parts of block g summed, red.release.add); waiters spin
+// with ld.acquire.  __syncwarp() orders the lanes' data stores before the
+// releasing lane's flag update; a global-memory vector is fenced
+// (__threadfence_block) before its flag.
 __device__ __forceinline__ void st_volatile_s32(unsigned a, int v) {
     asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -701,16 +702,27 @@ __device__ __forceinline__ int ld_volatile_s32(unsigned a) {
     asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_release_s32(unsigned a, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_s32(unsigned a) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned a, int v) {
+    asm volatile("red.release.cta.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __noinline__ void spin_fail(int what, int have, int want) {
     printf("phi spin guard: block %d thread %d wait %d have %d want %d\n", blockIdx.x, threadIdx.x, what, have, want);
     __trap();
 }
 // spin until *a >= v; returns the value seen
 __device__ __forceinline__ int wait_ge(unsigned a, int v) {
-    int h = ld_volatile_s32(a);
+    int h = ld_acquire_s32(a);
     if (h >= v) return h;
     const long long t0 = PHI_SPIN_GUARD ? clock64() : 0;
-    while ((h = ld_volatile_s32(a)) < v)
+    while ((h = ld_acquire_s32(a)) < v)
         if (PHI_SPIN_GUARD && clock64() - t0 > 4000000000LL) spin_fail(1, h, v);
     return h;
 }
@@ -910,8 +922,8 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             }
             if constexpr (!XSM) __threadfence_block();  // global x: order the stores before the hand-off
             __syncwarp();
-            if (lane == 0) st_volatile_s32(prog, g);  // monotone: block g+1 starts after the hand-off
-            if (g + 1 < total) hand_signal(kHandBar + w);
+            if (g + 1 < total) hand_signal(kHandBar + w);  // the chain: block g+1 may start
+            if (lane == 0) st_release_s32(prog, g);  // monotone; read by the workers (off the chain)
             if (tr) tr[5] = clock64();
             // ---- off the chain: bookkeeping for this solver's next block
             if (lane == 0) {
@@ -984,7 +996,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                          "d"(a0 + a1)
                          : "memory");
             __syncwarp();
-            if (lane == 0) atomicAdd(&sy.cnt[g & (kBlkHand - 1)], 1);
+            if (lane == 0) red_release_add(cnt + 4u * (g & (kBlkHand - 1)), 1);
             if (tr) tr[11] = clock64();
             if (++slot == n_slots) {
                 slot = 0;

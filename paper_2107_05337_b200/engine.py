@@ -38,7 +38,7 @@ EXPORTED = [
     "phi_dev_tuning", "phi_dev_trace", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
     "phi_mgrit_gnorm_terms", "phi_mgrit_residual_terms", "phi_mgrit_phase", "phi_mgrit_points",
     "phi_mgrit_stats", "phi_mgrit_residual_iters", "phi_mgrit_wave_levels",
-    "phi_comm_nccl_unique_id", "phi_comm_create_nccl", "phi_comm_create_ops", "phi_comm_free", "phi_mgrit_set_comm",
+    "phi_hier_vcycle_bytes", "phi_comm_nccl_unique_id", "phi_comm_create_nccl", "phi_comm_create_ops", "phi_comm_free", "phi_mgrit_set_comm",
 ]
 
 
@@ -115,6 +115,7 @@ def lib():
         L.phi_hier_unit.argtypes = [_vp, _i, _i, _i, _vp, _i, _vp, _i]
         L.phi_hier_spmm.argtypes = [_vp, _vp, _vp, _i, _i]
         L.phi_hier_time.argtypes = [_vp, _i, _i, _i, _i, _vp]
+        L.phi_hier_vcycle_bytes.argtypes = [_vp, _i, _vp]
         L.phi_stepper_create.argtypes = [_vp, _d, _d, _d, _vp, _vp]
         L.phi_stepper_free.argtypes = [_vp]
         L.phi_stepper_free.restype = None
@@ -320,6 +321,12 @@ class PMultigridHierarchy:
         ms = C.c_double()
         _check(lib().phi_hier_time(self.h, which, nrhs, reps, int(flush_l2), C.byref(ms)))
         return ms.value
+
+    def vcycle_bytes(self, nrhs: int) -> float:
+        """Algorithmic bytes of one V-cycle on nrhs right-hand sides."""
+        v = _d()
+        _check(lib().phi_hier_vcycle_bytes(self.h, nrhs, C.byref(v)))
+        return v.value
 
     def spmv(self, x):
         return self._unit(0, x, self.n)
