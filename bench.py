@@ -337,6 +337,8 @@ def run_c5(args, cfg):
     lib().phi_set_device(local)
     peak, peak_kind = peaks()
     rows = []
+    clocks = ClockSampler(local)
+    clocks.start()
     for p in (2, 3, 4, 5):
         d = P.SpatialDiscretization.build(p, cfg["k"])
         h = P.PMultigridHierarchy(d, cfg["c"])
@@ -350,8 +352,15 @@ def run_c5(args, cfg):
                          "GBs": by / ms / 1e6, "frac": by / ms / 1e6 / peak})
         for b in (1, 16, 64):
             ms = h.time_kernel(1, b, reps=max(2, args.steps))
-            rows.append({"p": p, "B": b, "kernel": "vcycle", "us": ms * 1e3,
-                         "cycles_per_s": b / (ms * 1e-3)})
+            by = h.vcycle_bytes(b)  # SURVEY 8(d) model: operators once per batch + 8 B per vector entry per RHS
+            rows.append({"p": p, "B": b, "kernel": "vcycle", "us": ms * 1e3, "alg_MB": by / 1e6,
+                         "GBs": by / ms / 1e6, "frac": by / ms / 1e6 / peak, "cycles_per_s": b / (ms * 1e-3)})
+    clk = clocks.stop()
+    for r in rows:  # SpMM flops (2 per stored nonzero and right-hand side): past the FP64 ridge at large B
+        if r["kernel"] == "spmm":
+            side = 2 ** cfg["k"] + r["p"] - 2
+            nnz = (side * (2 * r["p"] + 1) - r["p"] * (r["p"] + 1)) ** 2
+            r["fp64_TFLOPs"] = 2.0 * nnz * r["B"] / (r["us"] * 1e-6) / 1e12
     spmm5 = [r for r in rows if r["kernel"] == "spmm" and r["p"] == 5 and r["B"] == 1][0]
     line = {"metric": "SpMV/SpMM HBM GB/s (config 5 kernel microbenchmark)", "value": spmm5["GBs"], "unit": "GB/s",
             "n_gpus": 1, "steps": args.steps, "warmup": 1, "higher_is_better": True, "scaling": "strong",
@@ -360,7 +369,7 @@ def run_c5(args, cfg):
                        "l2": "flushed between repetitions (256 MB read: clean lines, no write-backs in the timed kernel)"},
             "roofline": {"kernel": "spmv_kernel (p=5, B=1)", "bound": "hbm", "achieved": spmm5["GBs"], "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": spmm5["frac"], "traffic": c5_traffic()},
-            "table": rows}
+            "clocks": clk, "table": rows}
     print(json.dumps(line), flush=True)
 
 

@@ -952,12 +952,12 @@ int Mgrit::wave_report(double* ms, double* bytes) {
         }
         const double vmat = H.vcycle_matrix_entries(), vvec = H.vcycle_vector_entries();
         (void)n1;
-        if (std::getenv("PHI_WAVE_DEBUG"))
-            std::fprintf(stderr, "wave %zu level %d: %.3f ms, points %d, cycles sum %d max %d\n", k, recs[k].level,
-                         t, (int)pts, (int)csum, (int)cmax);
         const double mat = nnzA /* A- */ + (1 + cmax) * nnzA + cmax * vmat;
         const double vec = pts * (5 * n + 3 * n) + (pts + csum) * 4 * n + csum * vvec;
         *bytes += 8.0 * (mat + vec);
+        if (std::getenv("PHI_WAVE_DEBUG"))
+            std::fprintf(stderr, "wave %zu level %d: %.3f ms, points %d, cycles sum %d max %d, algorithmic %.4e B\n", k,
+                         recs[k].level, t, (int)pts, (int)csum, (int)cmax, 8.0 * (mat + vec));
     }
     for (auto& r : recs) {
         cudaEventDestroy(r.start);

@@ -892,7 +892,8 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 int cq;
                 double vq;
                 lds_slot(fr + 512u * q, cq, vq);
-                f[q & 7] = __fma_rn(vq, xld<XSM>(xg, xs, cq), f[q & 7]);
+                // a fixed accumulator: an indexed f[] would live in local memory
+                f[0] = __fma_rn(vq, xld<XSM>(xg, xs, cq), f[0]);
             }
             const double t = c - (((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
             if (tr) tr[3] = clock64() + (long long)(t == 1.2345);
