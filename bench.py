@@ -513,12 +513,15 @@ def run_phi(args, cfg, name):
     sol.set_profile(False)
     peak, peak_kind = peaks()
     achieved = wave_bytes / (wave_ms * 1e-3) / 1e9 if wave_ms > 0 else 0.0
-    traffic = None
+    traffic = traffic_note = traffic_alg = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             key = name + ("_cg" if cfg.get("spatial_kind") else "")
-            traffic = json.load(open(tpath)).get(key)  # DRAM bytes of one captured wave launch
+            tj = json.load(open(tpath))
+            traffic = tj.get(key)  # DRAM bytes of one captured wave launch
+            traffic_note = tj.get("_note_" + key) or tj.get("_note")
+            traffic_alg = tj.get(key + "_algorithmic")
         except Exception:
             traffic = None
     # Latency model of the same kernel: the solve is a chain of dependent
@@ -539,7 +542,8 @@ def run_phi(args, cfg, name):
                    "note": "per-cycle time includes the residual checks and the right-hand-side product"}
     roofline = {"kernel": "phi_wave_kernel (fused batched Phi solve)", "bound": "hbm", "achieved": achieved,
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "waves": n_waves, "kernel_ms_per_step": wave_ms,
+                "traffic": traffic, "traffic_launch": traffic_note, "traffic_launch_algorithmic": traffic_alg,
+                "waves": n_waves, "kernel_ms_per_step": wave_ms,
                 "algorithmic_bytes_per_step": wave_bytes,
                 "per_level": per_level, "latency": latency,
                 "note": ("latency-bound, not bandwidth-bound: the serial coarse march runs ILUT block "
