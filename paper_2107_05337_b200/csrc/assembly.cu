@@ -6,8 +6,6 @@
 // Only the unit-square geometry map (identity Jacobian, det = 1) is supported.
 #include <cuda_runtime.h>
 
-#include <algorithm>
-
 #include "phi_kernels.cuh"
 
 namespace phi {
@@ -285,42 +283,27 @@ void launch_stencil_transpose(const DevStencil& a, double* out, cudaStream_t s) 
 // {alpha, f1, f2, f3} = {-a_inline / d, a_prev(-1) / d, a_prev(0) / d,
 // a_prev(+1) / d} (zero outside the grid), then 1 / d.  The in-line entry
 // is W (forward) / E (backward); the previous line is v-1 / v+1.
-// Line Gauss-Seidel coefficients of a 9-point order-1 level, per sweep
-// direction in the line-sweep layout (device_types.cuh line_rm): line q of
-// the sweep, slot r * 32 + lane = position p = lane RM + r of the line, row
-// (v, u) with v = q (forward) or nf - 1 - q, u = p (forward) or nf - 1 - p;
-// padding slots (p >= nf) are zero.  Then 1 / diagonal in natural order.
 __global__ void gs_line_coeffs_kernel(const double* __restrict__ a, int nf, double* out) {
-    const int n = nf * nf, rm = line_rm(nf), len = line_len(nf);
-    const size_t per_dir = (size_t)nf * len;
+    const int n = nf * nf;
     double4* fw = reinterpret_cast<double4*>(out);
-    double4* bw = fw + per_dir;
-    double* rd = out + 8 * per_dir;
-    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < 2 * per_dir; t += (size_t)gridDim.x * blockDim.x) {
-        const bool back = t >= per_dir;
-        const size_t k = back ? t - per_dir : t;
-        const int q = (int)(k / len), slot = (int)(k % len);
-        const int r = slot / 32, lane = slot % 32, p = lane * rm + r;
-        double4 c = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (p < nf) {
-            const int iv = back ? nf - 1 - q : q, iu = back ? nf - 1 - p : p;
-            const int i = iv * nf + iu;
-            auto at = [&](int dv, int du) -> double {
-                const int u = iu + du, v = iv + dv;
-                return (u >= 0 && u < nf && v >= 0 && v < nf) ? a[(size_t)((dv + 1) * 3 + (du + 1)) * n + i] : 0.0;
-            };
-            const double r1 = 1.0 / at(0, 0);
-            c = back ? make_double4(-at(0, 1) * r1, at(1, -1) * r1, at(1, 0) * r1, at(1, 1) * r1)
-                     : make_double4(-at(0, -1) * r1, at(-1, -1) * r1, at(-1, 0) * r1, at(-1, 1) * r1);
-            if (!back) rd[i] = r1;
-        }
-        (back ? bw : fw)[k] = c;
+    double4* bw = fw + n;
+    double* rd = out + 8 * (size_t)n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int iv = i / nf, iu = i - iv * nf;
+        auto at = [&](int dv, int du) -> double {
+            const int u = iu + du, v = iv + dv;
+            return (u >= 0 && u < nf && v >= 0 && v < nf) ? a[(size_t)((dv + 1) * 3 + (du + 1)) * n + i] : 0.0;
+        };
+        const double d = at(0, 0), r = 1.0 / d;
+        fw[i] = make_double4(-at(0, -1) * r, at(-1, -1) * r, at(-1, 0) * r, at(-1, 1) * r);
+        bw[i] = make_double4(-at(0, 1) * r, at(1, -1) * r, at(1, 0) * r, at(1, 1) * r);
+        rd[i] = r;
     }
 }
 
 void launch_gs_line_coeffs(const double* a, int nf, double* out, cudaStream_t s) {
-    const size_t total = 2 * (size_t)nf * line_len(nf);
-    gs_line_coeffs_kernel<<<(int)std::min<size_t>((total + 255) / 256, 4096), 256, 0, s>>>(a, nf, out);
+    const int n = nf * nf;
+    gs_line_coeffs_kernel<<<(n + 255) / 256, 256, 0, s>>>(a, nf, out);
     PHI_CUDA(cudaGetLastError());
 }
 

@@ -65,9 +65,8 @@ struct DevHLevel {
     DevStencil a;    // M_l + c K_l, 9-point
     DevTri gs_fwd, gs_bwd;  // Gauss-Seidel sweeps as level-scheduled streams (exact mode; empty on the coarsest)
     DevBlk gsb_fwd, gsb_bwd;  // the same sweeps as block recurrences (reassociated mode)
-    // reassociated mode, kLineMin <= nf <= kLineMax: line sweeps
-    // (gs_line_coeffs_kernel layout: double4 forward[nf][32 RM] and
-    // backward[nf][32 RM], lines in sweep order, then double rd[n]); null: none
+    // reassociated mode, nf <= kLineMax: line sweeps (gs_line_coeffs_kernel
+    // layout: double4 forward[n], double4 backward[n], double rd[n]); null: none
     const double* gsl;
     int nf;
     DevCsr embed;    // level l+1 -> level l (empty on the coarsest)
@@ -82,26 +81,6 @@ constexpr int kClScratch = 1024 + 160;
 constexpr int kLineMax = 256;
 /// Shortest grid line swept by lines (shorter levels: block sweeps).
 constexpr int kLineMin = 24;
-/// Line sweeps: rows per lane (a power of two, <= 8) for a line of nf points,
-/// and the padded line length 32 RM.  A line's coefficients and its prologue
-/// values o are stored line by line in SWEEP order, slot (r, lane) = the
-/// line's position p = lane RM + r, so a warp reads one line contiguously.
-__host__ __device__ constexpr int line_rm(int nf) {
-    return nf <= 32 ? 1 : (nf <= 64 ? 2 : (nf <= 128 ? 4 : 8));
-}
-__host__ __device__ constexpr int line_len(int nf) { return 32 * line_rm(nf); }
-/// Line-sweep staging ring: lines fetched ahead of the chain by TMA.
-constexpr int kLineSlots = 4;
-/// Doubles of one h-level's vectors, each 16-byte aligned (even offsets):
-/// b (n), x (n + 1, the zero slot x[n]), then r -- also the line sweeps'
-/// permuted o (nf lines of 32 RM, a TMA source).
-__host__ __device__ constexpr size_t even_up(size_t v) { return (v + 1) & ~size_t(1); }
-__host__ __device__ constexpr size_t level_x_off(int n) { return even_up((size_t)n); }
-__host__ __device__ constexpr size_t level_r_off(int n) { return even_up((size_t)n) + even_up((size_t)n + 1); }
-__host__ __device__ constexpr size_t level_doubles(int n, int nf) {
-    return level_r_off(n) +
-           even_up((size_t)nf * line_len(nf) > (size_t)n ? (size_t)nf * line_len(nf) : (size_t)n);
-}
 
 /// One p-multigrid hierarchy (PMultigridHierarchy, pmultigrid.hpp:215-324)
 /// plus the spatial solver settings of its ThetaStepper (theta.hpp:66-75).

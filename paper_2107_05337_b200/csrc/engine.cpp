@@ -293,7 +293,7 @@ Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_
         }
         gsl_dev.emplace_back();
         if (!opt.exact && d.h[l].nf <= kLineMax && d.h[l].nf >= kLineMin) {
-            gsl_dev.back().alloc((size_t)8 * d.h[l].nf * line_len(d.h[l].nf) + d.h[l].n);
+            gsl_dev.back().alloc((size_t)9 * d.h[l].n);
             launch_gs_line_coeffs(a_h[l].vals.get(), d.h[l].nf, gsl_dev.back().get(), s);
         }
     }

@@ -240,9 +240,9 @@ __device__ Ws carve(double* base, const DevHier& H, const SmemPlan& P, double* s
         w.lvl_off[l] = P.lvl_off[l];
         double* s = P.lvl_off[l] >= 0 ? smem + P.lvl_off[l] : g;
         w.hb[l] = s;
-        w.hx[l] = s + level_x_off(nl);  // x has a zero slot x[n] (padded sweep entries)
-        w.hr[l] = s + level_r_off(nl);  // 16-byte aligned (the line sweeps' o is a TMA source)
-        g += level_doubles(nl, H.h[l].nf);
+        w.hx[l] = s + nl;
+        w.hr[l] = s + 2 * (size_t)nl + 1;  // x has a zero slot x[n] (padded sweep entries)
+        g += 3 * (size_t)nl + 1;
     }
     w.zc = cl_main(w.z);
     if (H.n_h == 0) return w;  // CG kind: no hierarchy
@@ -758,8 +758,6 @@ struct __align__(16) BlkSync {
     int phase[kBlkMaxSlots];  // phases completed per slot since the kernel started
     int cnt[kBlkHand];
     int prog;
-    unsigned long long lbar[kLineSlots];  // line-sweep staging ring (gs_line_sweeps_t)
-    int lphase[kLineSlots];               // its phases completed per slot
 };
 // One per CTA.  The ring's mbarriers are initialised once per kernel
 // (blk_init) and never re-initialised: every sweep continues their phase
@@ -774,11 +772,6 @@ __device__ __forceinline__ void blk_init() {
             g_blk.phase[k] = 0;
         }
         for (int k = 0; k < kBlkHand; ++k) g_blk.cnt[k] = 0;
-        const unsigned lbar = sh_addr(g_blk.lbar);
-        for (int k = 0; k < kLineSlots; ++k) {
-            mbar_init(lbar + 8u * k);
-            g_blk.lphase[k] = 0;
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // the callers' next __syncthreads() publishes the initialisation
@@ -1219,38 +1212,33 @@ __device__ void coarse_solve(const DevHier& H, const double* b, double* x) {
 // lines (reassociated mode; solvers.hpp:80-99 restated per line).  For a
 // forward sweep the row (iu, v) reads new values of its west neighbour and of
 // line v-1, old values of its east neighbour and of line v+1:
-//   1. prologue, all threads: o_i = (b_i - sum_old a_ij x_j) / d_i, written
-//      in the line layout (device_types.cuh line_rm: lines in sweep order,
-//      slot r * 32 + lane = position lane RM + r);
+//   1. prologue, all threads: o_i = (b_i - sum_old a_ij x_j) / d_i;
 //   2. warp 0, line by line: beta_i = o_i - sum_{prev line} (a_ij / d_i) x_j,
 //      then the in-line recurrence x_i = beta_i + alpha_i x_{i-1} (alpha =
-//      -a_W / d) as a warp scan of affine maps (RM rows per lane, composed
-//      locally first).  Every line's coefficients (and its o when o is in
-//      global memory) arrive in a shared-memory ring by TMA bulk copies,
-//      kLineSlots lines ahead of the chain: the chain reads shared memory only.
+//      -a_W / d) as a warp scan of affine maps (R = ceil(nf / 32) rows per
+//      lane, composed locally first).  The next line's o and coefficients are
+//      loaded while the current line is solved.
 // A backward sweep mirrors both orders (lines v descending, iu descending).
 template <bool SM, int RM>
 __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double* b, double* x, double* o,
                                               const double* bc, const double* xc, double* oc, bool backward,
-                                              int count, int ring_off) {
+                                              int count) {
     // cluster mode: the prologue is split over the cluster (bc, xc, oc: the
     // main CTA's vectors as the cluster sees them), the chain runs on the
     // main CTA; without clusters part = 0, parts = 1 and bc = b, ...
     const int part = cl_rank(), parts = cl_size();
     // SM: x and o in shared memory (explicit shared accesses on the chain)
     const unsigned xs = SM ? sh_addr(x) : 0u, os = SM ? sh_addr(o) : 0u;
+    auto ldx = [&](int j) -> double { return SM ? vlds_f64(xs + 8u * j) : x[j]; };
+    // RM: rows per lane (compile time), R = RM
     const int nf = lv.nf, n = nf * nf;
-    constexpr int R = RM, L = 32 * RM;
+    constexpr int R = RM;
     const double* __restrict__ a = lv.a.vals;
-    const double4* __restrict__ cf = reinterpret_cast<const double4*>(lv.gsl) + (backward ? (size_t)nf * L : 0);
-    const double* __restrict__ rd = lv.gsl + 8 * (size_t)nf * L;
+    const double4* __restrict__ cf = reinterpret_cast<const double4*>(lv.gsl) + (backward ? n : 0);
+    const double* __restrict__ rd = lv.gsl + 8 * (size_t)n;
     const int sv = backward ? 1 : -1;  // the previous line in sweep order is v + sv
-    // staging ring: per slot the line's coefficients (L double4), then its o (L doubles, global o only)
-    constexpr unsigned kCoefBytes = 32u * L, kOBytes = SM ? 0u : 8u * L, kSlotBytes = kCoefBytes + kOBytes;
-    const unsigned ring = sh_addr(g_smem + ring_off);
-    const unsigned lbar = sh_addr(g_blk.lbar);
     for (int c = 0; c < count; ++c) {
-        // ---- 1. old part, scaled by 1/d, into the line layout
+        // ---- 1. old part, scaled by 1/d
         constexpr int U = 4;  // rows per thread and pass: independent loads in flight
         for (int i0 = threadIdx.x + part * U * NT; i0 < n; i0 += U * NT * parts) {
             double acc[U], sc[U];
@@ -1275,42 +1263,33 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                 sc[uu] = rd[i];
             }
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu) {
-                const int i = i0 + uu * NT;
-                if (i < n) {
-                    const int iv = i / nf, iu = i - iv * nf;
-                    const int q = backward ? nf - 1 - iv : iv, p = backward ? nf - 1 - iu : iu;
-                    oc[(size_t)q * L + (p % R) * 32 + p / R] = acc[uu] * sc[uu];
-                }
-            }
+            for (int uu = 0; uu < U; ++uu)
+                if (i0 + uu * NT < n) oc[i0 + uu * NT] = acc[uu] * sc[uu];
         }
         cl_sync();
         // ---- 2. the line chain
         if (threadIdx.x < 32 && part == 0) {
             const int lane = threadIdx.x;
-            auto fetch = [&](int q) {  // lane 0: line q into its ring slot
-                const int slot = q % kLineSlots;
-                const unsigned dst = ring + slot * kSlotBytes, bar = lbar + 8u * slot;
-                // order the slot's generic reads (and o's generic writes) before the async-proxy copy
-                asm volatile("fence.proxy.async;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kSlotBytes)
-                             : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                    "l"(cf + (size_t)q * L), "r"(kCoefBytes), "r"(bar)
-                    : "memory");
-                if (!SM)
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            dst + kCoefBytes),
-                        "l"(o + (size_t)q * L), "r"(kOBytes), "r"(bar)
-                        : "memory");
-            };
-            int ph[kLineSlots];  // phases completed per slot before this sweep
+            double on[RM];
+            double4 cn[RM];
+            auto load_line = [&](int q) {
+                const int v = backward ? nf - 1 - q : q;
 #pragma unroll
-            for (int k = 0; k < kLineSlots; ++k) ph[k] = g_blk.lphase[k];
-            if (lane == 0)
-                for (int q = 0; q < kLineSlots && q < nf; ++q) fetch(q);
+                for (int r = 0; r < RM; ++r) {
+                    const int p = lane * R + r;
+                    if (p < nf) {
+                        const int i = v * nf + (backward ? nf - 1 - p : p);
+                        on[r] = SM ? vlds_f64(os + 8u * i) : o[i];
+                        const double2* c2 = reinterpret_cast<const double2*>(cf + i);
+                        const double2 lo = __ldg(c2), hi = __ldg(c2 + 1);
+                        cn[r] = make_double4(lo.x, lo.y, hi.x, hi.y);
+                    } else {
+                        on[r] = 0.0;
+                        cn[r] = make_double4(0.0, 0.0, 0.0, 0.0);
+                    }
+                }
+            };
+            load_line(0);
             double xp[RM];  // the previous line's new values (sweep order); none before line 0
 #pragma unroll
             for (int r = 0; r < RM; ++r) xp[r] = 0.0;
@@ -1319,22 +1298,15 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                                     ? c_tune.trace + kTriTraceBase + 8 * q
                                     : nullptr;
                 if (tr) tr[0] = clock64();
-                const int slot = q % kLineSlots;
-                mbar_wait(lbar + 8u * slot, (unsigned)(ph[slot] + q / kLineSlots) & 1u);
-                const unsigned cs = ring + slot * kSlotBytes;
-                const int v = backward ? nf - 1 - q : q;
-                double oc_[RM];
+                const int v = backward ? nf - 1 - q : q, vp = v + sv;
+                double oc[RM];
                 double4 cc[RM];
 #pragma unroll
                 for (int r = 0; r < RM; ++r) {
-                    const unsigned e = (unsigned)(r * 32 + lane);
-                    double c0, c1, c2, c3;
-                    lds_v2f64(cs + 32u * e, c0, c1);
-                    lds_v2f64(cs + 32u * e + 16u, c2, c3);
-                    cc[r] = make_double4(c0, c1, c2, c3);
-                    const bool in = lane * R + r < nf;
-                    oc_[r] = !in ? 0.0 : (SM ? vlds_f64(os + 8u * ((unsigned)q * L + e)) : vlds_f64(cs + kCoefBytes + 8u * e));
+                    oc[r] = on[r];
+                    cc[r] = cn[r];
                 }
+                if (q + 1 < nf) load_line(q + 1);
                 // beta: fresh entries of the previous line, whose values this
                 // warp holds in registers (xp, sweep order); the neighbours
                 // across a lane boundary come by shuffle; positions outside
@@ -1348,13 +1320,10 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                     const double xr = r + 1 < RM ? xp[r + 1] : (lane < 31 ? rgt : 0.0);
                     // coefficients in natural order: iu-1, iu, iu+1
                     const double xm = backward ? xr : xl, xq = backward ? xl : xr;
-                    bl[r] = oc_[r] - ((cc[r].y * xm + cc[r].z * xp[r]) + cc[r].w * xq);
+                    bl[r] = oc[r] - ((cc[r].y * xm + cc[r].z * xp[r]) + cc[r].w * xq);
                     al[r] = cc[r].x;
                 }
                 if (tr) tr[1] = clock64() + (long long)(bl[0] == 1.2345) + (long long)(al[0] == 1.5);
-                // the slot's data is in registers: refill it with line q + kLineSlots
-                __syncwarp();
-                if (lane == 0 && q + kLineSlots < nf) fetch(q + kLineSlots);
                 // in-line recurrence: compose the lane's rows, scan the lanes
                 double B = bl[0], A = al[0];
 #pragma unroll
@@ -1392,11 +1361,6 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
                 __syncwarp();
                 if (tr) tr[3] = clock64();
             }
-            // phases delivered per slot in this sweep
-            if (lane == 0)
-                for (int k = 0; k < kLineSlots; ++k)
-                    g_blk.lphase[k] = ph[k] + (k < nf ? (nf - 1 - k) / kLineSlots + 1 : 0);
-            __syncwarp();
         }
         cl_sync();
     }
@@ -1405,23 +1369,25 @@ __device__ __noinline__ void gs_line_sweeps_t(const DevHLevel& lv, const double*
 template <int RM>
 __device__ __forceinline__ void gs_line_sweeps_r(const DevHLevel& lv, const double* b, double* x, double* o,
                                                  const double* bc, const double* xc, double* oc, bool backward,
-                                                 int count, int ring_off) {
+                                                 int count) {
     if (__isShared(x) && __isShared(o))
-        gs_line_sweeps_t<true, RM>(lv, b, x, o, bc, xc, oc, backward, count, ring_off);
+        gs_line_sweeps_t<true, RM>(lv, b, x, o, bc, xc, oc, backward, count);
     else
-        gs_line_sweeps_t<false, RM>(lv, b, x, o, bc, xc, oc, backward, count, ring_off);
+        gs_line_sweeps_t<false, RM>(lv, b, x, o, bc, xc, oc, backward, count);
 }
 // Called by every CTA of the cluster (by the CTA alone without clusters).
-// ring_off: the staging ring (SmemPlan: the Gauss-Seidel ring region).
 __device__ __forceinline__ void gs_line_sweeps(const DevHLevel& lv, const double* b, double* x, double* o,
                                                const double* bc, const double* xc, double* oc, bool backward,
-                                               int count, int ring_off) {
-    switch (line_rm(lv.nf)) {
-        case 1: gs_line_sweeps_r<1>(lv, b, x, o, bc, xc, oc, backward, count, ring_off); break;
-        case 2: gs_line_sweeps_r<2>(lv, b, x, o, bc, xc, oc, backward, count, ring_off); break;
-        case 4: gs_line_sweeps_r<4>(lv, b, x, o, bc, xc, oc, backward, count, ring_off); break;
-        default: gs_line_sweeps_r<8>(lv, b, x, o, bc, xc, oc, backward, count, ring_off); break;
-    }
+                                               int count) {
+    const int r = (lv.nf + 31) / 32;
+    if (r <= 1)
+        gs_line_sweeps_r<1>(lv, b, x, o, bc, xc, oc, backward, count);
+    else if (r <= 2)
+        gs_line_sweeps_r<2>(lv, b, x, o, bc, xc, oc, backward, count);
+    else if (r <= 4)
+        gs_line_sweeps_r<4>(lv, b, x, o, bc, xc, oc, backward, count);
+    else
+        gs_line_sweeps_r<8>(lv, b, x, o, bc, xc, oc, backward, count);
 }
 
 // x += C r for a dense column-major n x n operator (the collapsed coarse
@@ -1551,11 +1517,11 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
         const DevHLevel& lv = H.h[l];
         double* b = w.hb[l];
         double* x = w.hx[l];
-        const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + (int)level_x_off(lv.n) : -1;
+        const int bo = w.lvl_off[l], xo = bo >= 0 ? bo + lv.n : -1;
         if (phase[l] == 0) {
             mark(23);
             if (!H.exact && lv.gsl) {  // every CTA: the prologues are split over the cluster
-                gs_line_sweeps(lv, b, x, w.hr[l], w.hbc[l], w.hxc[l], w.hrc[l], false, H.gs_pre, w.ring_off);
+                gs_line_sweeps(lv, b, x, w.hr[l], w.hbc[l], w.hxc[l], w.hrc[l], false, H.gs_pre);
             } else {
                 if (main) {
                     if (H.exact)
@@ -1583,7 +1549,7 @@ __device__ __noinline__ void wcycle(const DevHier& H, const Ws& w) {
             cl_sync();
             mark(21);
             if (!H.exact && lv.gsl) {
-                gs_line_sweeps(lv, b, x, w.hr[l], w.hbc[l], w.hxc[l], w.hrc[l], true, H.gs_post, w.ring_off);
+                gs_line_sweeps(lv, b, x, w.hr[l], w.hbc[l], w.hxc[l], w.hrc[l], true, H.gs_post);
             } else {
                 if (main) {
                     if (H.exact)
@@ -1933,12 +1899,11 @@ __global__ void __launch_bounds__(NT, 1)
         __syncthreads();
         if (threadIdx.x == 0) w.hx[arg][lv.n] = 0.0;  // neutral slot of padded sweep entries
         __syncthreads();
-        const int bo = w.lvl_off[arg], xo = bo >= 0 ? bo + (int)level_x_off(lv.n) : -1;
+        const int bo = w.lvl_off[arg], xo = bo >= 0 ? bo + lv.n : -1;
         if (H.exact)
             gs_sweeps(lv, w.hb[arg], w.hx[arg], arg2 != 0, 1, true, xo, bo, w.ring_off, w.slot_bytes, w.prod_off);
         else if (lv.gsl)
-            gs_line_sweeps(lv, w.hb[arg], w.hx[arg], w.hr[arg], w.hb[arg], w.hx[arg], w.hr[arg], arg2 != 0, 1,
-                           w.ring_off);
+            gs_line_sweeps(lv, w.hb[arg], w.hx[arg], w.hr[arg], w.hb[arg], w.hx[arg], w.hr[arg], arg2 != 0, 1);
         else
             blk_sweep(arg2 ? lv.gsb_bwd : lv.gsb_fwd, 1, w.hx[arg], xo, w.hb[arg], bo, w.ring_off, w.gs_slot_bytes,
                       w.gs_n_slots);

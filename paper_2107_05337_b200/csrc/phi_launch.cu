@@ -80,7 +80,7 @@ __global__ void copy_kernel(double* dst, const double* src, size_t n) {
 // ---------------------------------------------------------------------------
 size_t phi_ws_doubles(const DevHier& H) {
     size_t s = 6 * ((size_t)H.n_p + 2);
-    for (int l = 0; l < H.n_h; ++l) s += level_doubles(H.h[l].n, H.h[l].nf);
+    for (int l = 0; l < H.n_h; ++l) s += 3 * (size_t)H.h[l].n + 1;
     return (s + 31) & ~size_t(31);
 }
 
@@ -137,12 +137,6 @@ SmemPlan phi_smem_plan(const DevHier& H) {
         tri = (size_t)ns * P.slot_bytes / 8;
         P.gs_n_slots = std::min(kBlkMaxSlots, 6);
         gs_tri = (size_t)P.gs_n_slots * P.gs_slot_bytes / 8;
-        // the line sweeps stage their lines in the same region (not concurrently)
-        for (int l = 0; l + 1 < H.n_h; ++l)
-            if (H.h[l].gsl) {
-                const size_t lb = (size_t)kLineSlots * line_len(H.h[l].nf) * 40;  // 32 B coefficients + 8 B o
-                gs_tri = std::max(gs_tri, lb / 8);
-            }
     }
     size_t top = std::max(tri, gs_tri);
     if (!H.exact && std::max(H.Lb.win, H.Ub.win) > 0) {  // z global, its window after the ring
@@ -158,7 +152,7 @@ SmemPlan phi_smem_plan(const DevHier& H) {
     // coarsest levels first: they are visited most often by the W-cycle
     size_t lv = gs_tri;
     for (int l = H.n_h - 1; l >= 0; --l) {
-        const size_t need = level_doubles(H.h[l].n, H.h[l].nf);
+        const size_t need = 3 * (size_t)H.h[l].n + 1;
         if (lv + need <= budget) {
             P.lvl_off[l] = (int)lv;
             lv += need;
