@@ -24,7 +24,7 @@ INIT_ZERO, INIT_SIN, INIT_COEFFS = 0, 1, 2
 CYCLE_V, CYCLE_F, CYCLE_TWO_LEVEL = 0, 1, 2
 RELAX_F, RELAX_FCF = 0, 1
 
-# every symbol include/phi_engine.h declares (checked by tests/test_capi_symbols.py)
+# every symbol include/phi_engine.h declares (checked by tests/test_capi_cpu.py)
 EXPORTED = [
     "phi_last_error", "phi_default_solver_config", "phi_default_mgrit_config", "phi_default_problem",
     "phi_device_count", "phi_set_device", "phi_synchronize", "phi_disc_build", "phi_disc_free",
