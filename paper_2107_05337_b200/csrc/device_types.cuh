@@ -179,6 +179,11 @@ struct WaveArgs {
     int* err;                  // [0] flag, [1] first k, [2] level
     double* err_rel;
     int level;
+    // overlap of the coarse march with the next phases (Mgrit::coarse_overlapped):
+    // after every completed task step the main CTA publishes the time index k
+    // just finished to this host-mapped counter (null: none)
+    volatile unsigned* progress;
+    int no_cluster;  // 1: one CTA per task even for few tasks (the side-stream waves)
 };
 
 }  // namespace phi

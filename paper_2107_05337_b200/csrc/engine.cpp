@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <string>
+#include <thread>
+#include <chrono>
 
 namespace phi {
 
@@ -495,6 +497,7 @@ Mgrit::Mgrit(std::shared_ptr<const Disc> disc_, const ProblemOptions& ps_, const
     err_rel.alloc(1);
     u0.alloc(disc->n_p);
     for (auto& lv : levels) ws.ensure(lv.stepper->H);
+    if (const char* e = std::getenv("PHI_OVERLAP")) overlap = std::atoi(e) != 0;
     PHI_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -613,8 +616,11 @@ void Mgrit::project_initial() {
     if (r[0] != 1) throw std::runtime_error("project_initial: mass solve did not converge");
 }
 
-void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, double* CG, double* CU) {
+void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, double* CG, double* CU,
+                 const Route* route) {
     Level& lv = levels[l];
+    const cudaStream_t st = route ? route->s : stream;
+    Workspace& wsp = route && route->w ? *route->w : ws;
     WaveArgs a{};
     a.mode = mode;
     a.epi = epi;
@@ -636,6 +642,8 @@ void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, 
     a.level = l;
     a.x0_empty = mode == kModeSolve ? 1 : 0;  // g-norm solves start from zero (mgrit.hpp:301)
     a.iters_out = iters_dev;
+    a.progress = route ? route->progress : nullptr;
+    a.no_cluster = route && route->no_cluster ? 1 : 0;
     const bool rec = profile && recs.size() * 3 < wstats.size();
     if (rec) {
         WaveRec r{};
@@ -643,12 +651,88 @@ void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, 
         PHI_CUDA(cudaEventCreate(&r.start));
         PHI_CUDA(cudaEventCreate(&r.stop));
         a.wave_max = wstats.get() + 3 * recs.size();
-        PHI_CUDA(cudaEventRecord(r.start, stream));
+        PHI_CUDA(cudaEventRecord(r.start, st));
         recs.push_back(r);
     }
-    launch_phi_wave(lv.stepper->H, lv.stepper->Aminus.view(), a, ws.buf.get(), ws.stride, ws.slots, stream);
-    if (rec) PHI_CUDA(cudaEventRecord(recs.back().stop, stream));
+    launch_phi_wave(lv.stepper->H, lv.stepper->Aminus.view(), a, wsp.buf.get(), wsp.stride, wsp.slots, st);
+    if (rec) PHI_CUDA(cudaEventRecord(recs.back().stop, st));
     ++launches;
+}
+
+Mgrit::~Mgrit() {
+    if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+    }
+    if (ev_pre) cudaEventDestroy(ev_pre);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (prog_host) cudaFreeHost(prog_host);
+}
+
+void Mgrit::coarse_overlapped(int lc, bool residual) {
+    const int lf = lc - 1;
+    Level& c = levels[lc];
+    Level& f = levels[lf];
+    const int n = disc->n_p, m = cfg.m, J = f.steps / m;
+    if (!side) {
+        int lo = 0, hi = 0;
+        PHI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        PHI_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+        PHI_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
+        PHI_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        PHI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&prog_host), sizeof(unsigned), cudaHostAllocMapped));
+        PHI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&prog_dev), prog_host, 0));
+        for (auto& lv : levels) ws_side.ensure(lv.stepper->H);
+    }
+    volatile unsigned* prog = prog_host;
+    *prog = 0u;
+    // the coarse march (coarsest_solve, mgrit.hpp:188-194), publishing its progress
+    launch_copy(c.u.get(), c.g.get(), n, stream);
+    ++launches;
+    PHI_CUDA(cudaEventRecord(ev_pre, stream));  // everything the fine-level work depends on
+    const Route coarse{stream, nullptr, false, prog_dev};
+    wave(lc, kModeStep, kEpiStore, 1, c.kAll.get(), c.steps, nullptr, nullptr, &coarse);
+    // the fine-level work, interval by interval as the coarse points land:
+    // injection (mgrit.hpp:172-180), F-relaxation, and (residual) the terms
+    // of residual_norm(0) (mgrit.hpp:197-214), on the side stream
+    PHI_CUDA(cudaStreamWaitEvent(side, ev_pre, 0));
+    const Route sr{side, &ws_side, true, nullptr};
+    if (residual) PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (f.steps + 1), side));
+    const int chunk = std::max(1, J / 16);
+    int injected = 0, done = 0;  // C-points injected, intervals relaxed
+    while (done < J) {
+        // coarse points 0..p are final (coarse point 0 is g[0], copied before the march)
+        const unsigned pv = *prog;
+        const int p = (int)std::min<unsigned>(pv, (unsigned)J);
+        const int ready = p;  // interval j needs coarse points j and j + 1
+        if (ready - done >= chunk || (p >= J && ready > done)) {
+            launch_inject_range(c.u.get(), f.u.get(), n, injected, p + 1, m, side);
+            ++launches;
+            if (residual && injected == 0) {  // point 0 after its injection
+                launch_resid0(f.g.get(), f.u.get(), sq.get(), n, side);
+                ++launches;
+            }
+            injected = p + 1;
+            wave(lf, kModeStep, kEpiStore, ready - done, f.kF.get() + done, m - 1, nullptr, nullptr, &sr);
+            if (residual)
+                wave(lf, kModeStep, kEpiResid, (ready - done) * m, f.kAll.get() + done * m, 1, nullptr, nullptr, &sr);
+            done = ready;
+            continue;
+        }
+        // poll: the march publishes after every coarse step
+        if (cudaStreamQuery(stream) == cudaErrorNotReady) {
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        } else {
+            PHI_CUDA(cudaGetLastError());
+            if (*prog < (unsigned)J) {  // the march ended without finishing (an error): drain
+                PHI_CUDA(cudaStreamSynchronize(stream));
+                *prog = (unsigned)J;
+            }
+        }
+    }
+    PHI_CUDA(cudaEventRecord(ev_join, side));
+    PHI_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+    sq_ready = residual;
 }
 
 void Mgrit::check_errors() {
@@ -722,12 +806,28 @@ void Mgrit::cycle_impl(int l, bool f_schedule) {
         f_relax(l, false);
     }
     restrict_residual(l);
-    cycle_impl(l + 1, f_schedule);
-    interpolate_and_correct(l);
-    if (f_schedule && l + 2 < n_levels()) cycle_impl(l, false);
+    const bool second_pass = f_schedule && l + 2 < n_levels();
+    // (only where the interpolation wave has enough intervals to run one CTA
+    // per interval anyway -- the overlapped waves always do, so the results
+    // stay bit-identical to the serial phases)
+    if (l + 2 == n_levels() && overlap && !comm && !scfg.pmg.exact && j_hi < 0 &&
+        levels[l].steps / cfg.m >= kOverlapMinIntervals) {
+        // the coarse march overlapped with this level's interpolation (and,
+        // at the top of a cycle, with the residual terms residual_norm reads)
+        coarse_overlapped(l + 1, l == 0 && top_cycle && !second_pass);
+    } else {
+        cycle_impl(l + 1, f_schedule);
+        interpolate_and_correct(l);
+    }
+    if (second_pass) cycle_impl(l, false);
 }
 
-void Mgrit::mgrit_cycle(int l) { cycle_impl(l, cfg.cycle == 1); }
+void Mgrit::mgrit_cycle(int l) {
+    sq_ready = false;
+    top_cycle = l == 0;
+    cycle_impl(l, cfg.cycle == 1);
+    top_cycle = false;
+}
 
 double Mgrit::residual_norm(int l) {
     std::vector<double> h(levels[l].steps + 1);
@@ -741,6 +841,14 @@ void Mgrit::residual_terms(int l, double* host) {
     Level& lv = levels[l];
     const int n = disc->n_p;
     const int lo = range_lo(l), hi = range_hi(l);
+    if (l == 0 && sq_ready && !iters_dev) {  // computed alongside the coarse march (coarse_overlapped)
+        sq_ready = false;
+        PHI_CUDA(cudaMemcpyAsync(host, sq.get(), sizeof(double) * (lv.steps + 1), cudaMemcpyDeviceToHost, stream));
+        PHI_CUDA(cudaStreamSynchronize(stream));
+        check_errors();
+        return;
+    }
+    sq_ready = false;
     PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (lv.steps + 1), stream));
     if (lo == 0) {  // point 0 belongs to the first rank
         launch_resid0(lv.g.get(), lv.u.get(), sq.get(), n, stream);

@@ -167,6 +167,10 @@ public:
     DevHier H;
 };
 
+/// Fewest coarse intervals of a level for which the coarse march is overlapped
+/// with that level's interpolation (Mgrit::coarse_overlapped).
+constexpr int kOverlapMinIntervals = 32;
+
 struct MgritOptions {  // MgritConfig (mgrit.hpp:17-31)
     int cycle = 0;  // 0 V, 1 F, 2 two-level
     int relax = 1;  // 0 F, 1 FCF
@@ -259,6 +263,16 @@ public:
     double g_norm = 0.0;
     long long launches = 0;  // kernels launched by the solve (bench evidence)
     int* iters_dev = nullptr;  // per-task iteration counts of the next waves (nullable)
+    // overlap of the coarse march with interpolation / residual (coarse_overlapped)
+    bool overlap = true;        // PHI_OVERLAP=0 disables
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_pre = nullptr, ev_join = nullptr;
+    unsigned* prog_host = nullptr;  // host-mapped progress counter of the coarse march
+    unsigned* prog_dev = nullptr;
+    Workspace ws_side;
+    bool sq_ready = false;      // level-0 residual terms of the current state are in `sq`
+    bool top_cycle = false;     // inside mgrit_cycle(0)
+    ~Mgrit();
 
     // Optional per-launch profile of the Phi waves (CUDA events on the engine
     // stream + device counters of p-MG cycles), for the bench's roofline.
@@ -283,8 +297,21 @@ private:
     void build_loads();
     void project_initial();
     double compute_g_norm();
+    /// where a wave runs: stream, workspace, one CTA per task, progress counter
+    struct Route {
+        cudaStream_t s;
+        Workspace* w;
+        bool no_cluster;
+        volatile unsigned* progress;
+    };
     void wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, double* CG = nullptr,
-              double* CU = nullptr);
+              double* CU = nullptr, const Route* route = nullptr);
+    /// coarsest_solve(lc) + interpolate_and_correct(lc - 1) (+ the level-0
+    /// residual terms when `residual`), with the fine-level work of every
+    /// interval issued on a side stream as soon as the coarse march has
+    /// published both of its C-points: the same operations per point as the
+    /// serial phases (bit-identical results), overlapped with the march.
+    void coarse_overlapped(int lc, bool residual);
     void check_errors();
     int range_lo(int l) const { return l == 0 ? j_lo : 0; }
     int range_hi(int l) const;

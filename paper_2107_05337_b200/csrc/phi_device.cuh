@@ -1831,6 +1831,12 @@ __global__ void __launch_bounds__(NT, 1)
         for (int s = 0; s < a.task_len; ++s) {
             const int k = a.task_k0 ? a.task_k0[task] + s : task;
             phi_point<DEG>(H, Am, a, w, task, k, sh);
+            // phi_point ends with a cluster barrier: every CTA's stores of
+            // point k are done; publish k to the host system-wide
+            if (a.progress && threadIdx.x == 0 && cl_rank() == 0) {
+                __threadfence_system();
+                *a.progress = (unsigned)k;
+            }
         }
     }
 }
@@ -2046,7 +2052,7 @@ void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs
     int n_sm = 0, dev = 0;
     PHI_CUDA(cudaGetDevice(&dev));
     PHI_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    if (!H.exact && cl > 1 && a.n_tasks * cl <= n_sm) {
+    if (!H.exact && !a.no_cluster && cl > 1 && a.n_tasks * cl <= n_sm) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(a.n_tasks * cl));
         cfg.blockDim = dim3(NT);

@@ -62,6 +62,8 @@ void launch_cg(const DevStencil& A, const double* diag, const double* b, double*
 void launch_restrict_first(const double* fg, const double* fu, double* cg, double* cu, int n,
                            cudaStream_t s);
 void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s);
+/// the same for the C-points j0 <= j < j1
+void launch_inject_range(const double* cu, double* fu, int n, int j0, int j1, int m, cudaStream_t s);
 void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s);
 /// Reads n doubles (a multiple of 4, > L2): flushes L2 leaving clean lines.
 void launch_l2_flush_read(const double* buf, size_t n, double* sink, cudaStream_t s);

@@ -26,13 +26,13 @@ __global__ void restrict_first_kernel(const double* fg, const double* fu, double
     }
 }
 
-// fine.u[j*m] += coarse.u[j], j = 0..J  (mgrit.hpp:172-180)
-__global__ void inject_kernel(const double* cu, double* fu, int n, int J, int m) {
-    const size_t total = (size_t)(J + 1) * n;
+// fine.u[j*m] += coarse.u[j], j = j0..j1-1  (mgrit.hpp:172-180)
+__global__ void inject_kernel(const double* cu, double* fu, int n, int j0, int j1, int m) {
+    const size_t total = (size_t)(j1 - j0) * n;
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-        const size_t j = t / n, i = t - j * n;
+        const size_t j = j0 + t / n, i = t % n;
         double* dst = fu + j * m * (size_t)n + i;
-        *dst = *dst + cu[t];
+        *dst = *dst + cu[j * n + i];
     }
 }
 
@@ -250,9 +250,14 @@ void launch_restrict_first(const double* fg, const double* fu, double* cg, doubl
 }
 
 void launch_inject(const double* cu, double* fu, int n, int J, int m, cudaStream_t s) {
-    const size_t total = (size_t)(J + 1) * n;
+    launch_inject_range(cu, fu, n, 0, J + 1, m, s);
+}
+
+void launch_inject_range(const double* cu, double* fu, int n, int j0, int j1, int m, cudaStream_t s) {
+    if (j1 <= j0) return;
+    const size_t total = (size_t)(j1 - j0) * n;
     const int grid = (int)std::min<size_t>((total + 255) / 256, 4096);
-    inject_kernel<<<grid, 256, 0, s>>>(cu, fu, n, J, m);
+    inject_kernel<<<grid, 256, 0, s>>>(cu, fu, n, j0, j1, m);
     PHI_CUDA(cudaGetLastError());
 }
 
