@@ -660,12 +660,15 @@ void Mgrit::wave(int l, int mode, int epi, int n_tasks, const int* k0, int len, 
 }
 
 Mgrit::~Mgrit() {
-    if (side) {
-        cudaStreamSynchronize(side);
-        cudaStreamDestroy(side);
+    for (int i = 0; i < kSides; ++i) {
+        if (side[i]) {
+            cudaStreamSynchronize(side[i]);
+            cudaStreamDestroy(side[i]);
+        }
+        if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+        if (ev_inj[i]) cudaEventDestroy(ev_inj[i]);
     }
     if (ev_pre) cudaEventDestroy(ev_pre);
-    if (ev_join) cudaEventDestroy(ev_join);
     if (prog_host) cudaFreeHost(prog_host);
 }
 
@@ -674,15 +677,19 @@ void Mgrit::coarse_overlapped(int lc, bool residual) {
     Level& c = levels[lc];
     Level& f = levels[lf];
     const int n = disc->n_p, m = cfg.m, J = f.steps / m;
-    if (!side) {
+    if (!side[0]) {
         int lo = 0, hi = 0;
         PHI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        PHI_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+        for (int i = 0; i < kSides; ++i) {
+            PHI_CUDA(cudaStreamCreateWithPriority(&side[i], cudaStreamNonBlocking, lo));
+            PHI_CUDA(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
+            PHI_CUDA(cudaEventCreateWithFlags(&ev_inj[i], cudaEventDisableTiming));
+            for (auto& lv : levels) ws_side[i].ensure(lv.stepper->H);
+        }
         PHI_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
-        PHI_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         PHI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&prog_host), sizeof(unsigned), cudaHostAllocMapped));
         PHI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&prog_dev), prog_host, 0));
-        for (auto& lv : levels) ws_side.ensure(lv.stepper->H);
+        preload_overlap_kernels(f.stepper->H);
     }
     volatile unsigned* prog = prog_host;
     *prog = 0u;
@@ -695,24 +702,41 @@ void Mgrit::coarse_overlapped(int lc, bool residual) {
     // the fine-level work, interval by interval as the coarse points land:
     // injection (mgrit.hpp:172-180), F-relaxation, and (residual) the terms
     // of residual_norm(0) (mgrit.hpp:197-214), on the side stream
-    PHI_CUDA(cudaStreamWaitEvent(side, ev_pre, 0));
-    const Route sr{side, &ws_side, true, nullptr};
-    if (residual) PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (f.steps + 1), side));
+    for (int i = 0; i < kSides; ++i) PHI_CUDA(cudaStreamWaitEvent(side[i], ev_pre, 0));
+    if (residual) PHI_CUDA(cudaMemsetAsync(sq.get(), 0, sizeof(double) * (f.steps + 1), side[0]));
+    int rr = 0;  // chunks go round-robin over the side streams (each chunk is m - 1 steps deep)
+    // chunks of J/16 intervals (shrinking chunks towards the end of the march
+    // measured no better: more launches)
     const int chunk = std::max(1, J / 16);
     int injected = 0, done = 0;  // C-points injected, intervals relaxed
+    const bool dbg = std::getenv("PHI_OVERLAP_DEBUG") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto since = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+    long long polls = 0;
     while (done < J) {
+        ++polls;
         // coarse points 0..p are final (coarse point 0 is g[0], copied before the march)
         const unsigned pv = *prog;
         const int p = (int)std::min<unsigned>(pv, (unsigned)J);
         const int ready = p;  // interval j needs coarse points j and j + 1
         if (ready - done >= chunk || (p >= J && ready > done)) {
-            launch_inject_range(c.u.get(), f.u.get(), n, injected, p + 1, m, side);
+            if (dbg) std::fprintf(stderr, "overlap: %.2f ms progress %u -> intervals [%d, %d) (%lld polls)\n", since(), pv, done, ready, polls);
+            const int cur = rr, prev = (rr + kSides - 1) % kSides;
+            const cudaStream_t ss = side[cur];
+            const Route sr{ss, &ws_side[cur], true, nullptr};
+            rr = (rr + 1) % kSides;
+            // the chunk's C-points [injected, p] -- disjoint from the other chunks'
+            launch_inject_range(c.u.get(), f.u.get(), n, injected, p + 1, m, ss);
             ++launches;
-            if (residual && injected == 0) {  // point 0 after its injection
-                launch_resid0(f.g.get(), f.u.get(), sq.get(), n, side);
+            if (residual && injected == 0) {  // point 0 after its injection (stream 0: after the memset)
+                launch_resid0(f.g.get(), f.u.get(), sq.get(), n, ss);
                 ++launches;
             }
             injected = p + 1;
+            // interval `done` starts from C-point done m, injected by the
+            // previous chunk (another stream): wait for that injection only
+            if (done > 0) PHI_CUDA(cudaStreamWaitEvent(ss, ev_inj[prev], 0));
+            PHI_CUDA(cudaEventRecord(ev_inj[cur], ss));
             wave(lf, kModeStep, kEpiStore, ready - done, f.kF.get() + done, m - 1, nullptr, nullptr, &sr);
             if (residual)
                 wave(lf, kModeStep, kEpiResid, (ready - done) * m, f.kAll.get() + done * m, 1, nullptr, nullptr, &sr);
@@ -724,14 +748,17 @@ void Mgrit::coarse_overlapped(int lc, bool residual) {
             std::this_thread::sleep_for(std::chrono::microseconds(20));
         } else {
             PHI_CUDA(cudaGetLastError());
+            if (dbg) std::fprintf(stderr, "overlap: %.2f ms march stream idle, progress %u\n", since(), *prog);
             if (*prog < (unsigned)J) {  // the march ended without finishing (an error): drain
                 PHI_CUDA(cudaStreamSynchronize(stream));
                 *prog = (unsigned)J;
             }
         }
     }
-    PHI_CUDA(cudaEventRecord(ev_join, side));
-    PHI_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+    for (int i = 0; i < kSides; ++i) {
+        PHI_CUDA(cudaEventRecord(ev_join[i], side[i]));
+        PHI_CUDA(cudaStreamWaitEvent(stream, ev_join[i], 0));
+    }
     sq_ready = residual;
 }
 
@@ -1063,9 +1090,12 @@ int Mgrit::wave_report(double* ms, double* bytes) {
         const double mat = nnzA /* A- */ + (1 + cmax) * nnzA + cmax * vmat;
         const double vec = pts * (5 * n + 3 * n) + (pts + csum) * 4 * n + csum * vvec;
         *bytes += 8.0 * (mat + vec);
-        if (std::getenv("PHI_WAVE_DEBUG"))
-            std::fprintf(stderr, "wave %zu level %d: %.3f ms, points %d, cycles sum %d max %d, algorithmic %.4e B\n", k,
-                         recs[k].level, t, (int)pts, (int)csum, (int)cmax, 8.0 * (mat + vec));
+        if (std::getenv("PHI_WAVE_DEBUG")) {
+            float t0 = 0.f;  // start relative to the first recorded wave
+            PHI_CUDA(cudaEventElapsedTime(&t0, recs[0].start, recs[k].start));
+            std::fprintf(stderr, "wave %zu level %d: %.3f ms at +%.3f ms, points %d, cycles sum %d max %d, algorithmic %.4e B\n",
+                         k, recs[k].level, t, t0, (int)pts, (int)csum, (int)cmax, 8.0 * (mat + vec));
+        }
     }
     for (auto& r : recs) {
         cudaEventDestroy(r.start);

@@ -265,11 +265,12 @@ public:
     int* iters_dev = nullptr;  // per-task iteration counts of the next waves (nullable)
     // overlap of the coarse march with interpolation / residual (coarse_overlapped)
     bool overlap = true;        // PHI_OVERLAP=0 disables
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_pre = nullptr, ev_join = nullptr;
+    static constexpr int kSides = 4;  // side streams (chunks round-robin, each with its own workspace)
+    cudaStream_t side[kSides] = {};
+    cudaEvent_t ev_pre = nullptr, ev_join[kSides] = {}, ev_inj[kSides] = {};
     unsigned* prog_host = nullptr;  // host-mapped progress counter of the coarse march
     unsigned* prog_dev = nullptr;
-    Workspace ws_side;
+    Workspace ws_side[kSides];
     bool sq_ready = false;      // level-0 residual terms of the current state are in `sq`
     bool top_cycle = false;     // inside mgrit_cycle(0)
     ~Mgrit();

@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "device_types.cuh"
 #include "phi_kernels.cuh"
@@ -1811,7 +1812,9 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
     cl_sync();
 }
 
-template <int DEG>
+// SIDE: a second instantiation for the side-stream waves that run while the
+// coarse march (a cluster launch of the SIDE = 0 instance) is in flight
+template <int DEG, int SIDE = 0>
 __global__ void __launch_bounds__(NT, 1)
     phi_wave_kernel(const __grid_constant__ DevHier H_param, const __grid_constant__ DevStencil Am,
                     const __grid_constant__ WaveArgs a_param, const __grid_constant__ SmemPlan P, double* ws_base,
@@ -1997,8 +2000,17 @@ static inline int occupancy_grid(K kernel, size_t smem, int want) {
         PHI_CUDA(cudaGetDevice(&dev));
         PHI_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
-    if (smem > 48 * 1024)
-        PHI_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the dynamic shared-memory limit is raised ONCE per kernel to the plan's
+    // budget: changing a function attribute while an instance of the same
+    // kernel runs serialises the next launch behind it (it defeated the
+    // overlap of the coarse march with the side-stream waves)
+    static std::vector<const void*> raised;
+    const void* key = reinterpret_cast<const void*>(kernel);
+    if (std::find(raised.begin(), raised.end(), key) == raised.end()) {
+        PHI_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(smem, kPhiSmemBudgetBytes)));
+        raised.push_back(key);
+    }
     int per_sm = 0;
     PHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NT, smem));
     if (per_sm < 1) per_sm = 1;
@@ -2065,10 +2077,19 @@ void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cl > 8) PHI_CUDA(cudaFuncSetAttribute(phi_wave_kernel<DEG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        static bool nonportable = false;
+        if (cl > 8 && !nonportable) {
+            PHI_CUDA(cudaFuncSetAttribute(phi_wave_kernel<DEG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            nonportable = true;
+        }
         PHI_CUDA(cudaLaunchKernelEx(&cfg, phi_wave_kernel<DEG>, H, Am, a, P, ws, ws_stride));
     } else {
-        phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
+        if (a.no_cluster) {
+            occupancy_grid(phi_wave_kernel<DEG, 1>, smem, grid);
+            phi_wave_kernel<DEG, 1><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
+        } else {
+            phi_wave_kernel<DEG><<<grid, NT, smem, s>>>(H, Am, a, P, ws, ws_stride);
+        }
     }
     PHI_CUDA(cudaGetLastError());
 }
@@ -2098,6 +2119,13 @@ void DegLaunch<DEG>::cg(const DevStencil& A, const double* diag, const double* b
                         double rel_tol, int max_iter, int* result, int exact, cudaStream_t s) {
     cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result, exact);
     PHI_CUDA(cudaGetLastError());
+}
+
+template <int DEG>
+void DegLaunch<DEG>::preload_side(const DevHier& H) {
+    cudaFuncAttributes fa;
+    PHI_CUDA(cudaFuncGetAttributes(&fa, phi_wave_kernel<DEG, 1>));
+    occupancy_grid(phi_wave_kernel<DEG, 1>, phi_smem_bytes(H), 1);
 }
 
 template <int DEG>

@@ -39,6 +39,9 @@ struct DegLaunch {
     static void cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
                    double rel_tol, int max_iter, int* result, int exact, cudaStream_t s);
     static void set_trace(long long* trace, int xmask);
+    /// load the side-stream wave kernel now (lazy module loading of a kernel
+    /// while the coarse march runs serialises its launch behind the march)
+    static void preload_side(const DevHier& H);
 };
 extern template struct DegLaunch<1>;
 extern template struct DegLaunch<2>;
@@ -67,6 +70,9 @@ void launch_inject_range(const double* cu, double* fu, int n, int j0, int j1, in
 void launch_resid0(const double* g, const double* u, double* sq, int n, cudaStream_t s);
 /// Reads n doubles (a multiple of 4, > L2): flushes L2 leaving clean lines.
 void launch_l2_flush_read(const double* buf, size_t n, double* sink, cudaStream_t s);
+/// force-load every kernel the overlapped coarse phase launches on its side
+/// stream (inject, resid0, the side wave kernel of H's degree)
+void preload_overlap_kernels(const DevHier& H);
 void launch_copy(double* dst, const double* src, size_t n, cudaStream_t s);
 
 // ---- device ILUT (ilut.cu) ------------------------------------------------

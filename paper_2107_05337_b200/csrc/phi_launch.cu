@@ -244,6 +244,14 @@ int phi_read_trace(long long* out, int n) {
     return m;
 }
 
+void preload_overlap_kernels(const DevHier& H) {
+    cudaFuncAttributes fa;
+    PHI_CUDA(cudaFuncGetAttributes(&fa, inject_kernel));
+    PHI_CUDA(cudaFuncGetAttributes(&fa, resid0_kernel));
+    PHI_CUDA(cudaFuncGetAttributes(&fa, copy_kernel));
+    PHI_DEG_DISPATCH(degree_of(H.A), DegLaunch<DEG>::preload_side(H));
+}
+
 void launch_restrict_first(const double* fg, const double* fu, double* cg, double* cu, int n, cudaStream_t s) {
     restrict_first_kernel<<<(n + 255) / 256, 256, 0, s>>>(fg, fu, cg, cu, n);
     PHI_CUDA(cudaGetLastError());
