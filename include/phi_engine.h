@@ -147,8 +147,10 @@ int phi_hier_spmm(phi_hier* h, const double* x, double* y, int nrhs, int device_
 /* Kernel microbenchmark (BASELINE config 5): average device time (CUDA events)
  * of `reps` launches on seeded N(0,1) inputs -- which 0: the SpMM above,
  * which 1: one V(nu_pre, nu_post) cycle (pmultigrid.hpp:256-267) from x0 = 0
- * on nrhs right-hand sides (one CTA each).  flush_l2: read a 256 MB buffer between
- * reps (L2 left with clean lines). */
+ * on nrhs right-hand sides (one CTA each).  flush_l2 = 1: read a 256 MB buffer
+ * between reps (L2 left with clean lines), events around every single launch;
+ * flush_l2 = 2 (which 0 only): 4 * reps back-to-back launches cycling through
+ * four copies of the tiled operator (> L2 in total), events around the lot. */
 int phi_hier_time(phi_hier* h, int which, int nrhs, int reps, int flush_l2, double* ms_out);
 /* Algorithmic bytes of one V(nu_pre, nu_post) cycle on nrhs right-hand sides
  * (SURVEY.md 8(d) model: 8 B per stored operator nonzero per application and

@@ -18,7 +18,10 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 # developer trace builds go to their own directory (PHI_TRACE=1 -> _lib_trace)
-OUT_DIR = os.path.join(HERE, "_lib_trace" if os.environ.get("PHI_TRACE") == "1" else "_lib")
+# developer A/B builds: PHI_VARIANT=name PHI_VARIANT_FLAGS="-DX=1 ..." -> _lib_<name>
+_VARIANT = os.environ.get("PHI_VARIANT", "")
+OUT_DIR = os.path.join(HERE, "_lib_trace" if os.environ.get("PHI_TRACE") == "1"
+                       else ("_lib_" + _VARIANT if _VARIANT else "_lib"))
 LIB = os.path.join(OUT_DIR, "libphi_engine.so")
 ROOT = os.path.dirname(HERE)
 
@@ -31,6 +34,9 @@ if os.environ.get("PHI_TRACE") == "1":  # developer timing stamps (tools/probe_*
     NVCC_FLAGS += ["-DPHI_TRACE_ON=1"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-unused-function",
              f"-I{CUDA_INC}"]
+if _VARIANT:
+    NVCC_FLAGS += os.environ.get("PHI_VARIANT_FLAGS", "").split()
+    CXX_FLAGS += os.environ.get("PHI_VARIANT_FLAGS", "").split()
 
 CU = ["phi_launch.cu", "assembly.cu", "spmm.cu", "ilut.cu"]
 DEGREES = range(1, 9)  # phi_deg.cu is compiled once per spline degree (-DPHI_DEG=d)

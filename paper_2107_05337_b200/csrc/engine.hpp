@@ -124,13 +124,13 @@ public:
     DenseLUHost coarse;
     DevBuf<double> coarse_lu;
     int dense_level = -1;      // reassociated mode: W-cycle subtree collapsed to a dense operator
-    DevBuf<double> a_tile;     // tiled copy of A for the streaming SpMV / SpMM (built on first use)
-    const double* a_tiled(cudaStream_t s) {
-        if (!a_tile.get()) {
-            a_tile.alloc(tile_doubles(A.view()));
-            launch_tile(A.view(), a_tile.get(), s);
+    DevBuf<double> a_tile[2];  // tiled copies of A for the streaming SpMV (0) / SpMM (1), built on first use
+    const double* a_tiled(cudaStream_t s, int kind) {
+        if (!a_tile[kind].get()) {
+            a_tile[kind].alloc(tile_doubles(A.view(), kind));
+            launch_tile(A.view(), a_tile[kind].get(), kind, s);
         }
-        return a_tile.get();
+        return a_tile[kind].get();
     }
     DevBuf<double> dense_op;
     int dense_level_cl = -1;   // the same for cluster mode (single-right-hand-side waves)

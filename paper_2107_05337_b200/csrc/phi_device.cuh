@@ -675,14 +675,17 @@ __device__ __forceinline__ void tri_solve_warp(const DevTri& T, double* zg, int 
 // ---- block-recurrence sweeps (reassociated mode) ---------------------------
 // `count` consecutive sweeps (ILUT substitution or Gauss-Seidel) over one
 // BlkStream (setup_host.hpp): blocks of 32 consecutive rows in solve order,
-// block k solved as x_{R_k} = B_k^{-1} (rhs - old - fresh).  The blocks of
-// the `count` sweeps form one sequence g = s * nb + k.
-//  * warp 0 (the solver) runs the dependent chain.  Per block it waits until
-//    the workers' old sums are in, then -- everything that does not depend on
-//    block g-1 issued first -- gathers the fresh columns (block g-1),
-//    broadcasts t = rhs - old - fresh through shared memory, multiplies by
-//    the dense inverse and stores the 32 new values;
-//  * warps 1..parts (the workers) each sum one interleaved part of the
+// block k solved as x_{R_k} = B_k^{-1} (rhs - old) - G_k x_{R_{k-1}} with the
+// folded coupling G_k = B_k^{-1} N_k to block k-1.  The blocks of the `count`
+// sweeps form one sequence g = s * nb + k.
+//  * the solver warps take the blocks in rotation.  Per block a solver waits
+//    until the workers' old sums are in and -- none of it depending on block
+//    g-1 -- broadcasts rhs - old through shared memory, multiplies by the
+//    dense inverse and loads G_k into registers; only then does it wait for
+//    block g-1, whose last 8 mf values (in solve order, sy.xb) it multiplies
+//    by G_k: the block-to-block critical path is the hand-off, 4 mf 16-byte
+//    loads and 8 mf fused multiply-adds in four chains (fold_block);
+//  * the other warps (the workers) each sum one interleaved part of the
 //    block's old entries as soon as block g-2 is done (and, for a later
 //    sweep, the previous sweep's rows they read), one block ahead of the
 //    solver.
@@ -754,7 +757,8 @@ __device__ __forceinline__ void lds_slot(unsigned a, int& c, double& v) {  // {i
 
 struct __align__(16) BlkSync {
     double cbuf[kBlkHand][kBlkMaxParts][32];  // workers' partial old sums
-    double tb[kBlkSolvers][32];               // per-solver broadcast of t (16-byte aligned)
+    double tb[kBlkSolvers][32];               // per-solver broadcast of rhs - old (16-byte aligned)
+    double xb[2][32];                         // block g's values in solve order at xb[g & 1] (the chain's input)
     unsigned long long bar[kBlkMaxSlots];
     int phase[kBlkMaxSlots];  // phases completed per slot since the kernel started
     int cnt[kBlkHand];
@@ -778,10 +782,67 @@ __device__ __forceinline__ void blk_init() {
     // the callers' next __syncthreads() publishes the initialisation
 }
 
-// named barriers of the solver hand-off: block g done -> solver (g + 1) % 2
+// named barriers of the solver hand-off: block g done -> solver (g + 1) % kBlkSolvers
 __device__ __forceinline__ void hand_wait(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void hand_signal(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 constexpr int kHandBar = 1;  // ids 1 .. kBlkSolvers
+
+// One block of a folded block sweep for NG groups of four column pairs of
+// G_k, from the point where the block's unit has landed and its inverse is
+// in registers: G_k into registers (before any wait), the workers' old sums,
+// y = B^{-1} (rhs - old) through a shared-memory broadcast, y pinned before
+// the hand-off wait (nothing but the chain's own loads and fused
+// multiply-adds after it), then y - G_k x_{g-1} in four chains.
+template <int NG>
+__device__ __forceinline__ double fold_block(unsigned gp, unsigned xp, const double (&iv)[32], double rhs, unsigned tb,
+                                             unsigned cnt_a, int P, unsigned cbuf_a, int lane, int hand_id,
+                                             long long* tr) {
+    double gq[NG > 0 ? 8 * NG : 1];
+#pragma unroll
+    for (int p2 = 0; p2 < 4 * NG; ++p2) lds_v2f64(gp + 512u * p2, gq[2 * p2], gq[2 * p2 + 1]);
+    if (tr) tr[7] = clock64();
+    // ---- all parts in: the partial old sums
+    const int all = wait_ge(cnt_a, P);
+    double part[kBlkMaxParts];
+#pragma unroll
+    for (int q = 0; q < kBlkMaxParts; ++q)
+        part[q] = q < P ? vlds_f64(cbuf_a + 8u * (q * 32 + lane) + (unsigned)(all - P)) : 0.0;
+    double old = 0.0;
+#pragma unroll
+    for (int q = 0; q < kBlkMaxParts; ++q) old = old + part[q];
+    const double c = rhs - old;
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(c) : "memory");
+    __syncwarp();
+    double acc[8];
+#pragma unroll
+    for (int p2 = 0; p2 < 16; ++p2) {
+        double t0, t1;
+        lds_v2f64(tb + 16u * p2, t0, t1);
+        if (p2 < 4) {
+            acc[2 * p2] = iv[2 * p2] * t0;
+            acc[2 * p2 + 1] = iv[2 * p2 + 1] * t1;
+        } else {
+            acc[(2 * p2) & 7] = __fma_rn(iv[2 * p2], t0, acc[(2 * p2) & 7]);
+            acc[(2 * p2 + 1) & 7] = __fma_rn(iv[2 * p2 + 1], t1, acc[(2 * p2 + 1) & 7]);
+        }
+    }
+    double y = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    // y is complete before the wait (volatile asm statements keep their order)
+    asm volatile("" : "+d"(y));
+    if (tr) tr[4] = clock64();
+    if (hand_id >= 0) hand_wait(hand_id);
+    if (tr) tr[2] = clock64();
+    if (NG == 0) return y;
+    double f[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int p2 = 0; p2 < 4 * NG; ++p2) {
+        double x0, x1;
+        lds_v2f64(xp + 16u * (15 - p2), x0, x1);
+        f[(2 * p2) & 3] = __fma_rn(gq[2 * p2], x0, f[(2 * p2) & 3]);
+        f[(2 * p2 + 1) & 3] = __fma_rn(gq[2 * p2 + 1], x1, f[(2 * p2 + 1) & 3]);
+    }
+    return y - ((f[0] + f[1]) + (f[2] + f[3]));
+}
 
 // WIN (rolling-window streams, BlkStream::win): x_off is the window, the
 // stream's columns are window slots (16-bit for the old entries), solved
@@ -805,7 +866,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
         // ---- solver warps 0 .. NS-1 take blocks g = w, w + NS, ...  The parts'
         // count implies the block's unit has landed (each worker waited).
         const unsigned tb = sh_addr(sy.tb[w]);
-        const int xn = WIN ? T.win : T.n;  // the zero slot x[n] (window: slot win)
+        const unsigned xbs = sh_addr(sy.xb);
         int slot = w % n_slots, k = w % nb;
         int4 info = w < total ? __ldg(table + k) : make_int4(0, 0, 0, 0);  // (off16, bytes, mf, 0)
         int4 refill_next = make_int4(0, 0, 0, 0);
@@ -850,70 +911,32 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             if (tr) tr[1] = clock64();
             // data dependence on the wait: none of these loads moves above it
             const unsigned u = ring + slot * slot_bytes + (unsigned)(seen > 0 ? 0 : 1);
-            // ---- independent of block g-1: row, rhs, inverse, mid slots
+            // ---- independent of block g-1: row, rhs, inverse, old sums, y = B^{-1} (rhs - old)
             const int row = RSM ? vlds_s32(u + 16u + 4u * lane) : row_of(k);
             double rhs = rhs_pref;
             if (RSM && row >= 0) rhs = vlds_f64(rs + 8u * row);
             double iv[32];
 #pragma unroll
             for (int p2 = 0; p2 < 16; ++p2) lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
-            const unsigned fr = u + kBlkFreshOff + 16u * lane;
-            constexpr int FB = 16;  // fresh slots held in registers (the rest: rare)
-            int fc[FB];
-            double fv[FB];
-#pragma unroll
-            for (int q = 0; q < FB; ++q) {
-                fc[q] = xn;
-                fv[q] = 0.0;
-                if (q < mf) lds_slot(fr + 512u * q, fc[q], fv[q]);
+            // ---- G_k, the old sums, y = B^{-1} (rhs - old), the wait for block
+            // g-1 (the previous solver), then the chain x_g = y - G_k x_{g-1}
+            // over the last 8 mf values of block g-1 (mf: groups of four column pairs)
+            const unsigned gp = u + kBlkFreshOff + 16u * lane;
+            const unsigned xp = xbs + 256u * ((g + 1) & 1);
+            const int hand_id = g > 0 ? kHandBar + (w == 0 ? NS - 1 : w - 1) : -1;
+            const unsigned cnt_a = cnt + 4u * (g & (kBlkHand - 1));
+            const unsigned cbuf_a = cbuf + 8u * ((g & (kBlkHand - 1)) * kBlkMaxParts * 32);
+            double z;
+            switch (mf) {
+                case 0: z = fold_block<0>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
+                case 1: z = fold_block<1>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
+                case 2: z = fold_block<2>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
+                case 3: z = fold_block<3>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
+                default: z = fold_block<4>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
             }
-            // ---- all parts in: the partial old sums
-            const int all = wait_ge(cnt + 4u * (g & (kBlkHand - 1)), P);
-            double part[kBlkMaxParts];
-#pragma unroll
-            for (int q = 0; q < kBlkMaxParts; ++q)
-                part[q] = q < P ? vlds_f64(cbuf + 8u * (((g & (kBlkHand - 1)) * kBlkMaxParts + q) * 32 + lane) +
-                                           (unsigned)(all - P))
-                                : 0.0;
-            double old = 0.0;
-#pragma unroll
-            for (int q = 0; q < kBlkMaxParts; ++q) old = old + part[q];
-            const double c = rhs - old;
-            // ---- wait for block g-1 (the other solver)
-            if (g > 0) hand_wait(kHandBar + (w == 0 ? NS - 1 : w - 1));
-            if (tr) tr[2] = clock64();
-            // ---- the chain: fresh columns of block g-1, broadcast, inverse
-            double xf[FB];
-#pragma unroll
-            for (int q = 0; q < FB; ++q) xf[q] = q < mf ? xld<XSM>(xg, xs, fc[q]) : 0.0;
-            double f[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) f[q] = __fma_rn(fv[q + 8], xf[q + 8], fv[q] * xf[q]);
-            for (int q = FB; q < mf; ++q) {  // rare: more than FB fresh slots
-                int cq;
-                double vq;
-                lds_slot(fr + 512u * q, cq, vq);
-                // a fixed accumulator: an indexed f[] would live in local memory
-                f[0] = __fma_rn(vq, xld<XSM>(xg, xs, cq), f[0]);
-            }
-            const double t = c - (((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
-            if (tr) tr[3] = clock64() + (long long)(t == 1.2345);
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(tb + 8u * lane), "d"(t) : "memory");
-            __syncwarp();
-            double acc[8];
-#pragma unroll
-            for (int p2 = 0; p2 < 16; ++p2) {
-                double t0, t1;
-                lds_v2f64(tb + 16u * p2, t0, t1);
-                if (p2 < 4) {
-                    acc[2 * p2] = iv[2 * p2] * t0;
-                    acc[2 * p2 + 1] = iv[2 * p2 + 1] * t1;
-                } else {
-                    acc[(2 * p2) & 7] = __fma_rn(iv[2 * p2], t0, acc[(2 * p2) & 7]);
-                    acc[(2 * p2 + 1) & 7] = __fma_rn(iv[2 * p2 + 1], t1, acc[(2 * p2 + 1) & 7]);
-                }
-            }
-            const double z = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            if (tr) tr[3] = clock64() + (long long)(z == 1.2345);
+            // the values in solve order, for block g+1's chain
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(xbs + 256u * (g & 1) + 8u * lane), "d"(z) : "memory");
             if constexpr (WIN) {
                 if (row >= 0) {
                     xst<true>(xg, xs, row & (T.win - 1), z);
@@ -961,7 +984,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             const int mo = vlds_s32(u), mf = vlds_s32(u + 12u);
             // part q: columns int32[mo][32] (window: uint16), then values double[mo][32]
             constexpr unsigned CB = WIN ? 2u : 4u;
-            const unsigned pb = u + kBlkFreshOff + 512u * mf + (32u * CB + 256u) * mo * q;
+            const unsigned pb = u + kBlkFreshOff + 2048u * mf + (32u * CB + 256u) * mo * q;
             const unsigned oc = pb + CB * lane;
             const unsigned ov = pb + 32u * CB * mo + 8u * lane;
             const int xpad = WIN ? T.win : T.n;
@@ -983,6 +1006,24 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
                 for (int e = 0; e < 8; ++e) xv[e] = e < mo ? xld<XSM>(xg, xs, c[e]) : 0.0;
                 a0 = __fma_rn(v[0], xv[0], v[1] * xv[1]) + __fma_rn(v[4], xv[4], v[5] * xv[5]);
                 a1 = __fma_rn(v[2], xv[2], v[3] * xv[3]) + __fma_rn(v[6], xv[6], v[7] * xv[7]);
+            } else if (mo <= 16) {  // the same with sixteen slots in registers (degree 4 and 5 factors)
+                int c[16];
+                double v[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    c[e] = e < mo ? ldc(e) : xpad;
+                    v[e] = e < mo ? vlds_f64(ov + 256u * e) : 0.0;
+                }
+                if (tr) tr[9] = clock64();
+                wait_ge(prog, need);
+                if (tr) tr[10] = clock64();
+                double xv[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) xv[e] = e < mo ? xld<XSM>(xg, xs, c[e]) : 0.0;
+                a0 = (__fma_rn(v[0], xv[0], v[1] * xv[1]) + __fma_rn(v[4], xv[4], v[5] * xv[5])) +
+                     (__fma_rn(v[8], xv[8], v[9] * xv[9]) + __fma_rn(v[12], xv[12], v[13] * xv[13]));
+                a1 = (__fma_rn(v[2], xv[2], v[3] * xv[3]) + __fma_rn(v[6], xv[6], v[7] * xv[7])) +
+                     (__fma_rn(v[10], xv[10], v[11] * xv[11]) + __fma_rn(v[14], xv[14], v[15] * xv[15]));
             } else {
                 if (tr) tr[9] = clock64();
                 wait_ge(prog, need);

@@ -108,9 +108,10 @@ void launch_stencil_transpose(const DevStencil& a, double* out, cudaStream_t s);
 /// out = a + c * b elementwise (sparse_add on a shared pattern, sparse.hpp:148-178).
 void launch_axpby(const double* a, double c, const double* b, double* out, size_t n, cudaStream_t s);
 /// Y = A X for nrhs in {1, 16, 32, 64}; X, Y [n][nrhs]; At: the tiled copy of A
-/// (launch_tile, tile_doubles doubles) (spmm.cu).
-void launch_tile(const DevStencil& A, double* At, cudaStream_t s);
-size_t tile_doubles(const DevStencil& A);
+/// of kind tile_kind(nrhs) (launch_tile, tile_doubles doubles) (spmm.cu).
+int tile_kind(int nrhs);
+void launch_tile(const DevStencil& A, double* At, int kind, cudaStream_t s);
+size_t tile_doubles(const DevStencil& A, int kind);
 void launch_spmm(const DevStencil& A, const double* At, const double* X, double* Y, int nrhs, cudaStream_t s);
 /// Line Gauss-Seidel coefficients of a 9-point order-1 level (9 n doubles).
 void launch_gs_line_coeffs(const double* a, int nf, double* out, cudaStream_t s);

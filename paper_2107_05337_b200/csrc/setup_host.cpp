@@ -646,9 +646,15 @@ BlkStream make_blk_stream(const BlkRowsView& rv, int win) {
                 }
             }
             b.maxold = std::max(b.maxold, b.olde[l].size());
-            b.mf = std::max(b.mf, b.frsh[l].size());
+            // fresh columns lie in block k-1 (kBlkFresh = 1): the folded
+            // coupling reaches back to local column 32 - nf of that block
+            for (const auto& fe : b.frsh[l]) {
+                const int jl = pos_of(fe.first) - (k - 1) * kBlkRows;
+                if (jl < 0 || jl >= kBlkRows) throw std::logic_error("make_blk_stream: fresh column outside block k-1");
+                b.mf = std::max<size_t>(b.mf, static_cast<size_t>(kBlkRows - jl));
+            }
         }
-        b.mf = (b.mf + 1) / 2 * 2;  // pairs of fresh slots
+        b.mf = (b.mf + 7) / 8;  // groups of four column pairs of the folded coupling G_k
         maxold_all = std::max(maxold_all, b.maxold);
     }
     // worker parts: about four old slots per part and lane
@@ -671,7 +677,7 @@ BlkStream make_blk_stream(const BlkRowsView& rv, int win) {
                 inv[l][j] = acc / b.B[l][l];
             }
         const size_t part_bytes = (win ? 320 : 384) * mo;
-        const size_t bytes = kBlkFreshOff + 512 * mf + static_cast<size_t>(P) * part_bytes;
+        const size_t bytes = kBlkFreshOff + 2048 * mf + static_cast<size_t>(P) * part_bytes;
         std::vector<unsigned char> img(bytes, 0);
         const int hdr[4] = {static_cast<int>(mo), 0, static_cast<int>(bytes), static_cast<int>(mf)};
         std::memcpy(img.data(), hdr, sizeof hdr);
@@ -682,20 +688,31 @@ BlkStream make_blk_stream(const BlkRowsView& rv, int win) {
                 iv[(pj * kBlkRows + l) * 2] = static_cast<double>(inv[l][2 * pj]);
                 iv[(pj * kBlkRows + l) * 2 + 1] = static_cast<double>(inv[l][2 * pj + 1]);
             }
-        unsigned char* fr = img.data() + kBlkFreshOff;
-        for (size_t q = 0; q < mf; ++q)
-            for (int l = 0; l < kBlkRows; ++l) {
-                int col = pad;
-                double v = 0.0;
-                if (q < b.frsh[l].size()) {
-                    col = stored(b.frsh[l][q].first);
-                    v = b.frsh[l][q].second;
+        // folded coupling to block k-1: G = B^{-1} N, N(l, j) = the fresh
+        // entry of row l at local column j of block k-1; pair q holds the
+        // columns (30 - 2q, 31 - 2q), so the chain walks back from the last
+        // solved value and stops after mf pairs
+        if (mf) {
+            static long double nn[kBlkRows][kBlkRows], gg[kBlkRows][kBlkRows];
+            for (auto& r : nn)
+                for (auto& v : r) v = 0.0L;
+            for (int l = 0; l < kBlkRows; ++l)
+                for (const auto& fe : b.frsh[l]) nn[l][pos_of(fe.first) - (k - 1) * kBlkRows] += fe.second;
+            for (int l = 0; l < kBlkRows; ++l)
+                for (int j = 0; j < kBlkRows; ++j) {
+                    long double acc = 0.0L;
+                    for (int m = 0; m <= l; ++m) acc += inv[l][m] * nn[m][j];
+                    gg[l][j] = acc;
                 }
-                std::memcpy(fr + (q * kBlkRows + l) * 16, &col, 4);
-                std::memcpy(fr + (q * kBlkRows + l) * 16 + 8, &v, 8);
-            }
+            double* gv = reinterpret_cast<double*>(img.data() + kBlkFreshOff);
+            for (size_t q = 0; q < 4 * mf; ++q)
+                for (int l = 0; l < kBlkRows; ++l) {
+                    gv[(q * kBlkRows + l) * 2] = static_cast<double>(gg[l][30 - 2 * q]);
+                    gv[(q * kBlkRows + l) * 2 + 1] = static_cast<double>(gg[l][31 - 2 * q]);
+                }
+        }
         for (int p = 0; p < P; ++p) {
-            unsigned char* pb = img.data() + kBlkFreshOff + 512 * mf + static_cast<size_t>(p) * part_bytes;
+            unsigned char* pb = img.data() + kBlkFreshOff + 2048 * mf + static_cast<size_t>(p) * part_bytes;
             const size_t cb = (win ? 2 : 4) * kBlkRows * mo;  // column bytes of the part
             double* ov = reinterpret_cast<double*>(pb + cb);
             auto put_col = [&](size_t slot, int c) {

@@ -131,34 +131,41 @@ TriStream make_tri_stream(const TriPlan& p, bool fast);
 /// per lane.  For block k with rows R_k the sweep
 ///     x_i = (rhs_i - sum_{j before i} a_ij x_j(new) - sum_{j after i} a_ij x_j(old)) / d_i
 /// (d_i = 1 for the unit lower ILUT factor) is
-///     x_{R_k} = B_k^{-1} (rhs - old - fresh),   B_k = D + (in-block lower part),
-/// with the dense inverse B_k^{-1} precomputed here.  Entries of a row are
+///     x_{R_k} = B_k^{-1} (rhs - old) - G_k x_{R_{k-1}},   B_k = D + (in-block lower part),
+/// with the dense inverse B_k^{-1} and the folded coupling G_k = B_k^{-1} N_k
+/// (N_k: the entries whose columns block k-1 solves) precomputed here in
+/// extended precision.  Only G_k x_{R_{k-1}} -- a dense product over the last
+/// 8 mf rows of block k-1 -- is on the block-to-block critical path; the
+/// inverse product no longer is.  Entries of a row are
 ///   in-block lower  -> folded into B_k;
-///   fresh           -> columns solved by blocks k-F .. k-1 (summed on the
-///                      critical path, after block k-1);
+///   fresh           -> columns solved by block k-1 (F = 1): folded into G_k;
 ///   old             -> columns solved by blocks <= k-F-1 (final once block
 ///                      k-F-1 is done) or solved later (Gauss-Seidel's old values,
 ///                      in-block ones included); summed ahead of time by the
 ///                      worker warps, split into `parts` interleaved parts.
 /// One block = one fetch unit (one cp.async.bulk):
-///   header int32[4]: mo (old slots per part), 0, bytes, mf (fresh slots)
+///   header int32[4]: mo (old slots per part), 0, bytes, mf (groups of four column pairs of G_k)
 ///   rows   int32[32]                 at 16 (-1 on padding lanes)
 ///   inv    double[16][32][2]         at 144: entries (L, 2p), (L, 2p+1) of
 ///                                    B_k^{-1} at (p * 32 + L) * 16 bytes
-///   fresh  {int32 col, pad, double val}[mf][32] at kBlkFreshOff
+///   G      double[4 mf][32][2]       at kBlkFreshOff: pair q of lane L holds
+///                                    G_k(L, 30 - 2q), G_k(L, 31 - 2q)
 ///   old    per part q: cols int32[mo][32], vals double[mo][32] at
-///          kBlkFreshOff + 512 mf + q * 384 mo  (slot s of lane L at s*32+L)
+///          kBlkFreshOff + 2048 mf + q * 384 mo  (slot s of lane L at s*32+L)
 /// Padding slots are (column n, +0.0) against the zero slot x[n].  `table`
 /// holds (offset / 16, bytes, mf, 0) per block.
 constexpr int kBlkRows = 32;
 constexpr int kBlkInvOff = 144;
 constexpr int kBlkFreshOff = kBlkInvOff + 8 * kBlkRows * kBlkRows;
-constexpr int kBlkMaxParts = 6;  // worker warps (8 - kBlkSolvers)
-constexpr int kBlkSolvers = 2;   // solver warps in rotation
-constexpr int kBlkFresh = 1;     // fresh distance F: columns of blocks k-F .. k-1
+#ifndef PHI_BLK_SOLVERS
+#define PHI_BLK_SOLVERS 2
+#endif
+constexpr int kBlkSolvers = PHI_BLK_SOLVERS;   // solver warps in rotation
+constexpr int kBlkMaxParts = 8 - kBlkSolvers;  // worker warps
+constexpr int kBlkFresh = 1;     // fresh distance F: columns of block k-1 (folded into G_k)
 struct BlkStream {
     std::vector<unsigned char> stream;
-    std::vector<int> table;  // 4 per block: offset / 16, bytes, fresh slots, 0
+    std::vector<int> table;  // 4 per block: offset / 16, bytes, G pair groups, 0
     int n = 0, n_blocks = 0, parts = 1, mf0 = 0, lookahead = 0, max_unit_bytes = 0;
     int win = 0;   // rolling-window layout (below), 0: absolute columns
     int desc = 0;  // solve order descending: block k, lane l solves row n - 1 - (32 k + l)
@@ -171,7 +178,7 @@ struct BlkStream {
 /// through to global memory.  Columns in the stream are then window slots
 /// (col & (WZ - 1); padding: the zero slot WZ) and the old entries are packed
 /// with 16-bit columns: per part q, cols uint16[mo][32], vals double[mo][32]
-/// at kBlkFreshOff + 512 mf + q * 320 mo.
+/// at kBlkFreshOff + 2048 mf + q * 320 mo.
 constexpr int kBlkMaxWin = 4096;
 /// Largest distance in solve order between a row and a column it reads, over
 /// both factors (the band of the IgA ILUT factors).

@@ -16,7 +16,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib_trace" if os.environ.get("PHI_TRACE") == "1" else "_lib", "libphi_engine.so")
+LIB_PATH = os.path.join(HERE, "_lib_trace" if os.environ.get("PHI_TRACE") == "1"
+                        else ("_lib_" + os.environ["PHI_VARIANT"] if os.environ.get("PHI_VARIANT") else "_lib"),
+                        "libphi_engine.so")
 
 PHI_OK, PHI_ERR_INVALID, PHI_ERR_NOT_CONVERGED, PHI_ERR_CUDA, PHI_ERR_RUNTIME = range(5)
 SOURCE_CONSTANT, SOURCE_SIN_EXP, SOURCE_SIN = 0, 1, 2
@@ -315,9 +317,11 @@ class PMultigridHierarchy:
         _check(lib().phi_hier_spmm(self.h, _p(X), _p(Y), nrhs, 0))
         return Y
 
-    def time_kernel(self, which: int, nrhs: int, reps: int = 5, flush_l2: bool = True) -> float:
+    def time_kernel(self, which: int, nrhs: int, reps: int = 5, flush_l2: int = 1) -> float:
         """Average device ms of one SpMM (which 0) or one V-cycle from x0 = 0
-        (which 1) on nrhs seeded N(0,1) right-hand sides (BASELINE config 5)."""
+        (which 1) on nrhs seeded N(0,1) right-hand sides (BASELINE config 5).
+        flush_l2 1: L2 flushed, events around each launch; 2 (SpMM): back-to-back
+        launches over four copies of the operator (phi_hier_time)."""
         ms = C.c_double()
         _check(lib().phi_hier_time(self.h, which, nrhs, reps, int(flush_l2), C.byref(ms)))
         return ms.value

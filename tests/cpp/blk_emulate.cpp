@@ -1,6 +1,6 @@
 // Host-side check of the block-recurrence sweep schedules (setup_host.hpp
 // BlkStream): the stream images are decoded and executed block by block on the
-// CPU, in the order the device runs them (old sums, fresh sums, dense block
+// CPU, in the order the device runs them (old sums, dense block
 // inverse), and compared with the plain sequential sweeps of the reference
 // (ilut.hpp:146-163 substitutions, solvers.hpp:80-99 Gauss-Seidel).
 // Test infrastructure only (tests/test_blk_schedule.py builds and runs it).
@@ -37,8 +37,8 @@ static HostCsr stencil_matrix(int m, int w, unsigned seed) {
 }
 
 // Execute a BlkStream sweep on x (rhs: separate vector, or x itself), block
-// by block in the device's order: old sums (per worker part), fresh sums,
-// dense block inverse.
+// by block in the device's order: old sums (per worker part), dense block
+// inverse, folded coupling to the previous block.
 // Rolling-window streams (bs.win > 0) read every column from a window of
 // win slots (initialised to NaN, so a read of a slot not yet solved in this
 // sweep poisons the result) plus the zero slot, with 16-bit old columns.
@@ -50,6 +50,7 @@ static void run_blk(const BlkStream& bs, std::vector<double>& x, const std::vect
     if (W) wv[W] = 0.0;
     double* xr = W ? wv.data() : x.data();  // what the column indices address
     const size_t cbytes = W ? 2 : 4;
+    double zprev[32] = {0.0};  // the previous block's values in solve order
     for (int k = 0; k < bs.n_blocks; ++k) {
         const unsigned char* u = bs.stream.data() + static_cast<size_t>(bs.table[4 * k]) * 16;
         int hdr[4];
@@ -63,7 +64,7 @@ static void run_blk(const BlkStream& bs, std::vector<double>& x, const std::vect
         for (int l = 0; l < 32; ++l) {
             double s = 0.0;
             for (int p = 0; p < P; ++p) {  // worker parts
-                const unsigned char* pb = u + kBlkFreshOff + 512 * mf + p * (32 * cbytes + 256) * mo;
+                const unsigned char* pb = u + kBlkFreshOff + 2048 * mf + p * (32 * cbytes + 256) * mo;
                 const double* ov = reinterpret_cast<const double*>(pb + 32 * cbytes * mo);
                 for (int q = 0; q < mo; ++q) {
                     int c = 0;
@@ -79,23 +80,21 @@ static void run_blk(const BlkStream& bs, std::vector<double>& x, const std::vect
             }
             t[l] = (rows[l] >= 0 ? rhs[rows[l]] : 0.0) - s;
         }
-        for (int l = 0; l < 32; ++l)  // fresh sums
-            for (int q = 0; q < mf; ++q) {
-                int c;
-                double v;
-                std::memcpy(&c, fr + (q * 32 + l) * 16, 4);
-                std::memcpy(&v, fr + (q * 32 + l) * 16 + 8, 8);
-                t[l] -= v * xr[c];
-            }
+        const double* gv = reinterpret_cast<const double*>(fr);
         for (int l = 0; l < 32; ++l) {
             z[l] = 0.0;
             for (int j = 0; j < 32; ++j) z[l] += iv[((j / 2) * 32 + l) * 2 + (j & 1)] * t[j];
+            // folded coupling: minus G_k times the last 8 mf values of block k-1
+            for (int q = 0; q < 4 * mf; ++q)
+                z[l] -= gv[(q * 32 + l) * 2] * zprev[30 - 2 * q] + gv[(q * 32 + l) * 2 + 1] * zprev[31 - 2 * q];
         }
-        for (int l = 0; l < 32; ++l)
+        for (int l = 0; l < 32; ++l) {
+            zprev[l] = z[l];
             if (rows[l] >= 0) {
                 x[rows[l]] = z[l];
                 if (W) wv[rows[l] & (W - 1)] = z[l];
             }
+        }
     }
     x.resize(n);
 }

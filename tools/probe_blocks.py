@@ -51,8 +51,10 @@ if len(g) > 8:
     done = T[g, 5]
     per = np.diff(done)
     print(f"blocks traced {len(g)}: per-block {np.median(per):.0f} cycles (median), p90 {np.percentile(per, 90):.0f}")
-    print(f"  wait parts-in (1-0) {np.median(T[g, 1] - T[g, 0]):.0f}, loads+hand wait (2-1) {np.median(T[g, 2] - T[g, 1]):.0f}, "
-          f"fresh (3-2) {np.median(T[g, 3] - T[g, 2]):.0f}, inverse+store (5-3) {np.median(T[g, 5] - T[g, 3]):.0f}")
+    print(f"  unit landed (1-0) {np.median(T[g, 1] - T[g, 0]):.0f}, inverse + G loads (7-1) {np.median(T[g, 7] - T[g, 1]):.0f}, "
+          f"parts + inverse product (4-7) {np.median(T[g, 4] - T[g, 7]):.0f}, hand wait (2-4) {np.median(T[g, 2] - T[g, 4]):.0f}, "
+          f"chain (3-2) {np.median(T[g, 3] - T[g, 2]):.0f}, store+signal (5-3) {np.median(T[g, 5] - T[g, 3]):.0f}, "
+          f"bookkeeping (6-5) {np.median(T[g, 6] - T[g, 5]):.0f}")
     w = T[g, 8] > 0
     if w.any():
         gw = g[w]
