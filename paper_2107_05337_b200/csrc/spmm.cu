@@ -49,7 +49,7 @@ void launch_spmv_w(const DevStencil& A, const double* At, const double* x, doubl
 template <int W, int NRHS>
 void launch_spmm_wn(const DevStencil& A, const double* At, const double* X, double* Y, cudaStream_t s) {
     using Cfg = spk::SpmmCfg<W, 2>;
-    auto kern = spk::spmm_tma_kernel<W, NRHS, 2, 0>;
+    auto kern = spk::spmm_tma_kernel<W, NRHS, 2>;
     static bool ready = false;
     if (!ready) {
         PHI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem));

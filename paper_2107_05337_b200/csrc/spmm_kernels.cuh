@@ -229,7 +229,7 @@ struct SpmmCfg {
     static constexpr size_t smem = (size_t)NS * tile_bytes;
 };
 
-template <int W, int NRHS, int NS, int PF = 0>
+template <int W, int NRHS, int NS>
 __global__ void __launch_bounds__(288, 1)
     spmm_tma_kernel(const DevStencil A, const double* __restrict__ At, const double* __restrict__ X,
                     double* __restrict__ Y) {
@@ -294,11 +294,6 @@ __global__ void __launch_bounds__(288, 1)
                     const int row = min(max(xb + c, 0), n - 1);
                     xw[c] = __ldg(reinterpret_cast<const double2*>(X + (size_t)row * NRHS + 2 * lg));
                 }
-            }
-            if (PF && interior && dv + G < W) {  // the next stencil row's x rows towards L1
-                const double* xn = X + (size_t)(xb + G * cu) * NRHS + 2 * lg;
-#pragma unroll
-                for (int c = 0; c < NX; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(xn + (size_t)c * NRHS));
             }
             const unsigned ap = sm + (unsigned)dv * SB;
 #pragma unroll

@@ -122,19 +122,19 @@ static void run_spmv(int p, const DevStencil& A, double* const* At, const double
     time_it(name, p, 1, bytes, flops, [&](int c) { kern<<<grid, Cfg::threads, Cfg::smem>>>(A, At[c], x, y); });
 }
 
-template <int W, int B, int NS, int PF = 0>
+template <int W, int B, int NS>
 static void run_spmm(int p, const DevStencil& A, double* const* At, const double* X, double* Y, const double* Yref,
                      double bytes, double flops, int grid) {
     using Cfg = spk::SpmmCfg<W, NS>;
     if (Cfg::smem > 227 * 1024) return;
-    auto kern = spk::spmm_tma_kernel<W, B, NS, PF>;
+    auto kern = spk::spmm_tma_kernel<W, B, NS>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem));
     CK(cudaMemset(Y, 0, (size_t)A.ru * A.rv * 8 * B));
     kern<<<grid, Cfg::threads, Cfg::smem>>>(A, At[0], X, Y);
     CK(cudaDeviceSynchronize());
     const double err = check(Y, Yref, (size_t)A.ru * A.rv * B);
     char name[96];
-    snprintf(name, sizeof name, "spmm_tma s%d g%d pf%d e%.0e", NS, grid, PF, err);
+    snprintf(name, sizeof name, "spmm_tma s%d g%d e%.0e", NS, grid, err);
     time_it(name, p, B, bytes, flops, [&](int c) { kern<<<grid, Cfg::threads, Cfg::smem>>>(A, At[c], X, Y); });
 }
 
