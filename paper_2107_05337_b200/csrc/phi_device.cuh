@@ -1894,16 +1894,19 @@ __global__ void __launch_bounds__(NT, 1)
     cl_init();
     blk_init();
     const DevHier& H = hier_shared(H_param);
-    const Ws& w = carve_shared(ws_base + (size_t)blockIdx.x * ws_stride, H, P, smem);
+    // one workspace per cluster (a cluster of one CTA without clusters); cluster c takes c, c + nclusters, ...
+    const int cid = blockIdx.x / cl_size(), ncl = gridDim.x / cl_size();
+    const int part = cl_rank(), parts = cl_size();
+    const Ws& w = carve_shared(ws_base + (size_t)cid * ws_stride, H, P, smem);
     const int n = H.n_p;
-    for (int t = blockIdx.x; t < nrhs; t += gridDim.x) {
-        cta_copy(w.b, B + (size_t)t * ldb, n);
-        cta_copy(w.x, X + (size_t)t * ldx, n);
-        __syncthreads();
+    for (int t = cid; t < nrhs; t += ncl) {
+        cta_copy(w.b, B + (size_t)t * ldb, n, part, parts);
+        cta_copy(w.x, X + (size_t)t * ldx, n, part, parts);
+        cl_sync();
         vcycle<DEG>(H, w);
         double* out = X + (size_t)t * ldx;
-        for (int i = threadIdx.x; i < n; i += NT) out[i] = w.x[i];
-        __syncthreads();
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) out[i] = w.x[i];
+        cl_sync();
     }
 }
 
@@ -2059,6 +2062,47 @@ static inline int occupancy_grid(K kernel, size_t smem, int want) {
 }
 
 
+// The largest cluster size (a power of two <= cl_max) at which the device can
+// keep n_tasks clusters of `kernel` resident at once (every task its own
+// cluster, one round), 1 if none: cudaOccupancyMaxActiveClusters, cached.
+template <class K>
+static int pick_cluster(K kernel, size_t smem, int n_tasks, int cl_max) {
+    static int cached_active[6] = {-1, -1, -1, -1, -1, -1};  // by log2(cl)
+    static size_t cached_smem = 0;
+    if (cached_smem != smem) {
+        for (int& c : cached_active) c = -1;
+        cached_smem = smem;
+    }
+    for (int cl = cl_max, lg = 0; cl > 1; cl /= 2) {
+        if (cl & (cl - 1)) return 1;  // powers of two only
+        for (lg = 0; (1 << lg) < cl; ++lg) {
+        }
+        if (lg > 5) continue;
+        if (cached_active[lg] < 0) {
+            if (cl > 8) PHI_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3((unsigned)cl);
+            q.blockDim = dim3(NT);
+            q.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = (unsigned)cl;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, kernel, &q) != cudaSuccess) {
+                (void)cudaGetLastError();
+                ncl = 0;
+            }
+            cached_active[lg] = ncl;
+        }
+        if (cached_active[lg] >= n_tasks) return cl;
+    }
+    return 1;
+}
+
 template <int DEG>
 int DegLaunch<DEG>::max_slots(const DevHier& H) {
     return occupancy_grid(phi_wave_kernel<DEG>, phi_smem_bytes(H), 1 << 30);
@@ -2105,7 +2149,16 @@ void DegLaunch<DEG>::wave(const DevHier& H, const DevStencil& Am, const WaveArgs
     int n_sm = 0, dev = 0;
     PHI_CUDA(cudaGetDevice(&dev));
     PHI_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    if (!H.exact && !a.no_cluster && cl > 1 && a.n_tasks * cl <= n_sm) {
+    // the largest cluster (a power of two up to the device's limit) that still
+    // gives every task its own cluster: 16 CTAs up to 9 tasks, 8 up to 18, ...
+    int use = cl;
+    if (a.n_tasks * cl > n_sm) {  // more than a few tasks: the largest size at which all their clusters are resident
+        use = (!H.exact && !a.no_cluster && cl > 1 && H.n_p >= 4096)  // (small systems: the barriers outweigh the split)
+                  ? pick_cluster(phi_wave_kernel<DEG>, smem, a.n_tasks, cl / 2)
+                  : 1;
+    }
+    if (!H.exact && !a.no_cluster && use > 1) {
+        const int cl = use;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(a.n_tasks * cl));
         cfg.blockDim = dim3(NT);
@@ -2141,7 +2194,32 @@ void DegLaunch<DEG>::vcycle(const DevHier& H, const double* B, long long ldb, do
     const SmemPlan P = phi_smem_plan(H);
     const size_t smem = (size_t)P.total * 8;
     occupancy_grid(vcycle_kernel<DEG>, smem, grid);
-    vcycle_kernel<DEG><<<grid, NT, smem, s>>>(H, B, ldb, X, ldx, nrhs, P, ws, ws_stride);
+    // few right-hand sides (reassociated mode): each on a cluster of CTAs, as
+    // the single-right-hand-side waves (developer override: PHI_CLUSTER)
+    int n_sm = 0, dev = 0;
+    PHI_CUDA(cudaGetDevice(&dev));
+    PHI_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    int cl = kPhiClusterWide;
+    if (const char* e = std::getenv("PHI_CLUSTER")) cl = std::atoi(e);
+    // every right-hand side its own resident cluster (small systems: the barriers outweigh the split)
+    cl = (!H.exact && cl > 1 && H.n_p >= 4096) ? pick_cluster(vcycle_kernel<DEG>, smem, nrhs, cl) : 1;
+    if (cl > 1) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(nrhs * cl));
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PHI_CUDA(cudaLaunchKernelEx(&cfg, vcycle_kernel<DEG>, H, B, ldb, X, ldx, nrhs, P, ws, ws_stride));
+    } else {
+        vcycle_kernel<DEG><<<grid, NT, smem, s>>>(H, B, ldb, X, ldx, nrhs, P, ws, ws_stride);
+    }
     PHI_CUDA(cudaGetLastError());
 }
 
