@@ -75,8 +75,8 @@ struct DevHLevel {
 };
 
 constexpr int kMaxH = 12;
-/// Scratch of the cluster dense coarse product: r copy (<= 1024) + 128 partials.
-constexpr int kClScratch = 1024 + 160;
+/// Scratch of the cluster dense coarse product: r copy (<= 1024) + 256 partials.
+constexpr int kClScratch = 1024 + 288;
 /// Longest grid line of a line Gauss-Seidel sweep (32 lanes x 8 rows).
 constexpr int kLineMax = 256;
 /// Shortest grid line swept by lines (shorter levels: block sweeps).

@@ -793,10 +793,20 @@ constexpr int kHandBar = 1;  // ids 1 .. kBlkSolvers
 // y = B^{-1} (rhs - old) through a shared-memory broadcast, y pinned before
 // the hand-off wait (nothing but the chain's own loads and fused
 // multiply-adds after it), then y - G_k x_{g-1} in four chains.
+// Once every part is in, the workers are done with the block's unit, and so
+// is this warp (inverse and G_k are in registers): lane 0 refills the ring slot
+// right there (refill_bytes > 0) -- a whole inverse product, chain and store
+// earlier than after the block, which the TMA stream needs (issuing it ~500
+// cycles later cost 20 % of the sweep).
+struct BlkRefill {
+    unsigned dst, bar;
+    const unsigned char* src;
+    int bytes;
+};
 template <int NG>
 __device__ __forceinline__ double fold_block(unsigned gp, unsigned xp, const double (&iv)[32], double rhs, unsigned tb,
                                              unsigned cnt_a, int P, unsigned cbuf_a, int lane, int hand_id,
-                                             long long* tr) {
+                                             const BlkRefill& rf, long long* tr) {
     double gq[NG > 0 ? 8 * NG : 1];
 #pragma unroll
     for (int p2 = 0; p2 < 4 * NG; ++p2) lds_v2f64(gp + 512u * p2, gq[2 * p2], gq[2 * p2 + 1]);
@@ -807,6 +817,10 @@ __device__ __forceinline__ double fold_block(unsigned gp, unsigned xp, const dou
 #pragma unroll
     for (int q = 0; q < kBlkMaxParts; ++q)
         part[q] = q < P ? vlds_f64(cbuf_a + 8u * (q * 32 + lane) + (unsigned)(all - P)) : 0.0;
+    // the unit is consumed: its slot takes the unit n_slots blocks ahead.  (Every shared load of
+    // the unit by this warp has returned -- the acquire load above was issued after them -- and the
+    // workers' loads precede their release of the parts.)
+    if (lane == 0 && rf.bytes > 0) bulk_fetch(rf.dst, rf.src, rf.bytes, rf.bar);
     double old = 0.0;
 #pragma unroll
     for (int q = 0; q < kBlkMaxParts; ++q) old = old + part[q];
@@ -926,13 +940,15 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             const int hand_id = g > 0 ? kHandBar + (w == 0 ? NS - 1 : w - 1) : -1;
             const unsigned cnt_a = cnt + 4u * (g & (kBlkHand - 1));
             const unsigned cbuf_a = cbuf + 8u * ((g & (kBlkHand - 1)) * kBlkMaxParts * 32);
+            BlkRefill rf{ring + slot * slot_bytes, bar + 8u * slot, stream + (size_t)refill.x * 16,
+                         g + n_slots < total ? refill.y : 0};
             double z;
             switch (mf) {
-                case 0: z = fold_block<0>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
-                case 1: z = fold_block<1>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
-                case 2: z = fold_block<2>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
-                case 3: z = fold_block<3>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
-                default: z = fold_block<4>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, tr); break;
+                case 0: z = fold_block<0>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, rf, tr); break;
+                case 1: z = fold_block<1>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, rf, tr); break;
+                case 2: z = fold_block<2>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, rf, tr); break;
+                case 3: z = fold_block<3>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, rf, tr); break;
+                default: z = fold_block<4>(gp, xp, iv, rhs, tb, cnt_a, P, cbuf_a, lane, hand_id, rf, tr); break;
             }
             if (tr) tr[3] = clock64() + (long long)(z == 1.2345);
             // the values in solve order, for block g+1's chain
@@ -951,11 +967,7 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             if (lane == 0) st_release_s32(prog, g);  // monotone; read by the workers (off the chain)
             if (tr) tr[5] = clock64();
             // ---- off the chain: bookkeeping for this solver's next block
-            if (lane == 0) {
-                st_volatile_s32(cnt + 4u * (g & (kBlkHand - 1)), 0);  // reused by block g + kBlkHand
-                if (g + n_slots < total)  // block g's unit is consumed: refill its slot
-                    bulk_fetch(ring + slot * slot_bytes, stream + (size_t)refill.x * 16, refill.y, bar + 8u * slot);
-            }
+            if (lane == 0) st_volatile_s32(cnt + 4u * (g & (kBlkHand - 1)), 0);  // reused by block g + kBlkHand
             if (tr) tr[6] = clock64();
             slot += NS;
             while (slot >= n_slots) slot -= n_slots;
@@ -1460,31 +1472,45 @@ __device__ __noinline__ void dense_apply(const double* __restrict__ c, int n, co
 __device__ __noinline__ void dense_apply_cl(const double* __restrict__ c, int n, const double* r_main,
                                             double* x_main, int part, int parts, double* scr) {
     double* rl = scr;           // n doubles
-    double* pp = scr + n + 1;   // 128 partial sums of the second column half
+    double* pp = scr + n + 1;   // 8 x 32 partial sums (kClScratch leaves room for them)
     for (int j = threadIdx.x; j < n; j += NT) rl[j] = r_main[j];
     __syncthreads();
     const int chunk = (n + parts - 1) / parts;
     const int r0 = part * chunk, r1 = min(n, r0 + chunk);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int jh = (n + 1) / 2;
-    for (int base = r0; base < r1; base += 128) {
-        const int i = base + (w & 3) * 32 + lane;  // this thread's row
-        const int j0 = (w >> 2) ? jh : 0, j1 = (w >> 2) ? n : jh;
+    // rw warps cover 32 rows each, the other warps split the columns: with 61
+    // rows per CTA (n = 961 on 16 CTAs) two row warps and four column quarters
+    const int rw = chunk > 64 ? 4 : (chunk > 32 ? 2 : 1), cs = 8 / rw;
+    const int wr = w % rw, wc = w / rw;
+    const int j0 = (int)((long long)n * wc / cs), j1 = (int)((long long)n * (wc + 1) / cs);
+    for (int base = r0; base < r1; base += 32 * rw) {
+        const int i = base + wr * 32 + lane;  // this thread's row
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (i < r1) {
+            // sixteen operator loads in flight per thread: the product is bound by
+            // the latency of the loads from L2 (each CTA streams n^2 / parts entries)
             int j = j0;
-            for (; j + 4 <= j1; j += 4) {
-                a0 = __fma_rn(__ldg(c + (size_t)j * n + i), rl[j], a0);
-                a1 = __fma_rn(__ldg(c + (size_t)(j + 1) * n + i), rl[j + 1], a1);
-                a2 = __fma_rn(__ldg(c + (size_t)(j + 2) * n + i), rl[j + 2], a2);
-                a3 = __fma_rn(__ldg(c + (size_t)(j + 3) * n + i), rl[j + 3], a3);
+            for (; j + 16 <= j1; j += 16) {
+                double v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = __ldg(c + (size_t)(j + u) * n + i);
+#pragma unroll
+                for (int u = 0; u < 16; u += 4) {
+                    a0 = __fma_rn(v[u], rl[j + u], a0);
+                    a1 = __fma_rn(v[u + 1], rl[j + u + 1], a1);
+                    a2 = __fma_rn(v[u + 2], rl[j + u + 2], a2);
+                    a3 = __fma_rn(v[u + 3], rl[j + u + 3], a3);
+                }
             }
             for (; j < j1; ++j) a0 = __fma_rn(__ldg(c + (size_t)j * n + i), rl[j], a0);
         }
-        const double s = (a0 + a1) + (a2 + a3);
-        if (w >= 4) pp[(w & 3) * 32 + lane] = s;
+        pp[w * 32 + lane] = (a0 + a1) + (a2 + a3);
         __syncthreads();
-        if (w < 4 && i < r1) x_main[i] = x_main[i] + (s + pp[(w & 3) * 32 + lane]);
+        if (wc == 0 && i < r1) {
+            double s = pp[wr * 32 + lane];
+            for (int q = 1; q < cs; ++q) s = s + pp[(q * rw + wr) * 32 + lane];  // column parts in order
+            x_main[i] = x_main[i] + s;
+        }
         __syncthreads();
     }
 }
