@@ -1756,6 +1756,7 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
                           int k, double* sh) {
     const int n = H.n_p;
     const int part = cl_rank(), parts = cl_size();
+    pstamp(50);
     // ---- right-hand side and initial guess
     if (a.mode == kModeStep) {
         const double* uprev = a.U ? a.U + (size_t)(k - 1) * n : a.UPREV + (size_t)task * a.ldu;
@@ -1788,11 +1789,13 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
             cta_copy(w.x, a.X + (size_t)task * a.ldx, n, part, parts);
     }
     cl_sync();
+    pstamp(51);
 
     // ---- p-multigrid solve
     int iters = 0, conv = 0;
     double rel = 0.0;
     const double bnorm = sqrt(cta_ordered_dot(w.b, w.b, n, w.dot, sh, H.exact != 0));
+    pstamp(52);
     if (bnorm == 0.0) {
         cta_fill(w.x, 0.0, n, part, parts);  // zero rhs -> zero solution, not the guess
         conv = 1;
@@ -1821,6 +1824,7 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
         }
     }
 
+    pstamp(53);
     // ---- bookkeeping (SolveStats::record, theta.hpp:81-84)
     if (threadIdx.x == 0 && part == 0) {
         if (a.stat) {
@@ -1877,6 +1881,7 @@ __device__ __noinline__ void phi_point(const DevHier& H, const DevStencil& Am, c
         for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) out[i] = w.x[i];
     }
     cl_sync();
+    pstamp(54);
 }
 
 // SIDE: a second instantiation for the side-stream waves that run while the
