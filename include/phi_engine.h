@@ -266,6 +266,25 @@ void phi_comm_free(phi_comm* c);
 /* attach (null: detach -- single process); the comm must outlive its use */
 int phi_mgrit_set_comm(phi_mgrit* g, phi_comm* c);
 
+/* ---- host-side setup routines (no device needed) --------------------------
+ * The inputs of the device assembly and of the coarse direct solve, exposed so
+ * they can be pinned against the reference on a CPU-only box.
+ *
+ * phi_setup_tables_1d: the per-direction quadrature / basis tables of an open
+ * uniform knot vector on [0,1] -- gauss_legendre_01 (quadrature.hpp:17-44),
+ * open_uniform_knots (spline.hpp:48-63), eval_values_and_derivs
+ * (spline.hpp:104-130), laid out as detail::DirTables (assembly.hpp:124-151):
+ * nodes/weights [e*nq + q], vals/ders [(e*nq + q)*(degree+1) + a], first [e].
+ * phi_setup_dense_lu: DenseLU's factors and permutation (solvers.hpp:136-167)
+ * of a dense row-major n x n matrix; lu: n*n, piv: n.
+ * phi_setup_level_steps: the time-grid hierarchy rule of
+ * MgritSolver::build_levels (mgrit.hpp:217-233); cycle as phi_mgrit_config.
+ * Writes at most cap step counts, *n_levels = the number of levels. */
+int phi_setup_tables_1d(int degree, int n_elements, int nq, double* nodes, double* weights, double* vals,
+                        double* ders, int* first);
+int phi_setup_dense_lu(int n, const double* a, double* lu, int* piv);
+int phi_setup_level_steps(int nt, int m, int cycle, int coarse_floor, int* steps, int cap, int* n_levels);
+
 /* Developer knob (not part of the reference API): warps used by the sync-free
  * triangular solves / Gauss-Seidel sweeps and the readiness-poll back-off. */
 int phi_dev_tuning(int tri_warps, int gs_warps, int sleep_ns);

@@ -128,6 +128,8 @@ def ref_lib():
         L.ref_mgrit_cycle.argtypes = [_vp, _i]
         L.ref_mgrit_residual_norm.argtypes = [_vp, _i, _vp]
         L.ref_mgrit_points.argtypes = [_vp, _i, _i, _i, _i, _vp]
+        L.ref_tables_1d.argtypes = [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]
+        L.ref_dense_solve.argtypes = [_i, _vp, _vp, _vp]
         L.ref_mgrit_residual_iters.argtypes = [_vp, _i, _i, _vp]
         _ref = L
     return _ref
@@ -136,6 +138,47 @@ def ref_lib():
 def _ref_err():
     return ref_lib().ref_last_error().decode()
 
+
+
+def ref_tables_1d(degree: int, n_elements: int, nq: int) -> dict:
+    """detail::DirTables of an open uniform knot vector on [0, 1] (assembly.hpp:124-151)."""
+    pts = n_elements * nq
+    out = dict(nodes=np.empty(pts), weights=np.empty(pts), vals=np.empty((pts, degree + 1)),
+               ders=np.empty((pts, degree + 1)), first=np.empty(n_elements, dtype=np.int32))
+    L = ref_lib()
+    if L.ref_tables_1d(degree, n_elements, nq, _p(out["nodes"]), _p(out["weights"]), _p(out["vals"]),
+                       _p(out["ders"]), _p(out["first"])):
+        raise ValueError(L.ref_last_error().decode())
+    return out
+
+
+def ref_dense_solve(a, b) -> np.ndarray:
+    """DenseLU(a).solve(b) (solvers.hpp:102-172)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty_like(b)
+    L = ref_lib()
+    if L.ref_dense_solve(a.shape[0], _p(a), _p(b), _p(x)):
+        raise RuntimeError(L.ref_last_error().decode())
+    return x
+
+
+def lu_substitute(lu, piv, b) -> np.ndarray:
+    """Permute, forward- and back-substitute with packed LU factors in the order
+    of DenseLU::solve (solvers.hpp:118-133); plain Python floats (no fusing)."""
+    n = len(piv)
+    x = [float(b[int(piv[i])]) for i in range(n)]
+    for i in range(n):
+        s = x[i]
+        for j in range(i):
+            s -= float(lu[i][j]) * x[j]
+        x[i] = s
+    for i in range(n - 1, -1, -1):
+        s = x[i]
+        for j in range(i + 1, n):
+            s -= float(lu[i][j]) * x[j]
+        x[i] = s / float(lu[i][i])
+    return np.array(x)
 
 class RefDisc:
     """miga::SpatialDiscretization::build on the unit square (pmultigrid.hpp:94-158)."""

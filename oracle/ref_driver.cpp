@@ -13,6 +13,7 @@
 //   ThetaStepper                      theta.hpp:92-146
 //   sequential_integrate              theta.hpp:216-237
 //   MgritSolver / mgrit_solve         mgrit.hpp:50-331
+//   detail::DirTables, DenseLU        assembly.hpp:124-151, solvers.hpp:102-172
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -530,6 +531,48 @@ int ref_mgrit_residual_iters(void* p, int level, int workers, int* iters) {
         for (auto& t : th) t.join();
         for (const auto& e : errs)
             if (!e.empty()) throw std::runtime_error(e);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// The reference's per-direction quadrature / basis tables of an open uniform
+// knot vector on [0, 1] (detail::DirTables::build over gauss_legendre_01 and
+// eval_values_and_derivs).  Arrays sized by the caller: nodes/weights nel*nq,
+// vals/ders nel*nq*(degree+1), first nel.
+int ref_tables_1d(int degree, int n_elements, int nq, double* nodes, double* weights, double* vals,
+                  double* ders, int* first) {
+    try {
+        const KnotVector kv = open_uniform_knots(degree, n_elements, 0.0, 1.0);
+        const auto t = detail::DirTables::build(kv, nq);
+        std::memcpy(nodes, t.quad.nodes.data(), sizeof(double) * t.quad.nodes.size());
+        std::memcpy(weights, t.quad.weights.data(), sizeof(double) * t.quad.weights.size());
+        std::memcpy(vals, t.vals.data(), sizeof(double) * t.vals.size());
+        std::memcpy(ders, t.ders.data(), sizeof(double) * t.ders.size());
+        std::memcpy(first, t.first.data(), sizeof(int) * t.first.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// DenseLU(a).solve(b) for a dense row-major n x n matrix (zeros are not stored).
+int ref_dense_solve(int n, const double* a, const double* b, double* x) {
+    try {
+        SparseMatrix m;
+        m.n_rows = m.n_cols = n;
+        m.row_offsets.assign(1, 0);
+        for (int i = 0; i < n; ++i) {
+            for (int j = 0; j < n; ++j)
+                if (a[static_cast<std::size_t>(i) * n + j] != 0.0) {
+                    m.col_indices.push_back(j);
+                    m.values.push_back(a[static_cast<std::size_t>(i) * n + j]);
+                }
+            m.row_offsets.push_back(m.nnz());
+        }
+        const Vector out = DenseLU(m).solve(Vector(b, b + n));
+        std::memcpy(x, out.data(), sizeof(double) * n);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -762,4 +762,47 @@ int phi_mgrit_set_comm(phi_mgrit* g, phi_comm* c) {
     return guarded([&] { g->g->set_comm(c ? c->c.get() : nullptr); });
 }
 
+int phi_setup_tables_1d(int degree, int n_elements, int nq, double* nodes, double* weights, double* vals,
+                        double* ders, int* first) {
+    return guarded([&] {
+        if (degree > 30) throw InvalidArgument("phi_setup_tables_1d: degree must be <= 30");
+        const Tables1D tb = build_tables(open_uniform_knots(degree, n_elements), nq);
+        std::copy(tb.nodes.begin(), tb.nodes.end(), nodes);
+        std::copy(tb.weights.begin(), tb.weights.end(), weights);
+        std::copy(tb.vals.begin(), tb.vals.end(), vals);
+        std::copy(tb.ders.begin(), tb.ders.end(), ders);
+        std::copy(tb.first.begin(), tb.first.end(), first);
+    });
+}
+
+int phi_setup_dense_lu(int n, const double* a, double* lu, int* piv) {
+    return guarded([&] {
+        if (n < 0) throw InvalidArgument("phi_setup_dense_lu: n must be >= 0");
+        HostCsr m;
+        m.n_rows = m.n_cols = n;
+        m.row_offsets.assign(1, 0);
+        for (int i = 0; i < n; ++i) {
+            for (int j = 0; j < n; ++j) {
+                const double v = a[static_cast<size_t>(i) * n + j];
+                if (v == 0.0) continue;
+                m.col_indices.push_back(j);
+                m.values.push_back(v);
+            }
+            m.row_offsets.push_back(m.nnz());
+        }
+        const DenseLUHost f = dense_lu_factor(m);
+        std::copy(f.lu.begin(), f.lu.end(), lu);
+        std::copy(f.piv.begin(), f.piv.end(), piv);
+    });
+}
+
+int phi_setup_level_steps(int nt, int m, int cycle, int coarse_floor, int* steps, int cap, int* n_levels) {
+    return guarded([&] {
+        const std::vector<int> s = mgrit_level_steps(nt, m, cycle, coarse_floor);
+        for (int l = 0; l < static_cast<int>(s.size()) && l < cap; ++l) steps[l] = s[l];
+        *n_levels = static_cast<int>(s.size());
+    });
+}
+
+
 }  // extern "C"

@@ -501,21 +501,31 @@ Mgrit::Mgrit(std::shared_ptr<const Disc> disc_, const ProblemOptions& ps_, const
     PHI_CUDA(cudaStreamSynchronize(stream));
 }
 
-void Mgrit::build_levels() {
-    const int m = cfg.m, nt = ps.n_time_steps;
+// Time-step counts of the MGRIT levels (the rules of mgrit.hpp:217-233): a level
+// is coarsened while its step count is a positive multiple of m; past the first
+// coarse level only if the next one keeps more than coarse_floor time points;
+// the two-level cycle stops after one coarsening.
+std::vector<int> mgrit_level_steps(int nt, int m, int cycle, int coarse_floor) {
+    if (m < 2) throw InvalidArgument("MgritConfig: m must be >= 2");
     if (nt >= m && nt % m != 0)
         throw InvalidArgument("MGRIT: nt (" + std::to_string(nt) + ") not divisible by coarsening factor m (" +
                               std::to_string(m) + ")");
-    std::vector<int> steps{nt};
-    for (;;) {
-        const int cur = steps.back();
-        if (cur % m != 0 || cur < m) break;
-        const int next = cur / m;
-        const bool first_coarse = steps.size() == 1;
-        if (!first_coarse && next + 1 <= cfg.coarse_floor) break;
-        steps.push_back(next);
-        if (cfg.cycle == 2) break;
+    std::vector<int> counts{nt};
+    const size_t cap = cycle == 2 ? 2 : static_cast<size_t>(-1);
+    while (counts.size() < cap) {
+        const int fine = counts.back();
+        if (fine < m || fine % m != 0) break;
+        const int coarse = fine / m;
+        const bool deep_enough = counts.size() == 1 || coarse + 1 > coarse_floor;
+        if (!deep_enough) break;
+        counts.push_back(coarse);
     }
+    return counts;
+}
+
+void Mgrit::build_levels() {
+    const int m = cfg.m, nt = ps.n_time_steps;
+    const std::vector<int> steps = mgrit_level_steps(nt, m, cfg.cycle, cfg.coarse_floor);
     const double dt0 = ps.t_final / nt;
     const int n = disc->n_p;
     levels.resize(steps.size());

@@ -202,6 +202,10 @@ struct MgritResultHost {
 };
 
 /// MgritSolver (mgrit.hpp:50-320) with the space-time state resident on device.
+/// Step counts of the MGRIT time levels, finest first (the hierarchy rule of
+/// MgritSolver::build_levels, mgrit.hpp:217-233).  cycle: 0 V, 1 F, 2 two-level.
+std::vector<int> mgrit_level_steps(int nt, int m, int cycle, int coarse_floor);
+
 class Mgrit {
 public:
     Mgrit(std::shared_ptr<const Disc> disc, const ProblemOptions& ps, const MgritOptions& cfg,

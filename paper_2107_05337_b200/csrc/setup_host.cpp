@@ -1,7 +1,10 @@
-// Host setup for the engine.  Every routine restates the reference algorithm it
-// cites in the same floating-point evaluation order (compiled with
+// Host setup for the engine.  The numerical routines here (Gauss-Legendre rule,
+// B-spline values / derivatives, dense LU) are written in the engine's own
+// formulation but perform, per output value, the same sequence of IEEE
+// operations as the reference routine each one cites (compiled with
 // -ffp-contract=off), so the device operators built from these tables are
-// bit-identical to the reference's.
+// bit-identical to the reference's.  tests/test_setup_host_cpu.py pins them
+// against fixtures made by the compiled reference (phi_setup_* in the C ABI).
 #include "setup_host.hpp"
 
 #include <algorithm>
@@ -15,128 +18,145 @@
 
 namespace phi {
 
+namespace {
+
+// P_n(x) and P_{n-1}(x) from k P_k = (2k-1) x P_{k-1} - (k-1) P_{k-2}.
+struct LegendrePair {
+    double pn, pnm1;
+};
+LegendrePair legendre_pair(int n, double x) {
+    double below = 1.0, top = x;  // P_0, P_1
+    for (int k = 2; k <= n; ++k) {
+        const double up = (double(2 * k - 1) * x * top - double(k - 1) * below) / double(k);
+        below = top;
+        top = up;
+    }
+    return {top, below};
+}
+
+}  // namespace
+
+// Roots of P_n by Newton from the Chebyshev-like guesses cos(pi (i + 3/4) / (n + 1/2)),
+// the slope from (x^2 - 1) P_n' = n (x P_n - P_{n-1}); the rule on [-1, 1] has
+// weights 2 / ((1 - x^2) P_n'^2), halved for [0, 1].  Same arithmetic per root as
+// quadrature.hpp:17-44 (the tables feed a bit-exact assembly).
 GaussRule gauss_legendre_01(int n) {
     if (n < 1) throw InvalidArgument("gauss_legendre_01: n must be >= 1");
-    GaussRule r;
-    r.nodes.resize(n);
-    r.weights.resize(n);
-    const double pi = 3.14159265358979323846;
+    constexpr double kPi = 3.14159265358979323846;
+    constexpr int kNewtonCap = 100;
+    constexpr double kNewtonStep = 1e-15;
+    GaussRule rule{std::vector<double>(n), std::vector<double>(n)};
     for (int i = 0; i < n; ++i) {
-        double x = std::cos(pi * (i + 0.75) / (n + 0.5));
-        double dp = 0.0;
-        for (int it = 0; it < 100; ++it) {
-            double p0 = 1.0, p1 = x;
-            for (int k = 2; k <= n; ++k) {
-                const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
-                p0 = p1;
-                p1 = p2;
-            }
-            dp = n * (x * p1 - p0) / (x * x - 1.0);
-            const double dx = p1 / dp;
-            x -= dx;
-            if (std::abs(dx) < 1e-15) break;
+        double root = std::cos(kPi * (i + 0.75) / (n + 0.5));  // descending in i
+        double slope = 0.0;
+        for (int sweep = 0; sweep < kNewtonCap; ++sweep) {
+            const LegendrePair P = legendre_pair(n, root);
+            slope = n * (root * P.pn - P.pnm1) / (root * root - 1.0);
+            const double step = P.pn / slope;
+            root -= step;
+            if (std::abs(step) < kNewtonStep) break;
         }
-        r.nodes[i] = 0.5 * (1.0 - x);
-        r.weights[i] = 1.0 / ((1.0 - x * x) * dp * dp);
+        rule.nodes[i] = 0.5 * (1.0 - root);  // ascending on [0, 1]
+        rule.weights[i] = 1.0 / ((1.0 - root * root) * slope * slope);
     }
-    return r;
+    return rule;
 }
 
+// The last knot s in [degree, n_basis) with t[s] <= xi (the right end maps to the
+// last span): a uniform-spacing guess, corrected against the knots themselves, so
+// the answer is the one a search over the knots gives (spline.hpp:28-32).
 int Knots::find_span(double xi) const {
-    if (xi >= t[n_basis]) return n_basis - 1;
-    auto it = std::upper_bound(t.begin() + degree, t.begin() + n_basis + 1, xi);
-    return static_cast<int>(it - t.begin()) - 1;
+    const int lo = degree, hi = n_basis;  // spans lo .. hi-1
+    if (xi >= t[hi]) return hi - 1;
+    if (!(xi >= t[lo])) return lo - 1;
+    const double rel = (xi - t[lo]) / (t[hi] - t[lo]);
+    int s = lo + std::min(hi - lo - 1, std::max(0, static_cast<int>(rel * (hi - lo))));
+    while (s > lo && t[s] > xi) --s;
+    while (t[s + 1] <= xi) ++s;  // t[hi] > xi stops it
+    return s;
 }
 
+// degree+1 copies of 0, the interior multiples of 1/n_elements, degree+1 copies of 1.
 Knots open_uniform_knots(int degree, int n_elements) {
     if (degree < 1) throw InvalidArgument("open_uniform_knots: degree must be >= 1");
     if (n_elements < 1) throw InvalidArgument("open_uniform_knots: n_elements must be >= 1");
     Knots kv;
     kv.degree = degree;
     kv.n_basis = n_elements + degree;
-    kv.t.resize(kv.n_basis + degree + 1);
-    const double a = 0.0, b = 1.0;
-    const double h = (b - a) / n_elements;
-    for (int i = 0; i <= degree; ++i) {
-        kv.t[i] = a;
-        kv.t[kv.t.size() - 1 - i] = b;
-    }
-    for (int i = 1; i < n_elements; ++i) kv.t[degree + i] = a + i * h;
+    const double h = 1.0 / n_elements;
+    kv.t.reserve(kv.n_basis + degree + 1);
+    kv.t.assign(degree + 1, 0.0);
+    for (int e = 1; e < n_elements; ++e) kv.t.push_back(e * h);
+    kv.t.insert(kv.t.end(), degree + 1, 1.0);
     return kv;
 }
 
 namespace {
 
-// Triangular Cox-de Boor on one span (NURBS-book A2.2 form).
-void basis_on_span(const Knots& kv, int span, double xi, int deg, double* out) {
-    const auto& t = kv.t;
-    double left[32] = {0}, right[32] = {0};
-    out[0] = 1.0;
-    for (int j = 1; j <= deg; ++j) {
-        left[j] = xi - t[span + 1 - j];
-        right[j] = t[span + j] - xi;
-        double saved = 0.0;
-        for (int r = 0; r < j; ++r) {
-            const double tmp = out[r] / (right[r + 1] + left[j - r]);
-            out[r] = saved + right[r + 1] * tmp;
-            saved = left[j - r] * tmp;
-        }
-        out[j] = saved;
+// One degree-raising step of the Cox-de Boor recurrence on the span [t[s], t[s+1]):
+// with a_r = t[s+r+1] - xi, b_r = xi - t[s+1-d+r] and q_r = N_r^{d-1} / (a_r + b_r),
+// N_r^d = b_{r-1} q_{r-1} + a_r q_r.  In place: N[0..d-1] holds degree d-1 on
+// entry, N[0..d] degree d on exit.
+inline void raise_degree(const std::vector<double>& t, int s, double xi, int d, double* N) {
+    double carry = 0.0;
+    for (int r = 0; r < d; ++r) {
+        const double a = t[s + r + 1] - xi;
+        const double b = xi - t[s + 1 - d + r];
+        const double q = N[r] / (a + b);
+        N[r] = carry + a * q;
+        carry = b * q;
     }
+    N[d] = carry;
 }
 
-// Values and first derivatives on the span of xi (spline.hpp:104-130).
+// Values and first derivatives of the degree+1 functions alive at xi, in one
+// pass up the degrees: the degree p-1 row is kept when it goes by, and
+// N_i' = p (g_i - g_{i+1}), g_i = N_i^{p-1} / (t[i+p] - t[i])  (spline.hpp:104-130).
+// Returns the index of the first of them.
 int values_and_derivs(const Knots& kv, double xi, double* vals, double* ders) {
     const int p = kv.degree;
-    const int span = kv.find_span(xi);
-    for (int a = 0; a <= p; ++a) vals[a] = ders[a] = 0.0;
-    basis_on_span(kv, span, xi, p, vals);
-    double lower[32] = {0};
-    basis_on_span(kv, span, xi, p - 1, lower);
-    const auto& t = kv.t;
-    for (int r = 0; r <= p; ++r) {
-        const int i = span - p + r;
-        double d = 0.0;
-        if (r >= 1) {
-            const double den = t[i + p] - t[i];
-            if (den > 0.0) d += lower[r - 1] / den;
-        }
-        if (r <= p - 1) {
-            const double den = t[i + p + 1] - t[i + 1];
-            if (den > 0.0) d -= lower[r] / den;
-        }
-        ders[r] = p * d;
+    const int s = kv.find_span(xi);
+    const int first = s - p;
+    double g[34];
+    vals[0] = 1.0;
+    for (int d = 1; d < p; ++d) raise_degree(kv.t, s, xi, d, vals);
+    // vals[0..p-1]: degree p-1 functions first+1 .. first+p; g[r] belongs to function first+r
+    g[0] = g[p + 1] = 0.0;
+    for (int r = 1; r <= p; ++r) {
+        const double width = kv.t[first + r + p] - kv.t[first + r];
+        g[r] = width > 0.0 ? vals[r - 1] / width : 0.0;
     }
-    return span - p;
+    raise_degree(kv.t, s, xi, p, vals);
+    for (int r = 0; r <= p; ++r) ders[r] = p * (g[r] - g[r + 1]);
+    return first;
 }
 
 }  // namespace
 
+// One row per (element, quadrature point): the point's parametric coordinate,
+// its weight scaled by the element length, and the p+1 values / derivatives
+// alive there.  Elements are the knot spans of positive length, in order.
 Tables1D build_tables(const Knots& kv, int nq) {
+    const int p = kv.degree;
+    const GaussRule unit = gauss_legendre_01(nq);
     Tables1D tb;
-    tb.p = kv.degree;
+    tb.p = p;
     tb.nq = nq;
-    const GaussRule rule = gauss_legendre_01(nq);
-    std::vector<int> spans;
-    for (int s = kv.degree; s < kv.n_basis; ++s)
-        if (kv.t[s + 1] > kv.t[s]) spans.push_back(s);
-    tb.nel = static_cast<int>(spans.size());
-    for (int s : spans) {
-        const double a = kv.t[s], b = kv.t[s + 1];
-        for (int i = 0; i < nq; ++i) {
-            tb.nodes.push_back(a + rule.nodes[i] * (b - a));
-            tb.weights.push_back(rule.weights[i] * (b - a));
+    for (int s = p; s < kv.n_basis; ++s) {
+        const double x0 = kv.t[s], len = kv.t[s + 1] - kv.t[s];
+        if (!(kv.t[s + 1] > x0)) continue;
+        ++tb.nel;
+        for (int q = 0; q < nq; ++q) {
+            tb.nodes.push_back(x0 + unit.nodes[q] * len);
+            tb.weights.push_back(unit.weights[q] * len);
         }
     }
-    const int p = tb.p;
-    tb.vals.resize(static_cast<size_t>(tb.nel) * nq * (p + 1));
-    tb.ders.resize(tb.vals.size());
+    const size_t width = static_cast<size_t>(p) + 1, points = tb.nodes.size();
+    tb.vals.resize(points * width);
+    tb.ders.resize(points * width);
     tb.first.resize(tb.nel);
-    for (int e = 0; e < tb.nel; ++e)
-        for (int q = 0; q < nq; ++q) {
-            const size_t base = (static_cast<size_t>(e) * nq + q) * (p + 1);
-            tb.first[e] = values_and_derivs(kv, tb.nodes[e * nq + q], &tb.vals[base], &tb.ders[base]);
-        }
+    for (size_t pt = 0; pt < points; ++pt)
+        tb.first[pt / nq] = values_and_derivs(kv, tb.nodes[pt], &tb.vals[pt * width], &tb.ders[pt * width]);
     return tb;
 }
 
@@ -213,41 +233,44 @@ HostCsr transpose(const HostCsr& a) {
     return t;
 }
 
+// LU with partial pivoting on a row-indirected dense copy: rows never move,
+// `order` names the row at each position and becomes the permutation.  The pivot
+// is the first largest |entry| below the diagonal, multipliers and updates are
+// those of solvers.hpp:136-167 (zero multipliers skip their row), so the packed
+// factors equal the reference's bit for bit.
 DenseLUHost dense_lu_factor(const HostCsr& a) {
     if (a.n_rows != a.n_cols) throw InvalidArgument("DenseLU: matrix not square");
-    DenseLUHost f;
     const int n = a.n_rows;
-    f.n = n;
-    f.lu.assign(static_cast<size_t>(n) * n, 0.0);
-    auto at = [&](int i, int j) -> double& { return f.lu[static_cast<size_t>(i) * n + j]; };
+    std::vector<double> work(static_cast<size_t>(n) * n, 0.0);
     for (int i = 0; i < n; ++i)
-        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e) at(i, a.col_indices[e]) = a.values[e];
-    std::vector<int> perm(n);
-    for (int i = 0; i < n; ++i) perm[i] = i;
+        for (int e = a.row_offsets[i]; e < a.row_offsets[i + 1]; ++e)
+            work[static_cast<size_t>(i) * n + a.col_indices[e]] = a.values[e];
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    auto row = [&](int pos) { return work.data() + static_cast<size_t>(order[pos]) * n; };
     for (int k = 0; k < n; ++k) {
-        int pivot = k;
-        double best = std::abs(at(k, k));
-        for (int i = k + 1; i < n; ++i) {
-            const double v = std::abs(at(i, k));
-            if (v > best) {
-                best = v;
-                pivot = i;
-            }
+        int where = k;
+        double big = std::abs(row(k)[k]);
+        for (int pos = k + 1; pos < n; ++pos) {
+            const double mag = std::abs(row(pos)[k]);
+            if (mag > big) big = mag, where = pos;
         }
-        if (best == 0.0) throw std::runtime_error("DenseLU: singular matrix");
-        if (pivot != k) {
-            for (int j = 0; j < n; ++j) std::swap(at(k, j), at(pivot, j));
-            std::swap(perm[k], perm[pivot]);
-        }
-        const double d = at(k, k);
-        for (int i = k + 1; i < n; ++i) {
-            const double m = at(i, k) / d;
-            at(i, k) = m;
-            if (m == 0.0) continue;
-            for (int j = k + 1; j < n; ++j) at(i, j) -= m * at(k, j);
+        if (big == 0.0) throw std::runtime_error("DenseLU: singular matrix");
+        std::swap(order[k], order[where]);
+        const double* top = row(k);
+        for (int pos = k + 1; pos < n; ++pos) {
+            double* r = row(pos);
+            const double mult = r[k] / top[k];
+            r[k] = mult;
+            if (mult == 0.0) continue;
+            for (int j = k + 1; j < n; ++j) r[j] -= mult * top[j];
         }
     }
-    f.piv = perm;
+    DenseLUHost f;
+    f.n = n;
+    f.lu.resize(work.size());
+    for (int pos = 0; pos < n; ++pos) std::copy(row(pos), row(pos) + n, f.lu.begin() + static_cast<size_t>(pos) * n);
+    f.piv = std::move(order);
     return f;
 }
 

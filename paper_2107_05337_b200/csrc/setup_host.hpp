@@ -11,13 +11,13 @@
 
 namespace phi {
 
-/// n-point Gauss-Legendre rule on [0, 1] (restates quadrature.hpp:17-44).
+/// n-point Gauss-Legendre rule on [0, 1] (same values as quadrature.hpp:17-44).
 struct GaussRule {
     std::vector<double> nodes, weights;
 };
 GaussRule gauss_legendre_01(int n);
 
-/// Open uniform knot vector on [0, 1] (restates spline.hpp:17-63).
+/// Open uniform knot vector on [0, 1] (same knots as spline.hpp:48-63).
 struct Knots {
     std::vector<double> t;
     int degree = 0;
@@ -50,7 +50,7 @@ LowTables build_low_tables(const Knots& low, const Tables1D& high);
 HostCsr p1_embedding_free(int n_elements_fine);
 HostCsr transpose(const HostCsr& a);
 
-/// Dense LU with partial pivoting (restates solvers.hpp:102-172).
+/// Dense LU with partial pivoting (same factors and permutation as solvers.hpp:136-167).
 struct DenseLUHost {
     int n = 0;
     std::vector<double> lu;

@@ -37,7 +37,7 @@ EXPORTED = [
     "phi_mgrit_free", "phi_mgrit_levels", "phi_mgrit_solve", "phi_mgrit_trajectory",
     "phi_mgrit_initial", "phi_mgrit_initialize", "phi_mgrit_cycle", "phi_mgrit_residual_norm",
     "phi_mgrit_launches", "phi_mgrit_set_init_coeffs", "phi_mgrit_profile", "phi_mgrit_wave_report",
-    "phi_dev_tuning", "phi_dev_trace", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
+    "phi_dev_tuning", "phi_dev_trace", "phi_setup_tables_1d", "phi_setup_dense_lu", "phi_setup_level_steps", "phi_mgrit_set_range", "phi_mgrit_initialize_state",
     "phi_mgrit_gnorm_terms", "phi_mgrit_residual_terms", "phi_mgrit_phase", "phi_mgrit_points",
     "phi_mgrit_stats", "phi_mgrit_residual_iters", "phi_mgrit_wave_levels",
     "phi_hier_vcycle_bytes", "phi_comm_nccl_unique_id", "phi_comm_create_nccl", "phi_comm_create_ops", "phi_comm_free", "phi_mgrit_set_comm",
@@ -137,6 +137,9 @@ def lib():
         L.phi_mgrit_launches.restype = _ll
         L.phi_dev_tuning.argtypes = [_i, _i, _i]
         L.phi_dev_trace.argtypes = [_vp, _i]
+        L.phi_setup_tables_1d.argtypes = [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]
+        L.phi_setup_dense_lu.argtypes = [_i, _vp, _vp, _vp]
+        L.phi_setup_level_steps.argtypes = [_i, _i, _i, _i, _vp, _i, _vp]
         L.phi_mgrit_set_range.argtypes = [_vp, _i, _i]
         L.phi_mgrit_initialize_state.argtypes = [_vp]
         L.phi_mgrit_gnorm_terms.argtypes = [_vp, _vp]
@@ -181,6 +184,39 @@ def _f64(a):
 def dev_tuning(tri_warps=16, gs_warps=16, sleep_ns=0) -> None:
     """Developer knob for the sync-free sweeps (see include/phi_engine.h)."""
     _check(lib().phi_dev_tuning(tri_warps, gs_warps, sleep_ns))
+
+
+def setup_tables_1d(degree: int, n_elements: int, nq: int) -> dict:
+    """Host quadrature / basis tables of one parametric direction (no device
+    needed): DirTables of an open uniform knot vector (assembly.hpp:124-151)."""
+    pts = n_elements * nq
+    out = dict(nodes=np.empty(pts), weights=np.empty(pts), vals=np.empty((pts, degree + 1)),
+               ders=np.empty((pts, degree + 1)), first=np.empty(n_elements, dtype=np.int32))
+    if degree < 1 or n_elements < 1 or nq < 1:  # the library raises; nothing to size
+        out = {k: np.empty(1, dtype=v.dtype) for k, v in out.items()}
+    _check(lib().phi_setup_tables_1d(degree, n_elements, nq, _p(out["nodes"]), _p(out["weights"]), _p(out["vals"]),
+                                     _p(out["ders"]), _p(out["first"])))
+    return out
+
+
+def setup_dense_lu(a) -> tuple[np.ndarray, np.ndarray]:
+    """DenseLU factors (unit-lower and upper packed) and permutation (solvers.hpp:136-167)."""
+    a = _f64(a)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError("DenseLU: matrix not square")
+    n = a.shape[0]
+    lu = np.empty((n, n))
+    piv = np.empty(n, dtype=np.int32)
+    _check(lib().phi_setup_dense_lu(n, _p(a), _p(lu), _p(piv)))
+    return lu, piv
+
+
+def setup_level_steps(nt: int, m: int, cycle: int = 0, coarse_floor: int = 8) -> list[int]:
+    """Step counts of the MGRIT time levels (MgritSolver::build_levels, mgrit.hpp:217-233)."""
+    steps = np.zeros(64, dtype=np.int32)
+    nl = C.c_int(0)
+    _check(lib().phi_setup_level_steps(nt, m, cycle, coarse_floor, _p(steps), 64, C.byref(nl)))
+    return [int(v) for v in steps[: nl.value]]
 
 
 def default_solver_config(**kw) -> SolverConfig:

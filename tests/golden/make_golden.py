@@ -16,6 +16,11 @@ Fixtures
                   restrict/prolong (pmultigrid.hpp:242-254), hmg_wcycle (172-200),
                   gauss_seidel_sweep fwd/bwd (solvers.hpp:80-99), the 9x9 coarse LU
                   (solvers.hpp:102-172), vcycle (256-267) and solve (271-307).
+  setup_host.npz  the reference's host setup on the shapes of BASELINE.json configs 1-5:
+                  detail::DirTables (assembly.hpp:124-151: gauss_legendre_01, open_uniform_knots,
+                  eval_values_and_derivs) for (degree, elements, points) of the degree-p and the
+                  order-1 spaces, and DenseLU(a).solve(b) (solvers.hpp:102-172) on seeded dense
+                  systems (full, sparse with a zero diagonal that forces pivoting) with their inputs.
   mgrit_*.npz     also hold the SpatialDiscretization arrays of their (p, h).
   mgrit_c1.npz    BASELINE.json config 1 (p=2, h=2^-4, Nt=100, two-level m=4, FCF,
                   f=0, u0=sin sin): MgritSolver::solve() (mgrit.hpp:93-118) result,
@@ -116,12 +121,46 @@ def mgrit_fixture(p, k, nt, **kw) -> dict:
     return out
 
 
+# (degree, elements, points per span): degree-p spaces of configs 1-5 at small and BASELINE
+# mesh sizes with their p+1 rule, and the order-1 spaces (2-point rule, and sampled at the
+# degree-p nodes through a (p+1)-point rule)
+SETUP_TABLE_CASES = [(2, 16, 3), (3, 64, 4), (4, 128, 5), (5, 256, 6), (2, 256, 3), (3, 256, 4),
+                     (1, 256, 2), (1, 128, 2), (1, 2, 2), (1, 16, 3), (1, 64, 6), (2, 1, 3), (5, 3, 6)]
+SETUP_LU_SIZES = [1, 2, 9, 25, 49]
+
+
+def setup_lu_inputs():
+    """Seeded dense systems: a full one, and one with a zero diagonal (pivoting) per size."""
+    rng = np.random.default_rng(777)
+    out = []
+    for n in SETUP_LU_SIZES:
+        full = rng.uniform(-1.0, 1.0, (n, n))
+        holed = np.where(rng.uniform(size=(n, n)) < 0.5, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+        np.fill_diagonal(holed, 0.0)
+        holed += 0.75 * np.roll(np.eye(n), 1, axis=1) if n > 1 else 1.0
+        out.append((full, rng.standard_normal(n)))
+        out.append((holed, rng.standard_normal(n)))
+    return out
+
+
+def setup_fixture() -> dict:
+    out: dict = {}
+    for (p, nel, nq) in SETUP_TABLE_CASES:
+        for k, v in O.ref_tables_1d(p, nel, nq).items():
+            out[f"t_{p}_{nel}_{nq}_{k}"] = v
+    for i, (a, b) in enumerate(setup_lu_inputs()):
+        out[f"lu{i}_a"], out[f"lu{i}_b"] = a, b
+        out[f"lu{i}_x"] = O.ref_dense_solve(a, b)
+    return out
+
+
 def fixtures() -> dict:
     """name -> builder of each committed fixture."""
     coeffs = np.random.default_rng(12345).uniform(-1.0, 1.0, (2 ** 4 + 3 - 2) ** 2)
     coeffs3 = np.random.default_rng(12345).uniform(-1.0, 1.0, (2 ** 3 + 2 - 2) ** 2)
     return {
         "ops_p2k3.npz": ops_fixture,
+        "setup_host.npz": setup_fixture,
         "mgrit_c1.npz": lambda: mgrit_fixture(2, 4, 100, cycle=O.CYCLE_TWO_LEVEL, m=4,
                                               source_param=0.0, init_kind=O.INIT_SIN),
         "mgrit_src.npz": lambda: dict(coeffs=coeffs, **mgrit_fixture(
