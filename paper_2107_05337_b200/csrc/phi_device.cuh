@@ -1996,73 +1996,77 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ---- IC projection: Jacobi-preconditioned CG on M (solvers.hpp:21-75) ------
-// Single CTA; exact: index-ordered dot products and operator rows (the
-// reference's rounding), else reassociated sums.  work: 4 vectors of n.
+// One CTA, or one cluster of CTAs: the operator rows and the vector updates are
+// split by row over the cluster, every CTA forms the dot products over the
+// whole vectors in the same order (as cg_point), so all CTAs take the same
+// decisions and the result does not depend on the cluster size -- bitwise, in
+// both summation modes.  exact: index-ordered dot products and operator rows
+// (the reference's rounding), else reassociated sums.  work: 4 vectors of n.
 template <int DEG>
 __global__ void __launch_bounds__(NT, 1)
     cg_kernel(const __grid_constant__ DevStencil A, const double* __restrict__ diag, const double* __restrict__ b,
               double* x, double* work, double rel_tol, int max_iter, int* result, int exact) {
     __shared__ double sh[4];
     __shared__ double scratch[kDotChunk];
+    cl_init();
+    __syncthreads();
+    const int part = cl_rank(), parts = cl_size();
+    const bool ex = exact != 0;
     const int n = A.ru * A.rv;
     double* r = work;
     double* z = work + n;
     double* p = work + 2 * (size_t)n;
     double* q = work + 3 * (size_t)n;
-    const double bnorm = sqrt(cta_ordered_dot(b, b, n, scratch, sh, exact != 0));
-    if (bnorm == 0.0) {
-        cta_fill(x, 0.0, n);
-        if (threadIdx.x == 0) {
-            result[0] = 1;
-            result[1] = 0;
+    auto finish = [&](int conv, int it) {
+        if (threadIdx.x == 0 && part == 0) {
+            result[0] = conv;
+            result[1] = it;
         }
-        return;
+    };
+    const double bnorm = sqrt(cta_ordered_dot(b, b, n, scratch, sh, ex));
+    cta_fill(x, 0.0, n, part, parts);
+    if (bnorm == 0.0) return finish(1, 0);
+    cl_sync();
+    stencil_apply<kOutResid, Widths<DEG>::A>(A, x, r, b, ex, part, parts);
+    cl_sync();
+    double rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh, ex));
+    if (rnorm <= rel_tol * bnorm) return finish(1, 0);
+    for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
+        const double zi = r[i] / diag[i];
+        z[i] = zi;
+        p[i] = zi;
     }
-    cta_fill(x, 0.0, n);
-    __syncthreads();
-    stencil_apply<kOutResid, Widths<DEG>::A>(A, x, r, b, exact != 0);
-    double rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh, exact != 0));
-    if (rnorm <= rel_tol * bnorm) {
-        if (threadIdx.x == 0) {
-            result[0] = 1;
-            result[1] = 0;
-        }
-        return;
-    }
-    for (int i = threadIdx.x; i < n; i += NT) {
-        z[i] = r[i] / diag[i];
-        p[i] = z[i];
-    }
-    double rz = cta_ordered_dot(r, z, n, scratch, sh, exact != 0);
+    cl_sync();
+    double rz = cta_ordered_dot(r, z, n, scratch, sh, ex);
     int conv = 0, it = 1;
     for (; it <= max_iter; ++it) {
-        stencil_apply<kOutSet, Widths<DEG>::A>(A, p, q, nullptr, exact != 0);
-        const double pq = cta_ordered_dot(p, q, n, scratch, sh, exact != 0);
+        stencil_apply<kOutSet, Widths<DEG>::A>(A, p, q, nullptr, ex, part, parts);
+        cl_sync();
+        const double pq = cta_ordered_dot(p, q, n, scratch, sh, ex);
         if (pq <= 0.0) {
             conv = -1;
             break;
         }
         const double alpha = rz / pq;
-        for (int i = threadIdx.x; i < n; i += NT) {
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) {
             x[i] += alpha * p[i];
             r[i] += -alpha * q[i];
         }
-        rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh, exact != 0));
+        cl_sync();
+        rnorm = sqrt(cta_ordered_dot(r, r, n, scratch, sh, ex));
         if (rnorm <= rel_tol * bnorm) {
             conv = 1;
             break;
         }
-        for (int i = threadIdx.x; i < n; i += NT) z[i] = r[i] / diag[i];
-        const double rz_new = cta_ordered_dot(r, z, n, scratch, sh, exact != 0);
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) z[i] = r[i] / diag[i];
+        cl_sync();
+        const double rz_new = cta_ordered_dot(r, z, n, scratch, sh, ex);
         const double beta = rz_new / rz;
         rz = rz_new;
-        for (int i = threadIdx.x; i < n; i += NT) p[i] = z[i] + beta * p[i];
-        __syncthreads();
+        for (int i = threadIdx.x + part * NT; i < n; i += NT * parts) p[i] = z[i] + beta * p[i];
+        cl_sync();
     }
-    if (threadIdx.x == 0) {
-        result[0] = conv;
-        result[1] = it;
-    }
+    finish(conv, it);
 }
 
 }  // namespace
@@ -2267,7 +2271,56 @@ void DegLaunch<DEG>::unit(const DevHier& H, int op, int arg, int arg2, const dou
 template <int DEG>
 void DegLaunch<DEG>::cg(const DevStencil& A, const double* diag, const double* b, double* x, double* work,
                         double rel_tol, int max_iter, int* result, int exact, cudaStream_t s) {
-    cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result, exact);
+    // a cluster for systems large enough that the row split outweighs its
+    // barriers (the threshold of the wave kernel); same result for any size
+    static int cl = -1;
+    if (cl < 0) {
+        cl = 1;
+        if (const char* e = std::getenv("PHI_CLUSTER")) {
+            cl = std::max(1, std::atoi(e));
+        } else {
+            for (int c = kPhiClusterWide; c > 1 && cl == 1; c /= 2) {
+                if (c > 8 && cudaFuncSetAttribute(cg_kernel<DEG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                                 cudaSuccess) {
+                    (void)cudaGetLastError();
+                    continue;
+                }
+                cudaLaunchConfig_t q{};
+                q.gridDim = dim3((unsigned)c);
+                q.blockDim = dim3(NT);
+                cudaLaunchAttribute qa[1];
+                qa[0].id = cudaLaunchAttributeClusterDimension;
+                qa[0].val.clusterDim.x = (unsigned)c;
+                qa[0].val.clusterDim.y = 1;
+                qa[0].val.clusterDim.z = 1;
+                q.attrs = qa;
+                q.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, cg_kernel<DEG>, &q) == cudaSuccess && ncl >= 1)
+                    cl = c;
+                else
+                    (void)cudaGetLastError();
+            }
+        }
+    }
+    const int use = A.ru * A.rv >= 4096 ? cl : 1;
+    if (use > 1) {
+        if (use > 8) PHI_CUDA(cudaFuncSetAttribute(cg_kernel<DEG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)use);
+        cfg.blockDim = dim3(NT);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)use;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PHI_CUDA(cudaLaunchKernelEx(&cfg, cg_kernel<DEG>, A, diag, b, x, work, rel_tol, max_iter, result, exact));
+    } else {
+        cg_kernel<DEG><<<1, NT, 0, s>>>(A, diag, b, x, work, rel_tol, max_iter, result, exact);
+    }
     PHI_CUDA(cudaGetLastError());
 }
 

@@ -264,3 +264,29 @@ def test_fcycle_four_levels_golden(exact):
     else:
         assert abs(r.iterations - int(g["iterations"][0])) <= 1
         assert _rel(eng.trajectory(), g["trajectory"]) <= TOL_TRAJ
+
+
+@pytest.mark.parametrize("p,k", [(3, 6), (4, 7)])
+def test_initial_projection_on_a_cluster_matches_reference(p, k):
+    """project_initial (theta.hpp:150-210: Jacobi CG on M, solvers.hpp:21-75) at the sizes
+    of configs 2 and 3, where the device CG runs on a cluster of CTAs (n >= 4096): the
+    projected u0 is bitwise the reference's in exact mode (rows split over the cluster,
+    whole-vector dot products in every CTA) and within the trajectory bar in the default
+    mode; both repeatable bit for bit."""
+    _need_ref()
+    kw = dict(cycle=E.CYCLE_TWO_LEVEL, m=4, init_kind=E.INIT_COEFFS, init_coeffs=_coeffs(p, k), source_param=0.0)
+    ref = O.RefMgrit(p, k, 8, workers=WORKERS, **kw)
+    ref.initialize()
+    u_ref = ref.initial()
+    disc = E.SpatialDiscretization.build(p, k)
+    for exact in (True, False):
+        got = []
+        for _ in range(2):
+            eng = E.MgritSolver(disc, 8, exact=exact, **kw)
+            eng.initialize()
+            got.append(eng.initial())
+        assert np.array_equal(got[0], got[1])
+        if exact:
+            assert np.array_equal(got[0], u_ref)
+        else:
+            assert _rel(got[0], u_ref) <= 1e-12
