@@ -82,7 +82,12 @@ def test_fast_mgrit_within_tolerance(case):
     rg, rr = eng.solve(), ref.solve()
     assert abs(rg.iterations - rr["iterations"]) <= 1
     assert rg.converged
-    assert abs(rg.mean_spatial_iterations - rr["mean_spatial_iterations"]) <= 1.0
+    # p-MG counts: the same number of solves, per-solve cycle counts within +-1 (residual
+    # wave on the final states: one Phi per time point on both sides), means within 0.02
+    assert rg.total_spatial_solves == rr["total_spatial_solves"]
+    ie, ir = eng.residual_iters(0), ref.residual_iters(0, 1)
+    assert np.abs(ie.astype(int) - ir.astype(int)).max() <= 1
+    assert abs(rg.mean_spatial_iterations - rr["mean_spatial_iterations"]) <= 0.02
     assert abs(rg.g_norm - rr["g_norm"]) <= 1e-10 * rr["g_norm"]
     assert _rel(eng.trajectory(), ref.trajectory()) <= TOL_TRAJ
 
@@ -115,7 +120,9 @@ def test_fast_and_exact_modes_agree_on_config3_4_shapes(p, k, nt, m):
     rf, re_ = fast.solve(), exact.solve()
     assert rf.converged and re_.converged
     assert abs(rf.iterations - re_.iterations) <= 1
-    assert abs(rf.mean_spatial_iterations - re_.mean_spatial_iterations) <= 1.0
+    assert rf.total_spatial_solves == re_.total_spatial_solves
+    assert np.abs(fast.residual_iters(0).astype(int) - exact.residual_iters(0).astype(int)).max() <= 1
+    assert abs(rf.mean_spatial_iterations - re_.mean_spatial_iterations) <= 0.05
     assert _rel(fast.trajectory(), exact.trajectory()) <= TOL_TRAJ
 
 
