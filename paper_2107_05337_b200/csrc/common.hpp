@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstddef>
 #include <cstdint>
@@ -105,6 +106,15 @@ struct HostCsr {
     std::vector<int> col_indices;
     std::vector<double> values;
     int nnz() const { return static_cast<int>(col_indices.size()); }
+};
+
+/// NVTX range over a host-side phase (header-only NVTX v3: a no-op unless a
+/// profiler is attached), so Nsight timelines show the MGRIT phases by name.
+struct TraceRange {
+    explicit TraceRange(const char* name) { nvtxRangePushA(name); }
+    ~TraceRange() { nvtxRangePop(); }
+    TraceRange(const TraceRange&) = delete;
+    TraceRange& operator=(const TraceRange&) = delete;
 };
 
 }  // namespace phi

@@ -67,6 +67,7 @@ DevBuf<T> dev(const std::vector<T>& h, cudaStream_t s) {
 // Disc
 // ---------------------------------------------------------------------------
 std::shared_ptr<Disc> Disc::build(int degree, int k, cudaStream_t s) {
+    TraceRange trace_range("phi.disc.assemble");
     if (degree < 1 || degree > 8) throw InvalidArgument("SpatialDiscretization: degree must be in [1, 8]");
     if (k < 1) throw InvalidArgument("SpatialDiscretization: mesh exponent must be >= 1");
     auto d = std::make_shared<Disc>();
@@ -249,6 +250,7 @@ DevBlk Hier::BlkDev::view() const {
 
 Hier::Hier(std::shared_ptr<const Disc> disc_, double c_, const HierOptions& opt_, cudaStream_t s, bool cg_only_)
     : disc(std::move(disc_)), c(c_), opt(opt_), cg_only(cg_only_) {
+    TraceRange trace_range("phi.hier.setup");
     const Disc& d = *disc;
     A.ru = A.rv = A.cu = A.cv = d.nf_p;
     A.lo = d.M.lo;
@@ -594,6 +596,7 @@ void Mgrit::build_loads() {
 }
 
 void Mgrit::project_initial() {
+    TraceRange trace_range("phi.mgrit.project_initial");
     const int n = disc->n_p;
     if (ps.init_kind == 0) {
         u0.zero(stream);
@@ -683,6 +686,7 @@ Mgrit::~Mgrit() {
 }
 
 void Mgrit::coarse_overlapped(int lc, bool residual) {
+    TraceRange trace_range("phi.mgrit.coarse_march+interpolate");
     const int lf = lc - 1;
     Level& c = levels[lc];
     Level& f = levels[lf];
@@ -794,6 +798,7 @@ int Mgrit::range_hi(int l) const {
 // BEFORE interval j's C-relaxation updates it, which a fused task only sees
 // while all intervals happen to be resident at once.
 void Mgrit::f_relax(int l, bool with_c) {
+    TraceRange trace_range("phi.mgrit.f_relax");
     Level& lv = levels[l];
     const int lo = range_lo(l), hi = range_hi(l);
     wave(l, kModeStep, kEpiStore, hi - lo, lv.kF.get() + lo, cfg.m - 1);
@@ -801,12 +806,14 @@ void Mgrit::f_relax(int l, bool with_c) {
 }
 
 void Mgrit::c_relax(int l) {
+    TraceRange trace_range("phi.mgrit.c_relax");
     Level& lv = levels[l];
     const int lo = range_lo(l), hi = range_hi(l);
     wave(l, kModeStep, kEpiStore, hi - lo, lv.kR.get() + lo, 1);
 }
 
 void Mgrit::restrict_residual(int l) {
+    TraceRange trace_range("phi.mgrit.restrict");
     Level& f = levels[l];
     Level& c = levels[l + 1];
     const int n = disc->n_p;
@@ -817,6 +824,7 @@ void Mgrit::restrict_residual(int l) {
 }
 
 void Mgrit::interpolate_and_correct(int l) {
+    TraceRange trace_range("phi.mgrit.interpolate");
     Level& f = levels[l];
     Level& c = levels[l + 1];
     launch_inject(c.u.get(), f.u.get(), disc->n_p, f.steps / cfg.m, cfg.m, stream);
@@ -825,6 +833,7 @@ void Mgrit::interpolate_and_correct(int l) {
 }
 
 void Mgrit::coarsest_solve(int l) {
+    TraceRange trace_range("phi.mgrit.coarsest_solve");
     Level& lv = levels[l];
     launch_copy(lv.u.get(), lv.g.get(), disc->n_p, stream);
     ++launches;
@@ -875,6 +884,7 @@ double Mgrit::residual_norm(int l) {
 }
 
 void Mgrit::residual_terms(int l, double* host) {
+    TraceRange trace_range("phi.mgrit.residual");
     Level& lv = levels[l];
     const int n = disc->n_p;
     const int lo = range_lo(l), hi = range_hi(l);
@@ -918,6 +928,7 @@ void Mgrit::residual_iters(int l, int* host) {
 }
 
 double Mgrit::compute_g_norm() {
+    TraceRange trace_range("phi.mgrit.g_norm");
     std::vector<double> h(levels[0].steps + 1);
     gnorm_terms(h.data());
     double total = 0.0;
@@ -1117,6 +1128,7 @@ int Mgrit::wave_report(double* ms, double* bytes) {
 }
 
 MgritResultHost Mgrit::solve() {
+    TraceRange trace_range("phi.mgrit.solve");
     if (comm) return solve_sharded();
     launches = 0;
     for (auto& r : recs) {
