@@ -748,6 +748,14 @@ __device__ __forceinline__ void xst(double* xg, unsigned xs, int j, double v) {
 __device__ __forceinline__ void lds_v2f64(unsigned a, double& x, double& y) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
 }
+// predicated pair load: {x, y} = on ? [a] : {0, 0} (the load is not issued for the other lanes)
+__device__ __forceinline__ void lds_v2f64_if(unsigned a, bool on, double& x, double& y) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %3, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
+        "mov.f64 %1, 0d0000000000000000;\n\t@p ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
+        : "=&d"(x), "=&d"(y)
+        : "r"(a), "r"((int)on));
+}
 __device__ __forceinline__ void lds_slot(unsigned a, int& c, double& v) {  // {int32 col, pad, double val}
     int pad;
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(c), "=r"(pad), "=r"(reinterpret_cast<int*>(&v)[0]),
@@ -931,7 +939,13 @@ __device__ __noinline__ void blk_sweep_t(const DevBlk& T, int count, double* xg,
             if (RSM && row >= 0) rhs = vlds_f64(rs + 8u * row);
             double iv[32];
 #pragma unroll
-            for (int p2 = 0; p2 < 16; ++p2) lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
+            for (int p2 = 0; p2 < 16; ++p2) {
+                if constexpr (kBlkTri)  // lower triangle only: lanes above the diagonal keep exact zeros
+                    lds_v2f64_if(u + kBlkInvOff + 16u * (p2 * (31 - p2) + lane), lane >= 2 * p2, iv[2 * p2],
+                                 iv[2 * p2 + 1]);
+                else
+                    lds_v2f64(u + kBlkInvOff + 16u * (p2 * 32 + lane), iv[2 * p2], iv[2 * p2 + 1]);
+            }
             // ---- G_k, the old sums, y = B^{-1} (rhs - old), the wait for block
             // g-1 (the previous solver), then the chain x_g = y - G_k x_{g-1}
             // over the last 8 mf values of block g-1 (mf: groups of four column pairs)

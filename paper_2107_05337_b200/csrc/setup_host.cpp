@@ -707,9 +707,10 @@ BlkStream make_blk_stream(const BlkRowsView& rv, int win) {
         std::memcpy(img.data() + 16, b.rows, sizeof b.rows);
         double* iv = reinterpret_cast<double*>(img.data() + kBlkInvOff);
         for (int pj = 0; pj < kBlkRows / 2; ++pj)
-            for (int l = 0; l < kBlkRows; ++l) {
-                iv[(pj * kBlkRows + l) * 2] = static_cast<double>(inv[l][2 * pj]);
-                iv[(pj * kBlkRows + l) * 2 + 1] = static_cast<double>(inv[l][2 * pj + 1]);
+            for (int l = kBlkTri ? 2 * pj : 0; l < kBlkRows; ++l) {
+                const int slot = kBlkTri ? pj * (31 - pj) + l : pj * kBlkRows + l;
+                iv[slot * 2] = static_cast<double>(inv[l][2 * pj]);
+                iv[slot * 2 + 1] = static_cast<double>(inv[l][2 * pj + 1]);
             }
         // folded coupling to block k-1: G = B^{-1} N, N(l, j) = the fresh
         // entry of row l at local column j of block k-1; pair q holds the

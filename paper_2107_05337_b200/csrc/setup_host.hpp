@@ -156,7 +156,16 @@ TriStream make_tri_stream(const TriPlan& p, bool fast);
 /// holds (offset / 16, bytes, mf, 0) per block.
 constexpr int kBlkRows = 32;
 constexpr int kBlkInvOff = 144;
-constexpr int kBlkFreshOff = kBlkInvOff + 8 * kBlkRows * kBlkRows;
+/// PHI_BLK_TRI: the inverse (lower triangular in solve order) is stored as its
+/// lower triangle -- column pair p keeps rows 2p .. 31 only, the pair of lane L
+/// at slot p (31 - p) + L (16 bytes each; 272 slots = 4352 bytes instead of
+/// 8192); lanes above the diagonal load nothing and use exact zeros.
+#ifndef PHI_BLK_TRI
+#define PHI_BLK_TRI 0
+#endif
+constexpr int kBlkTri = PHI_BLK_TRI;
+constexpr int kBlkInvBytes = kBlkTri ? 16 * 272 : 8 * kBlkRows * kBlkRows;
+constexpr int kBlkFreshOff = kBlkInvOff + kBlkInvBytes;
 #ifndef PHI_BLK_SOLVERS
 #define PHI_BLK_SOLVERS 2
 #endif
