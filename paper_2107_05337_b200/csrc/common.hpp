@@ -12,6 +12,12 @@
 #include <utility>
 #include <vector>
 
+// Threads per Phi CTA (phi_kernels.cuh: kPhiThreads; setup_host.hpp: the
+// number of block-sweep worker warps follows from it).
+#ifndef PHI_THREADS
+#define PHI_THREADS 256
+#endif
+
 namespace phi {
 
 /// Error categories surfaced through the C-ABI status codes

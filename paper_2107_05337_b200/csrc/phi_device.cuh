@@ -48,6 +48,8 @@ namespace {
 constexpr int NT = kPhiThreads;
 constexpr int NW = NT / 32;
 constexpr int kDotChunk = 2048;  // doubles of shared scratch for ordered dots
+constexpr int kDotThreads = 256;  // threads that form a reassociated dot product's partial sums
+static_assert(NT >= kDotThreads && NT % 32 == 0, "a Phi CTA has at least the dot product's threads");
 
 // Dynamic shared memory of every Phi kernel (laid out by SmemPlan).
 extern __shared__ __align__(16) double g_smem[];
@@ -1204,19 +1206,25 @@ __device__ __noinline__ double cta_ordered_dot(const double* a, const double* b,
                                                bool exact = true) {
     double s = 0.0;
     if (!exact) {  // reassociated: strided partial sums, warp butterflies, warp totals in order
-        double a0 = 0.0, a1 = 0.0;
-        for (int i = threadIdx.x; i < n; i += 2 * NT) {
-            a0 = a0 + a[i] * b[i];
-            if (i + NT < n) a1 = a1 + a[i + NT] * b[i + NT];
+        // the partial sums are defined on kDotThreads threads whatever the CTA
+        // size, so the rounding does not depend on the number of sweep warps
+        constexpr int DT = kDotThreads;
+        double t = 0.0;
+        if (threadIdx.x < DT) {
+            double a0 = 0.0, a1 = 0.0;
+            for (int i = threadIdx.x; i < n; i += 2 * DT) {
+                a0 = a0 + a[i] * b[i];
+                if (i + DT < n) a1 = a1 + a[i + DT] * b[i + DT];
+            }
+            t = a0 + a1;
+            for (int o = 16; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
         }
-        double t = a0 + a1;
-        for (int o = 16; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
         __syncthreads();
-        if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = t;
+        if (threadIdx.x < DT && (threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = t;
         __syncthreads();
         if (threadIdx.x == 0) {
             double u = 0.0;
-            for (int k = 0; k < NW; ++k) u = u + scratch[k];
+            for (int k = 0; k < DT / 32; ++k) u = u + scratch[k];
             sh[0] = u;
         }
         __syncthreads();
@@ -1494,13 +1502,15 @@ __device__ __noinline__ void dense_apply_cl(const double* __restrict__ c, int n,
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // rw warps cover 32 rows each, the other warps split the columns: with 61
     // rows per CTA (n = 961 on 16 CTAs) two row warps and four column quarters
+    // (the first eight warps; a CTA with more sweep warps leaves the others out)
     const int rw = chunk > 64 ? 4 : (chunk > 32 ? 2 : 1), cs = 8 / rw;
-    const int wr = w % rw, wc = w / rw;
+    const bool act = w < 8;
+    const int wr = w % rw, wc = act ? w / rw : 0;
     const int j0 = (int)((long long)n * wc / cs), j1 = (int)((long long)n * (wc + 1) / cs);
     for (int base = r0; base < r1; base += 32 * rw) {
         const int i = base + wr * 32 + lane;  // this thread's row
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        if (i < r1) {
+        if (act && i < r1) {
             // sixteen operator loads in flight per thread: the product is bound by
             // the latency of the loads from L2 (each CTA streams n^2 / parts entries)
             int j = j0;
@@ -1518,9 +1528,9 @@ __device__ __noinline__ void dense_apply_cl(const double* __restrict__ c, int n,
             }
             for (; j < j1; ++j) a0 = __fma_rn(__ldg(c + (size_t)j * n + i), rl[j], a0);
         }
-        pp[w * 32 + lane] = (a0 + a1) + (a2 + a3);
+        if (act) pp[w * 32 + lane] = (a0 + a1) + (a2 + a3);
         __syncthreads();
-        if (wc == 0 && i < r1) {
+        if (act && wc == 0 && i < r1) {
             double s = pp[wr * 32 + lane];
             for (int q = 1; q < cs; ++q) s = s + pp[(q * rw + wr) * 32 + lane];  // column parts in order
             x_main[i] = x_main[i] + s;

@@ -11,10 +11,15 @@
 
 namespace phi {
 
-constexpr int kPhiThreads = 256;
+// Threads per Phi CTA: 2 block-sweep solver warps + 6 worker warps by default
+// (PHI_THREADS / PHI_BLK_SOLVERS: developer A/B builds with more solver warps).
+constexpr int kPhiThreads = PHI_THREADS;
 // Dynamic shared memory one Phi CTA may use for its latency-critical vectors
 // (one CTA per SM; 227 KB is the sm_100 per-block maximum).
-constexpr size_t kPhiSmemBudgetBytes = 212 * 1024;
+#ifndef PHI_SMEM_BUDGET_KB
+#define PHI_SMEM_BUDGET_KB 212
+#endif
+constexpr size_t kPhiSmemBudgetBytes = PHI_SMEM_BUDGET_KB * 1024;
 /// CTAs per cluster for waves of few right-hand sides (reassociated mode).
 constexpr int kPhiCluster = 8;       // CTAs per single-RHS cluster (portable size)
 constexpr int kPhiClusterWide = 16;  // ... when the device can co-schedule this many (non-portable)

@@ -169,8 +169,8 @@ constexpr int kBlkFreshOff = kBlkInvOff + kBlkInvBytes;
 #ifndef PHI_BLK_SOLVERS
 #define PHI_BLK_SOLVERS 2
 #endif
-constexpr int kBlkSolvers = PHI_BLK_SOLVERS;   // solver warps in rotation
-constexpr int kBlkMaxParts = 8 - kBlkSolvers;  // worker warps
+constexpr int kBlkSolvers = PHI_BLK_SOLVERS;                  // solver warps in rotation
+constexpr int kBlkMaxParts = PHI_THREADS / 32 - kBlkSolvers;  // worker warps
 constexpr int kBlkFresh = 1;     // fresh distance F: columns of block k-1 (folded into G_k)
 struct BlkStream {
     std::vector<unsigned char> stream;

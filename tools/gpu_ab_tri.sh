@@ -1,8 +1,8 @@
-# A/B: block inverse stored as its lower triangle (PHI_BLK_TRI, _lib_tri) vs the default build
+# A/B of block-sweep variants against the default build: lower-triangle inverse
+# (tri), 9 / 10 / 12 warps per CTA with 3 / 4 / 4 / 6 solver warps
 cd $GRAFT_REPO_ROOT
-for rep in 1 2; do
-for v in "" tri; do
-  PHI_VARIANT=$v python tools/ab_variant.py c2 3 >> gpurun_out/ab_tri.log 2>&1
-  PHI_VARIANT=$v python tools/ab_variant.py c3 2 1 >> gpurun_out/ab_tri.log 2>&1
-done; done
-PHI_VARIANT=tri timeout 900 python -m pytest tests/test_gpu_fast.py tests/test_gpu_determinism.py -x -q > gpurun_out/ab_tri_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tri_pytest.log
+for v in "" tri w9 w10 w12 w12s6; do
+  PHI_VARIANT=$v timeout 300 python tools/ab_variant.py c2 3 >> gpurun_out/ab.log 2>&1
+  PHI_VARIANT=$v timeout 300 python tools/ab_variant.py c3 2 1 >> gpurun_out/ab.log 2>&1
+done
+PHI_VARIANT="" timeout 300 python tools/ab_variant.py c2 3 >> gpurun_out/ab.log 2>&1
