@@ -146,8 +146,9 @@ TriStream make_tri_stream(const TriPlan& p, bool fast);
 /// One block = one fetch unit (one cp.async.bulk):
 ///   header int32[4]: mo (old slots per part), 0, bytes, mf (groups of four column pairs of G_k)
 ///   rows   int32[32]                 at 16 (-1 on padding lanes)
-///   inv    double[16][32][2]         at 144: entries (L, 2p), (L, 2p+1) of
-///                                    B_k^{-1} at (p * 32 + L) * 16 bytes
+///   inv    lower triangle of B_k^{-1} at 144, 4352 bytes: entries (L, 2p),
+///                                    (L, 2p+1) for L >= 2p at (p (31 - p) + L) * 16
+///                                    bytes (PHI_BLK_TRI = 0: the full double[16][32][2])
 ///   G      double[4 mf][32][2]       at kBlkFreshOff: pair q of lane L holds
 ///                                    G_k(L, 30 - 2q), G_k(L, 31 - 2q)
 ///   old    per part q: cols int32[mo][32], vals double[mo][32] at
@@ -161,7 +162,7 @@ constexpr int kBlkInvOff = 144;
 /// at slot p (31 - p) + L (16 bytes each; 272 slots = 4352 bytes instead of
 /// 8192); lanes above the diagonal load nothing and use exact zeros.
 #ifndef PHI_BLK_TRI
-#define PHI_BLK_TRI 0
+#define PHI_BLK_TRI 1
 #endif
 constexpr int kBlkTri = PHI_BLK_TRI;
 constexpr int kBlkInvBytes = kBlkTri ? 16 * 272 : 8 * kBlkRows * kBlkRows;

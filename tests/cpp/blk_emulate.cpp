@@ -83,7 +83,17 @@ static void run_blk(const BlkStream& bs, std::vector<double>& x, const std::vect
         const double* gv = reinterpret_cast<const double*>(fr);
         for (int l = 0; l < 32; ++l) {
             z[l] = 0.0;
-            for (int j = 0; j < 32; ++j) z[l] += iv[((j / 2) * 32 + l) * 2 + (j & 1)] * t[j];
+            // the inverse: full double[16][32][2], or (kBlkTri) its lower triangle -- column pair
+            // p keeps the lanes l >= 2 p at slot p (31 - p) + l, the rest are exact zeros
+            for (int j = 0; j < 32; ++j) {
+                const int pj = j / 2;
+                double v = 0.0;
+                if (!kBlkTri)
+                    v = iv[(pj * 32 + l) * 2 + (j & 1)];
+                else if (l >= 2 * pj)
+                    v = iv[(pj * (31 - pj) + l) * 2 + (j & 1)];
+                z[l] += v * t[j];
+            }
             // folded coupling: minus G_k times the last 8 mf values of block k-1
             for (int q = 0; q < 4 * mf; ++q)
                 z[l] -= gv[(q * 32 + l) * 2] * zprev[30 - 2 * q] + gv[(q * 32 + l) * 2 + 1] * zprev[31 - 2 * q];
