@@ -2,6 +2,7 @@
 
   python tools/ncu_summary.py launches <launches.csv>      per-kernel share of GPU time
   python tools/ncu_summary.py full <report.ncu-rep>        key metrics of a --set full capture
+  python tools/ncu_summary.py raw <raw.csv>                the same from `ncu -i .. --page raw --csv` output
 """
 import csv
 import io
@@ -39,9 +40,12 @@ WANT = [
 ]
 
 
-def full(path):
-    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
+def full(path, raw_csv=False):
+    if raw_csv:
+        txt = open(path).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = [r for r in csv.reader(io.StringIO(txt)) if len(r) > 10]
     hdr, units, data = rows[0], rows[1], rows[2:]
     res = []
     for r in data:
@@ -65,4 +69,4 @@ def full(path):
 
 if __name__ == "__main__":
     kind, path = sys.argv[1], sys.argv[2]
-    print(json.dumps(launches(path) if kind == "launches" else full(path), indent=1))
+    print(json.dumps(launches(path) if kind == "launches" else full(path, raw_csv=kind == "raw"), indent=1))
