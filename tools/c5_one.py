@@ -1,5 +1,5 @@
 """Developer helper for ncu captures: one SpMV / SpMM launch set at a config-5
-shape.  python tools/c5_one.py p B"""
+shape, or (third argument 1) one V(1,1) cycle.  python tools/c5_one.py p B [which]"""
 import os
 import sys
 
@@ -11,4 +11,5 @@ p, b = int(sys.argv[1]), int(sys.argv[2])
 E.lib().phi_set_device(0)
 d = P.SpatialDiscretization.build(p, 8)
 h = P.PMultigridHierarchy(d, 1e-4)
-print(p, b, h.time_kernel(0, b, reps=2, flush_l2=1))
+which = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+print(p, b, which, h.time_kernel(which, b, reps=2, flush_l2=1))
